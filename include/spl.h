@@ -1,0 +1,164 @@
+/*
+ * spl.h — C ABI of the B200 sequence-parallel transformer layer (libspl.so).
+ *
+ * Drop-in for the hot path of the reference `actplan` library (arXiv 2205.05198):
+ * one pre-LN GPT layer, forward + backward, under Megatron tensor + sequence parallelism
+ * with none / selective / full activation recomputation, plus the activation-memory
+ * accountant. Every entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no C++ or torch types.
+ *  - Every function returns an int status: SPL_OK, or a code mapped 1:1 from the
+ *    reference's exceptions (std::invalid_argument -> SPL_EINVAL, std::domain_error ->
+ *    SPL_EDOMAIN) plus CUDA / NCCL failures. spl_last_error() gives the message
+ *    (thread-local).
+ *  - Tensors follow the reference layouts: activations {s, b, h} row-major, sequence
+ *    shards are contiguous axis-0 chunks {s/t, b, h}; weights [in, out] row-major (y = x·W);
+ *    parameters packed in LayerParams::named_tensors() order (block.cpp:293-298).
+ *  - A handle owns t "local ranks": t simulated ranks on one device (spl_create_local —
+ *    the reference's simulated-rank harness, collectives as device copies/ordered sums)
+ *    or exactly one rank of a t-way NCCL group, one process per GPU (spl_create_nccl).
+ *    Array arguments indexed by local rank have spl_local_ranks() entries.
+ *  - A handle is not re-entrant; distinct handles may be used from distinct threads.
+ */
+#ifndef SPL_H
+#define SPL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SPL_OK = 0,
+  SPL_EINVAL = 1,  /* std::invalid_argument (block.cpp:518-534, 626-635; collectives.cpp:21-28) */
+  SPL_EDOMAIN = 2, /* std::domain_error: non-finite layer output (block.cpp:454-456, 596-598)  */
+  SPL_ECUDA = 3,
+  SPL_ENCCL = 4,
+  SPL_ESTATE = 5   /* backward without a matching forward ("missing saved forward state")     */
+};
+
+/* RecomputeKind order of config.hpp:51 (None, Full, Selective). */
+enum { SPL_RECOMPUTE_NONE = 0, SPL_RECOMPUTE_FULL = 1, SPL_RECOMPUTE_SELECTIVE = 2 };
+enum { SPL_DTYPE_F32 = 0, SPL_DTYPE_BF16 = 1 };
+
+/* BlockConfig (block.hpp:28-42) + RecomputeStrategy (config.hpp:53-70) + ByteConvention
+ * (config.hpp:74-80) + execution dtype. */
+typedef struct spl_layer_desc {
+  int64_t heads, hidden, seq, batch;
+  double dropout_p;
+  int32_t causal;
+  uint64_t seed;
+  uint32_t layer_index, microbatch;
+  double ln_eps;
+  int32_t recompute;         /* SPL_RECOMPUTE_* */
+  int32_t sequence_parallel; /* 1: g/ḡ = all-gather/reduce-scatter; 0: f/f̄ = all-reduce */
+  int32_t dtype;             /* SPL_DTYPE_*: storage/GEMM type; accumulation always fp32 */
+  int32_t check_finite;      /* 1: forward fails with SPL_EDOMAIN on non-finite y (reference) */
+  int64_t act_bytes, mask_bytes; /* ByteConvention for the ledger/accountant (2, 1 default) */
+} spl_layer_desc;
+
+typedef struct spl_handle spl_handle;
+
+/* Fill a desc with the reference defaults (BlockConfig{} + ByteConvention{}). */
+void spl_desc_default(spl_layer_desc* d);
+
+/* t simulated ranks on one CUDA device (the reference's in-process harness,
+ * seqpar_block_forward(x_shards, params, t, cfg), block.cpp:512). */
+int spl_create_local(const spl_layer_desc* d, int device, int t, spl_handle** out);
+/* One rank of a t-way tensor-parallel group over NCCL (one process per GPU). `nccl_id` is the
+ * 128-byte ncclUniqueId from spl_nccl_unique_id() on rank 0, distributed by the caller. */
+int spl_nccl_unique_id(unsigned char id_out[128]);
+int spl_create_nccl(const spl_layer_desc* d, int device, int t, int rank,
+                    const unsigned char nccl_id[128], spl_handle** out);
+int spl_destroy(spl_handle* h);
+int spl_local_ranks(const spl_handle* h);
+const char* spl_last_error(void);
+
+/* Parameters. Replaces passing `const LayerParams&` (block.hpp:47-59) to every call:
+ * the full-layout fp64 params are sliced per rank (shard_params, block.cpp:122-135) and
+ * cast once. packed_f64 holds 12h²+13h doubles in named_tensors() order. */
+int spl_load_params(spl_handle* h, const double* packed_f64);
+/* LayerParams::random(cfg, seed) generated on the device, bit-identical to the host
+ * values before the cast (block.cpp:234-265, rng.cpp:59-66); each rank makes only its shard. */
+int spl_init_params(spl_handle* h, uint64_t seed);
+
+/* Forward: seqpar_block_forward (block.cpp:512-602). x[r], y[r] are DEVICE pointers of the
+ * desc dtype, one per local rank: {s/t, b, h} with SP, {s, b, h} (replicated) without. */
+int spl_forward(spl_handle* h, const void* const* x, void* const* y);
+/* Backward: seqpar_block_backward (block.cpp:622-749). Consumes the state of the last
+ * forward. dy[r], dx[r] as above. Parameter gradients stay on the device (fp32). */
+int spl_backward(spl_handle* h, const void* const* dy, void* const* dx);
+/* One training step through HOST buffers (the end-to-end path): H2D of x and dy, forward,
+ * backward, D2H of y and dx. Buffers are the local ranks' shards concatenated in rank
+ * order, in the desc dtype; pinned host memory is used directly, pageable is staged. */
+int spl_step_host(spl_handle* h, const void* x_host, const void* dy_host, void* y_host,
+                  void* dx_host);
+
+/* Gradients assembled into the full fp64 layout (block.cpp:730-746). For an NCCL rank, only
+ * the rank's own shard of column/row-sharded tensors is filled (others left zero) and the
+ * replicated tensors hold the all-reduced values. */
+int spl_get_grads(spl_handle* h, double* packed_f64_out);
+/* One rank's w1 gradient shard [h, 4h/t] (SeqparBackward::w1_grad_shards, block.hpp:169). */
+int spl_get_w1_grad_shard(spl_handle* h, int local_rank, double* out);
+
+/* Host read of one saved activation (by ledger name) of a local rank, converted to fp64
+ * (masks as 0/1); for tests of the stored state and the recompute property. */
+int spl_get_saved(spl_handle* h, int local_rank, const char* name, double* out, int64_t n);
+/* Attention interior recomputed from the saved Q/K by the device kernel, full fp64
+ * {local_heads, b, s, s} x3 (softmax_out, dropout_mask, dropout_out): the
+ * attention_interior() call of the reference's recompute property (verify.cpp:253-283). */
+int spl_attention_interior(spl_handle* h, int local_rank, double* out3);
+
+/* ActivationLedger (block.hpp:61-73): one entry per saved tensor of the last forward.
+ * bytes = elements × the desc ByteConvention width (the reference's counting);
+ * physical_bytes = what the device actually holds for it. */
+typedef struct {
+  char name[32];
+  int64_t elements;
+  int64_t bytes;
+  int64_t physical_bytes;
+} spl_ledger_entry;
+int spl_ledger(spl_handle* h, int local_rank, spl_ledger_entry* entries, int* n_inout);
+/* Totals per local rank: reference-convention ledger bytes, physical saved bytes, and the
+ * saved bytes the reference does not count (LN statistics, softmax LSE). */
+int spl_saved_bytes(spl_handle* h, int local_rank, int64_t* ledger_bytes,
+                    int64_t* physical_bytes, int64_t* uncounted_bytes);
+
+/* CommLog (collectives.hpp:28-52): counts and modelled ring elements per tag.
+ * tag 0 Schedule (g/ḡ), 1 Regather (Y_i^s re-gathers), 2 GradSync, 3 Recompute (the forward
+ * re-run of full recomputation). counters[tag*4 + {0 AG, 1 RS, 2 AR, 3 ring_elements}]. */
+int spl_comm_log(spl_handle* h, int64_t counters[16]);
+int spl_comm_log_reset(spl_handle* h);
+
+/* Activation-memory accountant: per_layer_bytes / _exact (activation_memory.cpp:54-82),
+ * kind = SPL_RECOMPUTE_*. Floor-once exact arithmetic. */
+int spl_per_layer_bytes(int64_t a, int64_t h, int64_t s, int64_t b, int64_t t, int kind,
+                        int sequence_parallel, int64_t act_bytes, int64_t mask_bytes,
+                        int64_t* bytes_out);
+int spl_per_layer_bytes_exact(int64_t a, int64_t h, int64_t s, int64_t b, int64_t t, int kind,
+                              int sequence_parallel, int64_t act_bytes, int64_t mask_bytes,
+                              int64_t* num, int64_t* den);
+
+/* Device timing on the handle's compute stream (CUDA events; synchronizes at stop). */
+int spl_timer_start(spl_handle* h);
+int spl_timer_stop(spl_handle* h, float* ms);
+int spl_synchronize(spl_handle* h);
+/* Per-kernel-class device time: when enabled, every launch is bracketed by CUDA events on
+ * its own stream. Classes: 0 gemm, 1 attention, 2 layernorm/elementwise, 3 collective,
+ * 4 other. ms[c], launches[c], flops[c] (algorithmic FLOPs), bytes[c] (algorithmic bytes). */
+int spl_profile_enable(spl_handle* h, int on);
+int spl_profile_read(spl_handle* h, double ms[5], int64_t launches[5], double flops[5],
+                     double bytes[5]);
+/* Number of kernel launches of this library recorded since the last reset. */
+int spl_launch_count(spl_handle* h, int64_t* count, int reset);
+
+/* Capture forward+backward into CUDA graphs after the first call (1) or run eagerly (0). */
+int spl_set_graphs(spl_handle* h, int on);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

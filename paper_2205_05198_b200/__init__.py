@@ -1,0 +1,7 @@
+"""B200-native sequence-parallel transformer layer with selective recomputation
+(arXiv 2205.05198 hot path). The compute lives in libspl.so (sm_100a CUDA + NCCL) behind the
+C ABI of include/spl.h; this package is the Python mirror of the reference's seqpar API."""
+from ._lib import lib, header_symbols, SplError, SplStateError  # noqa: F401
+from .seqpar import (BlockConfig, SeqparLayer, SeqparForward, SeqparBackward,  # noqa: F401
+                     seqpar_block_forward, seqpar_block_backward, per_layer_bytes,
+                     per_layer_bytes_exact, param_count, PARAM_NAMES)

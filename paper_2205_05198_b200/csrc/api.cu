@@ -1,0 +1,307 @@
+// extern "C" boundary of libspl (include/spl.h). Maps spl::Error and std exceptions to the
+// reference's error classes: std::invalid_argument -> SPL_EINVAL, std::domain_error ->
+// SPL_EDOMAIN (block.cpp:518-534, 596-598), plus CUDA / NCCL / state errors.
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+
+#include "layer.hpp"
+
+struct spl_handle {
+  std::unique_ptr<spl::LayerBase> layer;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  int device = 0;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return SPL_OK;
+  } catch (const spl::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return SPL_EINVAL;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return SPL_EDOMAIN;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SPL_ECUDA;
+  }
+}
+
+void check_handle(const spl_handle* h) {
+  if (h == nullptr || !h->layer) spl::raise(SPL_EINVAL, "null handle");
+}
+
+spl_handle* make_handle(const spl_layer_desc* d, int device, std::unique_ptr<spl::Comm> comm) {
+  auto* h = new spl_handle();
+  h->device = device;
+  try {
+    SPL_CUDA(cudaSetDevice(device));
+    h->layer = spl::make_layer(*d, device, std::move(comm));
+    SPL_CUDA(cudaEventCreate(&h->t0));
+    SPL_CUDA(cudaEventCreate(&h->t1));
+  } catch (...) {
+    delete h;
+    throw;
+  }
+  return h;
+}
+}  // namespace
+
+extern "C" {
+
+const char* spl_last_error(void) { return g_err.c_str(); }
+
+void spl_desc_default(spl_layer_desc* d) {
+  std::memset(d, 0, sizeof(*d));
+  d->seed = 42;
+  d->microbatch = 1;
+  d->ln_eps = 1e-5;
+  d->recompute = SPL_RECOMPUTE_NONE;
+  d->sequence_parallel = 1;
+  d->dtype = SPL_DTYPE_BF16;
+  d->check_finite = 1;
+  d->act_bytes = 2;
+  d->mask_bytes = 1;
+}
+
+int spl_create_local(const spl_layer_desc* d, int device, int t, spl_handle** out) {
+  return guard([&] {
+    spl::require(d != nullptr && out != nullptr, "null argument");
+    spl::require(t >= 1, "t must be >= 1");
+    *out = make_handle(d, device, spl::make_local_comm(t));
+  });
+}
+
+int spl_nccl_unique_id(unsigned char id_out[128]) {
+  return guard([&] {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) spl::raise(SPL_ENCCL, "ncclGetUniqueId failed");
+    std::memcpy(id_out, id.internal, 128);
+  });
+}
+
+int spl_create_nccl(const spl_layer_desc* d, int device, int t, int rank,
+                    const unsigned char nccl_id[128], spl_handle** out) {
+  return guard([&] {
+    spl::require(d != nullptr && out != nullptr && nccl_id != nullptr, "null argument");
+    SPL_CUDA(cudaSetDevice(device));
+    *out = make_handle(d, device, spl::make_nccl_comm(t, rank, nccl_id));
+  });
+}
+
+int spl_destroy(spl_handle* h) {
+  return guard([&] {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    h->layer.reset();
+    if (h->t0) cudaEventDestroy(h->t0);
+    if (h->t1) cudaEventDestroy(h->t1);
+    delete h;
+  });
+}
+
+int spl_local_ranks(const spl_handle* h) { return h && h->layer ? h->layer->local_ranks() : 0; }
+
+int spl_load_params(spl_handle* h, const double* p) {
+  return guard([&] {
+    check_handle(h);
+    spl::require(p != nullptr, "null params");
+    h->layer->load_params(p);
+  });
+}
+
+int spl_init_params(spl_handle* h, uint64_t seed) {
+  return guard([&] {
+    check_handle(h);
+    h->layer->init_params(seed);
+  });
+}
+
+int spl_forward(spl_handle* h, const void* const* x, void* const* y) {
+  return guard([&] {
+    check_handle(h);
+    spl::require(x != nullptr && y != nullptr, "expected one input shard per rank");
+    h->layer->forward(x, y);
+  });
+}
+
+int spl_backward(spl_handle* h, const void* const* dy, void* const* dx) {
+  return guard([&] {
+    check_handle(h);
+    spl::require(dy != nullptr && dx != nullptr, "expected one gradient shard per rank");
+    h->layer->backward(dy, dx);
+  });
+}
+
+int spl_step_host(spl_handle* h, const void* x, const void* dy, void* y, void* dx) {
+  return guard([&] {
+    check_handle(h);
+    spl::require(x && dy && y && dx, "null host buffer");
+    h->layer->step_host(x, dy, y, dx);
+  });
+}
+
+int spl_get_grads(spl_handle* h, double* out) {
+  return guard([&] {
+    check_handle(h);
+    h->layer->get_grads(out);
+  });
+}
+
+int spl_get_w1_grad_shard(spl_handle* h, int r, double* out) {
+  return guard([&] {
+    check_handle(h);
+    h->layer->get_w1_grad_shard(r, out);
+  });
+}
+
+int spl_get_saved(spl_handle* h, int r, const char* name, double* out, int64_t n) {
+  return guard([&] {
+    check_handle(h);
+    spl::require(name != nullptr && out != nullptr, "null argument");
+    h->layer->get_saved(r, name, out, n);
+  });
+}
+
+int spl_attention_interior(spl_handle* h, int r, double* out3) {
+  return guard([&] {
+    check_handle(h);
+    h->layer->attention_interior(r, out3);
+  });
+}
+
+int spl_ledger(spl_handle* h, int r, spl_ledger_entry* entries, int* n) {
+  return guard([&] {
+    check_handle(h);
+    spl::require(n != nullptr, "null count");
+    spl::require(r >= 0 && r < h->layer->local_ranks(), "local rank out of range");
+    auto items = h->layer->ledger(r);
+    const int cap = *n;
+    *n = (int)items.size();
+    if (entries == nullptr) return;
+    for (int i = 0; i < (int)items.size() && i < cap; ++i) {
+      std::memset(entries[i].name, 0, sizeof(entries[i].name));
+      std::strncpy(entries[i].name, items[i].name.c_str(), sizeof(entries[i].name) - 1);
+      entries[i].elements = items[i].elements;
+      entries[i].bytes = items[i].bytes;
+      entries[i].physical_bytes = items[i].physical;
+    }
+  });
+}
+
+int spl_saved_bytes(spl_handle* h, int r, int64_t* lb, int64_t* pb, int64_t* ub) {
+  return guard([&] {
+    check_handle(h);
+    spl::require(r >= 0 && r < h->layer->local_ranks(), "local rank out of range");
+    h->layer->saved_bytes(r, lb, pb, ub);
+  });
+}
+
+int spl_comm_log(spl_handle* h, int64_t c[16]) {
+  return guard([&] {
+    check_handle(h);
+    auto& comm = h->layer->comm();
+    for (int tag = 0; tag < 4; ++tag) {
+      c[tag * 4 + 0] = comm.counters[tag].all_gathers;
+      c[tag * 4 + 1] = comm.counters[tag].reduce_scatters;
+      c[tag * 4 + 2] = comm.counters[tag].all_reduces;
+      c[tag * 4 + 3] = comm.counters[tag].ring_elements;
+    }
+  });
+}
+
+int spl_comm_log_reset(spl_handle* h) {
+  return guard([&] {
+    check_handle(h);
+    auto& comm = h->layer->comm();
+    for (auto& c : comm.counters) c = spl::CommCounters{};
+  });
+}
+
+int spl_per_layer_bytes(int64_t a, int64_t hh, int64_t s, int64_t b, int64_t t, int kind,
+                        int sp, int64_t act, int64_t mask, int64_t* out) {
+  return guard([&] {
+    __int128 n, d;
+    if (spl::per_layer_bytes_exact(a, hh, s, b, t, kind, sp, act, mask, &n, &d))
+      spl::raise(SPL_EINVAL, "invalid configuration");
+    const __int128 q = n / d;
+    if (q > (__int128)INT64_MAX) spl::raise(SPL_EINVAL, "value does not fit in 64-bit integer");
+    *out = (int64_t)q;
+  });
+}
+
+int spl_per_layer_bytes_exact(int64_t a, int64_t hh, int64_t s, int64_t b, int64_t t, int kind,
+                              int sp, int64_t act, int64_t mask, int64_t* num, int64_t* den) {
+  return guard([&] {
+    __int128 n, d;
+    if (spl::per_layer_bytes_exact(a, hh, s, b, t, kind, sp, act, mask, &n, &d))
+      spl::raise(SPL_EINVAL, "invalid configuration");
+    if (n > (__int128)INT64_MAX) spl::raise(SPL_EINVAL, "value does not fit in 64-bit integer");
+    *num = (int64_t)n;
+    *den = (int64_t)d;
+  });
+}
+
+int spl_timer_start(spl_handle* h) {
+  return guard([&] {
+    check_handle(h);
+    SPL_CUDA(cudaEventRecord(h->t0, h->layer->stream()));
+  });
+}
+
+int spl_timer_stop(spl_handle* h, float* ms) {
+  return guard([&] {
+    check_handle(h);
+    SPL_CUDA(cudaEventRecord(h->t1, h->layer->stream()));
+    SPL_CUDA(cudaEventSynchronize(h->t1));
+    SPL_CUDA(cudaEventElapsedTime(ms, h->t0, h->t1));
+  });
+}
+
+int spl_synchronize(spl_handle* h) {
+  return guard([&] {
+    check_handle(h);
+    SPL_CUDA(cudaStreamSynchronize(h->layer->stream()));
+  });
+}
+
+int spl_profile_enable(spl_handle* h, int on) {
+  return guard([&] {
+    check_handle(h);
+    h->layer->set_profile(on != 0);
+  });
+}
+
+int spl_profile_read(spl_handle* h, double ms[5], int64_t n[5], double fl[5], double by[5]) {
+  return guard([&] {
+    check_handle(h);
+    h->layer->read_profile(ms, n, fl, by);
+  });
+}
+
+int spl_launch_count(spl_handle* h, int64_t* count, int reset) {
+  return guard([&] {
+    check_handle(h);
+    *count = h->layer->launch_count(reset != 0);
+  });
+}
+
+int spl_set_graphs(spl_handle* h, int on) {
+  return guard([&] {
+    check_handle(h);
+    h->layer->set_graphs(on != 0);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,57 @@
+// Collectives of the tensor+sequence-parallel layer (the g / ḡ transitions and their duals,
+// collectives.hpp:57-62 of the reference), behind one interface with two transports:
+//   LocalComm — t simulated ranks on one device (the reference's in-process harness); sums in
+//               rank order 0..t-1 with fp32 accumulation (collectives.cpp:40-46).
+//   NcclComm  — one rank per process/GPU over NCCL (NVLink 5 / NVSwitch on a B200 node).
+// Sequence shards are contiguous axis-0 chunks of {s, b, h}, so every collective is a flat
+// buffer operation with no packing.
+#pragma once
+#include <nccl.h>
+
+#include <memory>
+#include <vector>
+
+#include "common.hpp"
+
+namespace spl {
+
+// CommTag of collectives.hpp:28 plus the forward re-run of full recomputation.
+enum CommTag : int { kSchedule = 0, kRegather = 1, kGradSync = 2, kRecompute = 3 };
+
+struct CommCounters {
+  int64_t all_gathers = 0, reduce_scatters = 0, all_reduces = 0, ring_elements = 0;
+};
+
+class Comm {
+ public:
+  virtual ~Comm() = default;
+  int t() const { return t_; }
+  int local() const { return local_; }
+  int rank0() const { return rank0_; }
+  // full[r] (t*n elements) = concat_q shard[q] (n elements each), every local rank r.
+  virtual void all_gather(const void* const* shard, void* const* full, int64_t n, DType dt,
+                          cudaStream_t st) = 0;
+  // shard[r] (n) = sum_q part[q][r*n .. (r+1)*n), for every local rank r.
+  virtual void reduce_scatter(const void* const* part, void* const* shard, int64_t n, DType dt,
+                              cudaStream_t st) = 0;
+  // buf[r] (n) = sum_q buf[q], in place.
+  virtual void all_reduce(void* const* buf, int64_t n, DType dt, cudaStream_t st) = 0;
+  virtual void all_reduce_f32(float* const* buf, int64_t n, cudaStream_t st) = 0;
+
+  void log(CommTag tag, int kind, int64_t logical_elems) {
+    CommCounters& c = counters[tag];
+    if (kind == 0) c.all_gathers++;
+    if (kind == 1) c.reduce_scatters++;
+    if (kind == 2) c.all_reduces++;
+    c.ring_elements += (kind == 2 ? 2 : 1) * (logical_elems / t_) * (t_ - 1);
+  }
+  CommCounters counters[4];
+
+ protected:
+  int t_ = 1, local_ = 1, rank0_ = 0;
+};
+
+std::unique_ptr<Comm> make_local_comm(int t);
+std::unique_ptr<Comm> make_nccl_comm(int t, int rank, const unsigned char id[128]);
+
+}  // namespace spl

@@ -1,0 +1,31 @@
+// GEMM dispatch: bf16 shapes the tcgen05 kernel can tile go to the tensor cores
+// (k_gemm_tc.cu); fp32 (the exact-fp32 execution dtype) and unaligned shapes use the SIMT
+// kernel (k_gemm_simt.cu). Both are on-device; there is no host path.
+#include "kernels.hpp"
+
+namespace spl::k {
+
+template <typename T>
+void gemm_simt(const GemmArgs& a, cudaStream_t st);
+bool gemm_tc_supported(const GemmArgs& a);
+void gemm_tc(const GemmArgs& a, cudaStream_t st);
+
+template <>
+void gemm<float>(const GemmArgs& a, cudaStream_t st) {
+  gemm_simt<float>(a, st);
+}
+template <>
+void gemm<bf16>(const GemmArgs& a, cudaStream_t st) {
+  if (gemm_tc_supported(a)) gemm_tc(a, st);
+  else gemm_simt<bf16>(a, st);
+}
+template <>
+int gemm_backend<float>(const GemmArgs&) {
+  return 0;
+}
+template <>
+int gemm_backend<bf16>(const GemmArgs& a) {
+  return gemm_tc_supported(a) ? 1 : 0;
+}
+
+}  // namespace spl::k

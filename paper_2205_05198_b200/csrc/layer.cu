@@ -1,0 +1,912 @@
+// SpLayer implementation. The schedule below is the reference's seqpar_block_forward /
+// seqpar_block_backward (/root/reference/proj/core/src/seqpar/block.cpp:512-749) with:
+//  - per-rank work as device kernels (LN, fused bias-dropout-residual(+LN2), tcgen05 GEMMs
+//    with fused bias / bias+GELU / GELU-backward epilogues, flash-style attention),
+//  - g / ḡ (and duals) as all-gather / reduce-scatter on contiguous sequence chunks,
+//  - the three recompute regimes executed (the reference only accounts for them):
+//      none      — stores the attention interior (softmax_out, mask, dropout_out),
+//      selective — stores Q/K/V and a per-row LSE; backward recomputes QKᵀ, softmax, dropout,
+//      full      — stores only the layer input; backward re-runs the forward first,
+//  - SP off (TP baseline): LN/dropout regions replicated, f/f̄ as all-reduces.
+// Local ranks r of a handle map to global TP ranks rank0 + r.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <type_traits>
+
+#include "layer.hpp"
+
+namespace spl {
+
+namespace {
+
+using k::Epi;
+using k::GemmArgs;
+using k::Major;
+
+constexpr int kChunkRows = 64;
+
+struct Alloc {
+  void* ptr;
+  size_t bytes;
+  int cat;
+  int rank;
+};
+
+template <typename T>
+class Layer final : public LayerBase {
+ public:
+  Layer(const spl_layer_desc& d, int device, std::unique_ptr<Comm> comm)
+      : d_(d), dev_(device), comm_(std::move(comm)) {
+    t_ = comm_->t();
+    L_ = comm_->local();
+    rank0_ = comm_->rank0();
+    s_ = d.seq;
+    b_ = d.batch;
+    h_ = d.hidden;
+    a_ = d.heads;
+    validate();
+    hd_ = h_ / a_;
+    lh_ = a_ / t_;
+    lw_ = h_ / t_;
+    fw_ = 4 * h_ / t_;
+    RF_ = s_ * b_;
+    sp_ = d.sequence_parallel != 0;
+    RL_ = sp_ ? RF_ / t_ : RF_;
+    kind_ = d.recompute;
+    scale_ = (float)(1.0 / std::sqrt((double)hd_));
+    k_soft_ = make_drop_key(d.seed, d.layer_index, kSoftmaxDrop, d.microbatch, d.dropout_p);
+    k_attn_ = make_drop_key(d.seed, d.layer_index, kAttnOutDrop, d.microbatch, d.dropout_p);
+    k_mlp_ = make_drop_key(d.seed, d.layer_index, kMlpDrop, d.microbatch, d.dropout_p);
+    SPL_CUDA(cudaSetDevice(dev_));
+    SPL_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    SPL_CUDA(cudaEventCreate(&tstart_));
+    SPL_CUDA(cudaEventCreate(&tstop_));
+    allocate();
+  }
+
+  ~Layer() override {
+    cudaSetDevice(dev_);
+    cudaStreamSynchronize(st_);
+    for (auto& a : allocs_) cudaFree(a.ptr);
+    if (pinned_) cudaFreeHost(pinned_);
+    for (auto& e : evpool_) cudaEventDestroy(e);
+    cudaEventDestroy(tstart_);
+    cudaEventDestroy(tstop_);
+    cudaStreamDestroy(st_);
+  }
+
+  int local_ranks() const override { return L_; }
+  Comm& comm() override { return *comm_; }
+  cudaStream_t stream() const override { return st_; }
+
+  // ------------------------------------------------------------------ params
+  void load_params(const double* P) override {
+    SPL_CUDA(cudaSetDevice(dev_));
+    const int64_t h = h_;
+    // named_tensors() offsets (block.cpp:293-298)
+    const int64_t o_wq = 0, o_wk = h * h, o_wv = 2 * h * h, o_bq = 3 * h * h, o_bk = o_bq + h,
+                  o_bv = o_bk + h, o_wo = o_bv + h, o_bo = o_wo + h * h, o_w1 = o_bo + h,
+                  o_b1 = o_w1 + 4 * h * h, o_w2 = o_b1 + 4 * h, o_b2 = o_w2 + 4 * h * h,
+                  o_g1 = o_b2 + h, o_be1 = o_g1 + h, o_g2 = o_be1 + h, o_be2 = o_g2 + h;
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      const int64_t g = rank0_ + r;
+      std::vector<T> w((size_t)(h * 3 * lw_));
+      for (int which = 0; which < 3; ++which) {
+        const double* src = P + (which == 0 ? o_wq : which == 1 ? o_wk : o_wv);
+        for (int64_t i = 0; i < h; ++i)
+          for (int64_t j = 0; j < lw_; ++j)
+            w[(size_t)(i * 3 * lw_ + which * lw_ + j)] = cvt(src[i * h + g * lw_ + j]);
+      }
+      up(R.wqkv, w);
+      std::vector<float> bq((size_t)(3 * lw_));
+      for (int which = 0; which < 3; ++which) {
+        const double* src = P + (which == 0 ? o_bq : which == 1 ? o_bk : o_bv);
+        for (int64_t j = 0; j < lw_; ++j) bq[(size_t)(which * lw_ + j)] = (float)src[g * lw_ + j];
+      }
+      up(R.bqkv, bq);
+      w.assign((size_t)(lw_ * h), T());
+      for (int64_t i = 0; i < lw_; ++i)
+        for (int64_t j = 0; j < h; ++j) w[(size_t)(i * h + j)] = cvt(P[o_wo + (g * lw_ + i) * h + j]);
+      up(R.wo, w);
+      w.assign((size_t)(h * fw_), T());
+      for (int64_t i = 0; i < h; ++i)
+        for (int64_t j = 0; j < fw_; ++j)
+          w[(size_t)(i * fw_ + j)] = cvt(P[o_w1 + i * 4 * h + g * fw_ + j]);
+      up(R.w1, w);
+      w.assign((size_t)(fw_ * h), T());
+      for (int64_t i = 0; i < fw_; ++i)
+        for (int64_t j = 0; j < h; ++j) w[(size_t)(i * h + j)] = cvt(P[o_w2 + (g * fw_ + i) * h + j]);
+      up(R.w2, w);
+      auto upf = [&](float* dst, int64_t off, int64_t n) {
+        std::vector<float> v((size_t)n);
+        for (int64_t j = 0; j < n; ++j) v[(size_t)j] = (float)P[off + j];
+        up(dst, v);
+      };
+      std::vector<float> b1((size_t)fw_);
+      for (int64_t j = 0; j < fw_; ++j) b1[(size_t)j] = (float)P[o_b1 + g * fw_ + j];
+      up(R.b1, b1);
+      upf(R.bo, o_bo, h);
+      upf(R.b2, o_b2, h);
+      upf(R.g1, o_g1, h);
+      upf(R.be1, o_be1, h);
+      upf(R.g2, o_g2, h);
+      upf(R.be2, o_be2, h);
+    }
+    SPL_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  void init_params(uint64_t seed) override {
+    SPL_CUDA(cudaSetDevice(dev_));
+    const int64_t h = h_;
+    const double ws = 1.0 / std::sqrt((double)h);
+    auto key = [&](int salt) { return hash_counter(seed, (uint64_t)salt); };
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      const int64_t g = rank0_ + r;
+      for (int which = 0; which < 3; ++which) {
+        k::init_uniform<T>(R.wqkv + which * lw_, h, lw_, 3 * lw_, 0, g * lw_, h, key(1 + which),
+                           -ws, ws, 0.0, st_);
+        k::init_uniform<float>(R.bqkv + which * lw_, 1, lw_, lw_, 0, g * lw_, h, key(4 + which),
+                               -0.1, 0.1, 0.0, st_);
+      }
+      k::init_uniform<T>(R.wo, lw_, h, h, g * lw_, 0, h, key(7), -ws, ws, 0.0, st_);
+      k::init_uniform<float>(R.bo, 1, h, h, 0, 0, h, key(8), -0.1, 0.1, 0.0, st_);
+      k::init_uniform<T>(R.w1, h, fw_, fw_, 0, g * fw_, 4 * h, key(9), -ws, ws, 0.0, st_);
+      k::init_uniform<float>(R.b1, 1, fw_, fw_, 0, g * fw_, 4 * h, key(10), -0.1, 0.1, 0.0, st_);
+      k::init_uniform<T>(R.w2, fw_, h, h, g * fw_, 0, h, key(11), -ws, ws, 0.0, st_);
+      k::init_uniform<float>(R.b2, 1, h, h, 0, 0, h, key(12), -0.1, 0.1, 0.0, st_);
+      k::init_uniform<float>(R.g1, 1, h, h, 0, 0, h, key(13), -0.1, 0.1, 1.0, st_);
+      k::init_uniform<float>(R.be1, 1, h, h, 0, 0, h, key(14), -0.1, 0.1, 0.0, st_);
+      k::init_uniform<float>(R.g2, 1, h, h, 0, 0, h, key(15), -0.1, 0.1, 1.0, st_);
+      k::init_uniform<float>(R.be2, 1, h, h, 0, 0, h, key(16), -0.1, 0.1, 0.0, st_);
+    }
+    SPL_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  // ------------------------------------------------------------------ forward
+  void forward(const void* const* x, void* const* y) override {
+    SPL_CUDA(cudaSetDevice(dev_));
+    for (int r = 0; r < L_; ++r) {
+      require(x[r] != nullptr && y[r] != nullptr, "expected one input shard per rank");
+      SPL_CUDA(cudaMemcpyAsync(R_[r].x_s, x[r], (size_t)(RL_ * h_) * sizeof(T),
+                               cudaMemcpyDeviceToDevice, st_));
+    }
+    if (d_.check_finite) SPL_CUDA(cudaMemsetAsync(nonfinite_, 0, sizeof(int), st_));
+    std::vector<T*> ys(L_);
+    for (int r = 0; r < L_; ++r) ys[r] = static_cast<T*>(y[r]);
+    run_forward(ys.data(), kSchedule, d_.check_finite ? nonfinite_ : nullptr);
+    if (d_.check_finite) {
+      int flag = 0;
+      SPL_CUDA(cudaMemcpyAsync(&flag, nonfinite_, sizeof(int), cudaMemcpyDeviceToHost, st_));
+      SPL_CUDA(cudaStreamSynchronize(st_));
+      if (flag) {
+        have_fwd_ = false;
+        raise(2, "seqpar_block_forward produced non-finite values");
+      }
+    }
+    have_fwd_ = true;
+  }
+
+  void backward(const void* const* dy, void* const* dx) override {
+    SPL_CUDA(cudaSetDevice(dev_));
+    if (!have_fwd_) raise(5, "missing saved forward state");
+    for (int r = 0; r < L_; ++r) require(dy[r] != nullptr && dx[r] != nullptr, "expected one gradient shard per rank");
+    if (kind_ == SPL_RECOMPUTE_FULL) {
+      // Full recomputation: only x_s survived; re-run the forward (with its collectives).
+      std::vector<T*> ys(L_);
+      for (int r = 0; r < L_; ++r) ys[r] = R_[r].y_re;
+      run_forward(ys.data(), kRecompute, nullptr);
+    }
+    run_backward(dy, dx);
+  }
+
+  void step_host(const void* x, const void* dy, void* y, void* dx) override {
+    SPL_CUDA(cudaSetDevice(dev_));
+    const size_t shard = (size_t)(RL_ * h_) * sizeof(T);
+    ensure_staging();
+    std::vector<const void*> xs(L_), dys(L_);
+    std::vector<void*> ysv(L_), dxs(L_);
+    for (int r = 0; r < L_; ++r) {
+      SPL_CUDA(cudaMemcpyAsync(stage_[4 * r + 0], static_cast<const char*>(x) + r * shard, shard,
+                               cudaMemcpyHostToDevice, st_));
+      SPL_CUDA(cudaMemcpyAsync(stage_[4 * r + 1], static_cast<const char*>(dy) + r * shard, shard,
+                               cudaMemcpyHostToDevice, st_));
+      xs[r] = stage_[4 * r + 0];
+      dys[r] = stage_[4 * r + 1];
+      ysv[r] = stage_[4 * r + 2];
+      dxs[r] = stage_[4 * r + 3];
+    }
+    forward(xs.data(), ysv.data());
+    backward(dys.data(), dxs.data());
+    for (int r = 0; r < L_; ++r) {
+      SPL_CUDA(cudaMemcpyAsync(static_cast<char*>(y) + r * shard, ysv[r], shard,
+                               cudaMemcpyDeviceToHost, st_));
+      SPL_CUDA(cudaMemcpyAsync(static_cast<char*>(dx) + r * shard, dxs[r], shard,
+                               cudaMemcpyDeviceToHost, st_));
+    }
+    SPL_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  // ------------------------------------------------------------------ read-back
+  void get_grads(double* P) override {
+    SPL_CUDA(cudaSetDevice(dev_));
+    SPL_CUDA(cudaStreamSynchronize(st_));
+    const int64_t h = h_;
+    const int64_t np = 12 * h * h + 13 * h;
+    std::memset(P, 0, sizeof(double) * (size_t)np);
+    const int64_t o_wq = 0, o_wk = h * h, o_wv = 2 * h * h, o_bq = 3 * h * h, o_bk = o_bq + h,
+                  o_bv = o_bk + h, o_wo = o_bv + h, o_bo = o_wo + h * h, o_w1 = o_bo + h,
+                  o_b1 = o_w1 + 4 * h * h, o_w2 = o_b1 + 4 * h, o_b2 = o_w2 + 4 * h * h,
+                  o_g1 = o_b2 + h, o_be1 = o_g1 + h, o_g2 = o_be1 + h, o_be2 = o_g2 + h;
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      const int64_t g = rank0_ + r;
+      auto wqkv = down(R.dwqkv, h * 3 * lw_);
+      for (int which = 0; which < 3; ++which) {
+        double* dst = P + (which == 0 ? o_wq : which == 1 ? o_wk : o_wv);
+        for (int64_t i = 0; i < h; ++i)
+          for (int64_t j = 0; j < lw_; ++j)
+            dst[i * h + g * lw_ + j] = wqkv[(size_t)(i * 3 * lw_ + which * lw_ + j)];
+      }
+      auto bqkv = down(R.dbqkv, 3 * lw_);
+      for (int which = 0; which < 3; ++which) {
+        double* dst = P + (which == 0 ? o_bq : which == 1 ? o_bk : o_bv);
+        for (int64_t j = 0; j < lw_; ++j) dst[g * lw_ + j] = bqkv[(size_t)(which * lw_ + j)];
+      }
+      auto wo = down(R.dwo, lw_ * h);
+      for (int64_t i = 0; i < lw_ * h; ++i) P[o_wo + g * lw_ * h + i] = wo[(size_t)i];
+      auto w1 = down(R.dw1, h * fw_);
+      for (int64_t i = 0; i < h; ++i)
+        for (int64_t j = 0; j < fw_; ++j) P[o_w1 + i * 4 * h + g * fw_ + j] = w1[(size_t)(i * fw_ + j)];
+      auto b1 = down(R.db1, fw_);
+      for (int64_t j = 0; j < fw_; ++j) P[o_b1 + g * fw_ + j] = b1[(size_t)j];
+      auto w2 = down(R.dw2, fw_ * h);
+      for (int64_t i = 0; i < fw_ * h; ++i) P[o_w2 + g * fw_ * h + i] = w2[(size_t)i];
+      if (r == 0) {
+        auto repl = down(R.repl, 6 * h);
+        const int64_t dst[6] = {o_bo, o_b2, o_g1, o_be1, o_g2, o_be2};
+        for (int kx = 0; kx < 6; ++kx)
+          for (int64_t j = 0; j < h; ++j) P[dst[kx] + j] = repl[(size_t)(kx * h + j)];
+      }
+    }
+  }
+
+  void get_w1_grad_shard(int r, double* out) override {
+    require(r >= 0 && r < L_, "local rank out of range");
+    SPL_CUDA(cudaStreamSynchronize(st_));
+    auto w1 = down(R_[r].dw1, h_ * fw_);
+    for (size_t i = 0; i < w1.size(); ++i) out[i] = w1[i];
+  }
+
+  void get_saved(int r, const std::string& name, double* out, int64_t n) override {
+    require(r >= 0 && r < L_, "local rank out of range");
+    SPL_CUDA(cudaSetDevice(dev_));
+    if (!have_fwd_) raise(5, "missing saved forward state");
+    Rank& R = R_[r];
+    const T* src = nullptr;
+    const uint8_t* msrc = nullptr;
+    int64_t cnt = 0, col = -1, width = 0, ld = 0;
+    if (name == "ln1_input") { src = R.x_s; cnt = RL_ * h_; }
+    else if (name == "qkv_input") { src = R.y1_s; cnt = RL_ * h_; }
+    else if (name == "query" || name == "key" || name == "value") {
+      src = R.qkv; cnt = RF_ * lw_; width = lw_; ld = 3 * lw_;
+      col = name == "query" ? 0 : name == "key" ? lw_ : 2 * lw_;
+    }
+    else if (name == "softmax_out" && R.sm) { src = R.sm; cnt = lh_ * b_ * s_ * s_; }
+    else if (name == "softmax_dropout_mask" && R.mask_i) { msrc = R.mask_i; cnt = lh_ * b_ * s_ * s_; }
+    else if (name == "softmax_dropout_out" && R.sd) { src = R.sd; cnt = lh_ * b_ * s_ * s_; }
+    else if (name == "attn_proj_input") { src = R.api; cnt = RF_ * lw_; }
+    else if (name == "attn_dropout_mask") { msrc = R.amask; cnt = RL_ * h_; }
+    else if (name == "ln2_input") { src = R.r1; cnt = RL_ * h_; }
+    else if (name == "mlp_fc1_input") { src = R.y2; cnt = RL_ * h_; }
+    else if (name == "gelu_input") { src = R.gin; cnt = RF_ * fw_; }
+    else if (name == "mlp_fc2_input") { src = R.fin; cnt = RF_ * fw_; }
+    else if (name == "mlp_dropout_mask") { msrc = R.mmask; cnt = RL_ * h_; }
+    else raise(1, "unknown or not-stored saved tensor: " + name);
+    require(n == cnt, "saved tensor size mismatch for " + name);
+    double* dbuf = nullptr;
+    SPL_CUDA(cudaMalloc(&dbuf, sizeof(double) * (size_t)cnt));
+    if (msrc) {
+      k::u8_to_f64(msrc, dbuf, cnt, st_);
+    } else if (col >= 0) {
+      T* tmp = nullptr;
+      SPL_CUDA(cudaMalloc(&tmp, sizeof(T) * (size_t)cnt));
+      SPL_CUDA(cudaMemcpy2DAsync(tmp, width * sizeof(T), src + col, ld * sizeof(T),
+                                 width * sizeof(T), RF_, cudaMemcpyDeviceToDevice, st_));
+      k::cast_to_f64<T>(tmp, dbuf, cnt, st_);
+      SPL_CUDA(cudaStreamSynchronize(st_));
+      cudaFree(tmp);
+    } else {
+      k::cast_to_f64<T>(src, dbuf, cnt, st_);
+    }
+    SPL_CUDA(cudaMemcpyAsync(out, dbuf, sizeof(double) * (size_t)cnt, cudaMemcpyDeviceToHost, st_));
+    SPL_CUDA(cudaStreamSynchronize(st_));
+    cudaFree(dbuf);
+  }
+
+  void attention_interior(int r, double* out3) override {
+    require(r >= 0 && r < L_, "local rank out of range");
+    if (!have_fwd_) raise(5, "missing saved forward state");
+    SPL_CUDA(cudaSetDevice(dev_));
+    const int64_t n = lh_ * b_ * s_ * s_;
+    T *sm = nullptr, *sd = nullptr, *o = nullptr;
+    uint8_t* mk = nullptr;
+    double* dbuf = nullptr;
+    SPL_CUDA(cudaMalloc(&sm, sizeof(T) * n));
+    SPL_CUDA(cudaMalloc(&sd, sizeof(T) * n));
+    SPL_CUDA(cudaMalloc(&mk, n));
+    SPL_CUDA(cudaMalloc(&o, sizeof(T) * RF_ * lw_));
+    SPL_CUDA(cudaMalloc(&dbuf, sizeof(double) * 3 * n));
+    k::AttnArgs a = attn_args(r);
+    a.o = o;
+    a.ldo = lw_;
+    a.lse = nullptr;
+    a.sm = sm;
+    a.mask = mk;
+    a.sd = sd;
+    k::attn_fwd<T>(a, st_);
+    k::cast_to_f64<T>(sm, dbuf, n, st_);
+    k::u8_to_f64(mk, dbuf + n, n, st_);
+    k::cast_to_f64<T>(sd, dbuf + 2 * n, n, st_);
+    SPL_CUDA(cudaMemcpyAsync(out3, dbuf, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st_));
+    SPL_CUDA(cudaStreamSynchronize(st_));
+    cudaFree(sm); cudaFree(sd); cudaFree(mk); cudaFree(o); cudaFree(dbuf);
+  }
+
+  // ------------------------------------------------------------------ accounting
+  std::vector<LedgerItem> ledger(int r) const override {
+    (void)r;
+    std::vector<LedgerItem> v;
+    const int64_t A = d_.act_bytes, M = d_.mask_bytes, TS = sizeof(T);
+    auto add = [&](const char* n, int64_t e, bool mask) {
+      v.push_back({n, e, e * (mask ? M : A), e * (mask ? 1 : TS)});
+    };
+    add("ln1_input", RL_ * h_, false);
+    if (kind_ == SPL_RECOMPUTE_FULL) return v;
+    add("qkv_input", RL_ * h_, false);
+    add("query", RF_ * lw_, false);
+    add("key", RF_ * lw_, false);
+    add("value", RF_ * lw_, false);
+    if (kind_ == SPL_RECOMPUTE_NONE) {
+      const int64_t ni = lh_ * b_ * s_ * s_;
+      add("softmax_out", ni, false);
+      add("softmax_dropout_mask", ni, true);
+      add("softmax_dropout_out", ni, false);
+    }
+    add("attn_proj_input", RF_ * lw_, false);
+    add("attn_dropout_mask", RL_ * h_, true);
+    add("ln2_input", RL_ * h_, false);
+    add("mlp_fc1_input", RL_ * h_, false);
+    add("gelu_input", RF_ * fw_, false);
+    add("mlp_fc2_input", RF_ * fw_, false);
+    add("mlp_dropout_mask", RL_ * h_, true);
+    return v;
+  }
+
+  void saved_bytes(int r, int64_t* lb, int64_t* pb, int64_t* ub) const override {
+    int64_t l = 0, p = 0;
+    for (auto& e : ledger(r)) {
+      l += e.bytes;
+      p += e.physical;
+    }
+    int64_t u = 0;
+    if (kind_ != SPL_RECOMPUTE_FULL) u += 4 * RL_ * (int64_t)sizeof(float);  // LN stats
+    if (kind_ == SPL_RECOMPUTE_SELECTIVE) u += lh_ * b_ * s_ * (int64_t)sizeof(float);  // LSE
+    *lb = l;
+    *pb = p;
+    *ub = u;
+  }
+
+  // ------------------------------------------------------------------ profiling
+  void set_profile(bool on) override {
+    SPL_CUDA(cudaStreamSynchronize(st_));
+    profiling_ = on;
+    pending_.clear();
+    for (int c = 0; c < K_NCLASS; ++c) prof_ms_[c] = prof_flops_[c] = prof_bytes_[c] = 0, prof_n_[c] = 0;
+    ev_next_ = 0;
+  }
+  void read_profile(double ms[K_NCLASS], int64_t n[K_NCLASS], double fl[K_NCLASS],
+                    double by[K_NCLASS]) override {
+    SPL_CUDA(cudaStreamSynchronize(st_));
+    for (auto& p : pending_) {
+      float e = 0.f;
+      SPL_CUDA(cudaEventElapsedTime(&e, p.a, p.b));
+      prof_ms_[p.cls] += e;
+    }
+    pending_.clear();
+    ev_next_ = 0;
+    for (int c = 0; c < K_NCLASS; ++c) {
+      ms[c] = prof_ms_[c];
+      n[c] = prof_n_[c];
+      fl[c] = prof_flops_[c];
+      by[c] = prof_bytes_[c];
+    }
+  }
+  int64_t launch_count(bool reset) override {
+    const int64_t v = launches_;
+    if (reset) launches_ = 0;
+    return v;
+  }
+  void set_graphs(bool on) override { graphs_ = on; }
+
+ private:
+  struct Rank {
+    T *wqkv = nullptr, *wo = nullptr, *w1 = nullptr, *w2 = nullptr;
+    float *bqkv = nullptr, *bo = nullptr, *b1 = nullptr, *b2 = nullptr, *g1 = nullptr,
+          *be1 = nullptr, *g2 = nullptr, *be2 = nullptr;
+    float *dwqkv = nullptr, *dbqkv = nullptr, *dwo = nullptr, *dw1 = nullptr, *db1 = nullptr,
+          *dw2 = nullptr, *repl = nullptr;
+    T *x_s = nullptr, *y1_s = nullptr, *qkv = nullptr, *sm = nullptr, *sd = nullptr,
+      *api = nullptr, *r1 = nullptr, *y2 = nullptr, *gin = nullptr, *fin = nullptr;
+    uint8_t *mask_i = nullptr, *amask = nullptr, *mmask = nullptr;
+    float *mu1 = nullptr, *rs1 = nullptr, *mu2 = nullptr, *rs2 = nullptr, *lse = nullptr;
+    T *yfull = nullptr, *part = nullptr, *rs_out = nullptr, *dfull = nullptr, *dgin = nullptr,
+      *dqkv = nullptr, *dproj = nullptr, *d_s = nullptr, *dr1 = nullptr, *y_re = nullptr;
+    float *delta = nullptr, *partials = nullptr;
+  };
+
+  void validate() {
+    require(t_ >= 1, "t must be >= 1");
+    require(a_ >= 1 && h_ >= 1 && s_ >= 1 && b_ >= 1, "shape fields must be >= 1");
+    require(h_ % a_ == 0, "hidden not divisible by heads");
+    require(s_ % t_ == 0 && h_ % t_ == 0, "s and h must be divisible by t");
+    require(a_ % t_ == 0, "attention heads must be divisible by t");
+    require(d_.dropout_p >= 0.0 && d_.dropout_p < 1.0, "dropout probability must lie in [0, 1)");
+    require(d_.recompute >= 0 && d_.recompute <= 2, "unknown recompute kind");
+    require(d_.act_bytes >= 1 && d_.mask_bytes >= 1, "byte convention widths must be >= 1");
+    require(h_ / a_ <= 256, "head_dim > 256 unsupported");
+  }
+
+  static T cvt(double v) {
+    if constexpr (std::is_same_v<T, float>) return (float)v;
+    else return __double2bfloat16(v);
+  }
+
+  template <typename U>
+  U* alloc(int64_t n, int cat, int r) {
+    void* p = nullptr;
+    const size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(U);
+    SPL_CUDA(cudaMalloc(&p, bytes));
+    SPL_CUDA(cudaMemset(p, 0, bytes));
+    allocs_.push_back({p, bytes, cat, r});
+    return static_cast<U*>(p);
+  }
+
+  template <typename U>
+  void up(U* dst, const std::vector<U>& v) {
+    SPL_CUDA(cudaMemcpy(dst, v.data(), v.size() * sizeof(U), cudaMemcpyHostToDevice));
+  }
+  std::vector<double> down(const float* src, int64_t n) {
+    std::vector<float> f((size_t)n);
+    SPL_CUDA(cudaMemcpy(f.data(), src, sizeof(float) * (size_t)n, cudaMemcpyDeviceToHost));
+    return std::vector<double>(f.begin(), f.end());
+  }
+
+  void allocate() {
+    R_.resize(L_);
+    const int64_t ni = lh_ * b_ * s_ * s_;
+    const int saved = kind_ == SPL_RECOMPUTE_FULL ? kWork : kSaved;
+    const int saved_u = kind_ == SPL_RECOMPUTE_FULL ? kWork : kSavedUncounted;
+    const int nch_l = k::num_chunks(RL_, kChunkRows), nch_f = k::num_chunks(RF_, kChunkRows);
+    const int64_t npart = std::max<int64_t>(2 * (int64_t)nch_l * h_, nch_f * std::max<int64_t>(3 * lw_, fw_));
+    T *yfull = nullptr, *dfull = nullptr, *dgin = nullptr, *dqkv = nullptr, *dproj = nullptr;
+    float *delta = nullptr, *partials = nullptr;
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      R.wqkv = alloc<T>(h_ * 3 * lw_, kParam, r);
+      R.bqkv = alloc<float>(3 * lw_, kParam, r);
+      R.wo = alloc<T>(lw_ * h_, kParam, r);
+      R.bo = alloc<float>(h_, kParam, r);
+      R.w1 = alloc<T>(h_ * fw_, kParam, r);
+      R.b1 = alloc<float>(fw_, kParam, r);
+      R.w2 = alloc<T>(fw_ * h_, kParam, r);
+      R.b2 = alloc<float>(h_, kParam, r);
+      R.g1 = alloc<float>(h_, kParam, r);
+      R.be1 = alloc<float>(h_, kParam, r);
+      R.g2 = alloc<float>(h_, kParam, r);
+      R.be2 = alloc<float>(h_, kParam, r);
+      R.dwqkv = alloc<float>(h_ * 3 * lw_, kGrad, r);
+      R.dbqkv = alloc<float>(3 * lw_, kGrad, r);
+      R.dwo = alloc<float>(lw_ * h_, kGrad, r);
+      R.dw1 = alloc<float>(h_ * fw_, kGrad, r);
+      R.db1 = alloc<float>(fw_, kGrad, r);
+      R.dw2 = alloc<float>(fw_ * h_, kGrad, r);
+      R.repl = alloc<float>(6 * h_, kGrad, r);
+      R.x_s = alloc<T>(RL_ * h_, kSaved, r);
+      R.y1_s = alloc<T>(RL_ * h_, saved, r);
+      R.qkv = alloc<T>(RF_ * 3 * lw_, saved, r);
+      if (kind_ == SPL_RECOMPUTE_NONE) {
+        R.sm = alloc<T>(ni, kSaved, r);
+        R.mask_i = alloc<uint8_t>(ni, kSaved, r);
+        R.sd = alloc<T>(ni, kSaved, r);
+      } else {
+        R.lse = alloc<float>(lh_ * b_ * s_, saved_u, r);
+      }
+      R.api = alloc<T>(RF_ * lw_, saved, r);
+      R.amask = alloc<uint8_t>(RL_ * h_, saved, r);
+      R.r1 = alloc<T>(RL_ * h_, saved, r);
+      R.y2 = alloc<T>(RL_ * h_, saved, r);
+      R.gin = alloc<T>(RF_ * fw_, saved, r);
+      R.fin = alloc<T>(RF_ * fw_, saved, r);
+      R.mmask = alloc<uint8_t>(RL_ * h_, saved, r);
+      R.mu1 = alloc<float>(RL_, saved_u, r);
+      R.rs1 = alloc<float>(RL_, saved_u, r);
+      R.mu2 = alloc<float>(RL_, saved_u, r);
+      R.rs2 = alloc<float>(RL_, saved_u, r);
+      // workspaces (transient, not stored activations)
+      if (sp_) {
+        if (!yfull || comm_->local() == 1) yfull = alloc<T>(RF_ * h_, kWork, r);
+        if (!dfull || comm_->local() == 1) dfull = alloc<T>(RF_ * h_, kWork, r);
+        R.yfull = yfull;
+        R.dfull = dfull;
+        R.rs_out = alloc<T>(RL_ * h_, kWork, r);
+      }
+      R.part = alloc<T>(RF_ * h_, kWork, r);
+      if (!dgin) {
+        dgin = alloc<T>(RF_ * fw_, kWork, r);
+        dqkv = alloc<T>(RF_ * 3 * lw_, kWork, r);
+        dproj = alloc<T>(RF_ * lw_, kWork, r);
+        delta = alloc<float>(lh_ * b_ * s_, kWork, r);
+        partials = alloc<float>(npart, kWork, r);
+      }
+      R.dgin = dgin;
+      R.dqkv = dqkv;
+      R.dproj = dproj;
+      R.delta = delta;
+      R.partials = partials;
+      R.d_s = alloc<T>(RL_ * h_, kWork, r);
+      R.dr1 = alloc<T>(RL_ * h_, kWork, r);
+      if (kind_ == SPL_RECOMPUTE_FULL) R.y_re = alloc<T>(RL_ * h_, kWork, r);
+    }
+    nonfinite_ = alloc<int>(1, kWork, 0);
+  }
+
+  void ensure_staging() {
+    if (!stage_.empty()) return;
+    for (int r = 0; r < L_; ++r)
+      for (int i = 0; i < 4; ++i) stage_.push_back(alloc<T>(RL_ * h_, kWork, r));
+  }
+
+  // ---- launch bookkeeping
+  template <typename F>
+  void launch(KClass cls, int kernels, double flops, double bytes, F&& f) {
+    launches_ += kernels;
+    if (!profiling_) {
+      f();
+      return;
+    }
+    if (ev_next_ + 2 > evpool_.size()) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t e;
+        SPL_CUDA(cudaEventCreate(&e));
+        evpool_.push_back(e);
+      }
+    }
+    cudaEvent_t ea = evpool_[ev_next_++], eb = evpool_[ev_next_++];
+    SPL_CUDA(cudaEventRecord(ea, st_));
+    f();
+    SPL_CUDA(cudaEventRecord(eb, st_));
+    pending_.push_back({ea, eb, cls});
+    prof_n_[cls] += kernels;
+    prof_flops_[cls] += flops;
+    prof_bytes_[cls] += bytes;
+  }
+
+  void gemm(int64_t M, int64_t N, int64_t K, const T* A, int64_t lda, Major am, const T* B,
+            int64_t ldb, Major bm, void* C, int64_t ldc, Epi epi, const float* bias = nullptr,
+            void* C2 = nullptr, const T* aux = nullptr, int64_t ldaux = 0) {
+    GemmArgs g;
+    g.M = M; g.N = N; g.K = K;
+    g.A = A; g.lda = lda; g.amaj = am;
+    g.B = B; g.ldb = ldb; g.bmaj = bm;
+    g.C = C; g.ldc = ldc; g.epi = epi; g.bias = bias; g.C2 = C2; g.aux = aux; g.ldaux = ldaux;
+    const double es = sizeof(T);
+    const double bytes = (M * K + K * N) * es + M * N * (epi == Epi::F32 ? 4.0 : es) *
+                         (epi == Epi::BiasGelu ? 2 : 1) + (epi == Epi::GeluBwd ? M * N * es : 0);
+    launch(K_GEMM, 1, 2.0 * M * N * K, bytes, [&] { k::gemm<T>(g, st_); });
+  }
+
+  k::AttnArgs attn_args(int r) {
+    Rank& R = R_[r];
+    k::AttnArgs a;
+    a.s = s_; a.b = b_; a.lh = lh_; a.hd = hd_;
+    a.head_offset = (rank0_ + r) * lh_;
+    a.heads_total = a_;
+    a.qkv = R.qkv; a.ld = 3 * lw_; a.qoff = 0; a.koff = lw_; a.voff = 2 * lw_;
+    a.o = R.api; a.ldo = lw_;
+    a.scale = scale_;
+    a.causal = d_.causal;
+    a.drop = k_soft_;
+    a.lse = R.lse;
+    a.sm = R.sm; a.mask = R.mask_i; a.sd = R.sd;
+    return a;
+  }
+
+  double attn_flops(bool bwd) const {
+    // QKᵀ and P·V per head: 2·s²·hd each (halved when causal); backward: 5 GEMM-equivalents
+    // of which recompute of QKᵀ is one (flash-style backward).
+    const double per = 2.0 * (double)s_ * s_ * hd_ * lh_ * b_ * (d_.causal ? 0.5 : 1.0);
+    return bwd ? per * 5.0 : per * 2.0;
+  }
+
+  // ---- collectives
+  std::vector<const void*> cptrs(std::function<const void*(int)> f) {
+    std::vector<const void*> v(L_);
+    for (int r = 0; r < L_; ++r) v[r] = f(r);
+    return v;
+  }
+  std::vector<void*> mptrs(std::function<void*(int)> f) {
+    std::vector<void*> v(L_);
+    for (int r = 0; r < L_; ++r) v[r] = f(r);
+    return v;
+  }
+  DType dt() const { return std::is_same_v<T, float> ? DType::F32 : DType::BF16; }
+
+  // g (forward) / ḡ-dual (backward): shards {RL,h} -> full {RF,h}
+  void gather(std::function<const void*(int)> shard, std::function<void*(int)> full, CommTag tag) {
+    auto s = cptrs(shard);
+    auto f = mptrs(full);
+    comm_->log(tag, 0, RF_ * h_);
+    launch(K_COMM, 1, 0, (double)RF_ * h_ * sizeof(T) * (t_ - 1) / t_,
+           [&] { comm_->all_gather(s.data(), f.data(), RL_ * h_, dt(), st_); });
+  }
+  // ḡ (forward) / g-dual (backward): partials {RF,h} -> shards {RL,h}; without SP an
+  // all-reduce in place (f̄ / f), the result left in part.
+  void scatter(CommTag tag) {
+    if (sp_) {
+      auto p = cptrs([&](int r) { return (const void*)R_[r].part; });
+      auto o = mptrs([&](int r) { return (void*)R_[r].rs_out; });
+      comm_->log(tag, 1, RF_ * h_);
+      launch(K_COMM, 1, 0, (double)RF_ * h_ * sizeof(T) * (t_ - 1) / t_,
+             [&] { comm_->reduce_scatter(p.data(), o.data(), RL_ * h_, dt(), st_); });
+    } else if (t_ > 1) {
+      auto p = mptrs([&](int r) { return (void*)R_[r].part; });
+      comm_->log(tag, 2, RF_ * h_);
+      launch(K_COMM, 1, 0, 2.0 * RF_ * h_ * sizeof(T) * (t_ - 1) / t_,
+             [&] { comm_->all_reduce(p.data(), RF_ * h_, dt(), st_); });
+    }
+  }
+  T* scattered(int r) { return sp_ ? R_[r].rs_out : R_[r].part; }
+
+  // ------------------------------------------------------------------ schedules
+  void run_forward(T* const* y, CommTag tag, int* nonfinite) {
+    const int64_t h = h_;
+    const float eps = (float)d_.ln_eps;
+    const double eb = sizeof(T);
+    // LN1 on sequence shards (block.cpp:546-550)
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      launch(K_ELEM, 1, 0, 2.0 * RL_ * h * eb, [&] {
+        k::layernorm_fwd<T>(R.x_s, R.g1, R.be1, R.y1_s, R.mu1, R.rs1, RL_, h, eps, st_);
+      });
+    }
+    // g: all-gather Y1 (block.cpp:551)
+    if (sp_) gather([&](int r) { return (const void*)R_[r].y1_s; },
+                    [&](int r) { return (void*)R_[r].yfull; }, tag);
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      const T* y1 = sp_ ? R.yfull : R.y1_s;
+      // fused QKV projection, column-parallel (block.cpp:556-558)
+      gemm(RF_, 3 * lw_, h, y1, h, Major::K, R.wqkv, 3 * lw_, Major::MN, R.qkv, 3 * lw_,
+           Epi::Bias, R.bqkv);
+      // attention interior + attention over values (block.cpp:559-562)
+      k::AttnArgs a = attn_args(r);
+      launch(K_ATTN, 1, attn_flops(false), 0, [&] { k::attn_fwd<T>(a, st_); });
+      // row-parallel projection partial (block.cpp:563)
+      gemm(RF_, h, lw_, R.api, lw_, Major::K, R.wo, h, Major::MN, R.part, h, Epi::Store);
+    }
+    scatter(tag);  // ḡ (block.cpp:567)
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      const uint64_t base = sp_ ? (uint64_t)((rank0_ + r) * RL_ * h) : 0;
+      // bias + dropout + residual, fused with LN2 (block.cpp:568-578)
+      launch(K_ELEM, 1, 0, (4.0 * eb + 1.0) * RL_ * h, [&] {
+        k::bias_dropout_residual<T>(scattered(r), R.bo, R.x_s, R.r1, R.amask, R.y2, R.g2, R.be2,
+                                    R.mu2, R.rs2, RL_, h, k_attn_, base, eps, nullptr, st_);
+      });
+    }
+    if (sp_) gather([&](int r) { return (const void*)R_[r].y2; },
+                    [&](int r) { return (void*)R_[r].yfull; }, tag);  // block.cpp:580
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      const T* y2 = sp_ ? R.yfull : R.y2;
+      // FC1 + bias + GELU, keeping both pre- and post-activation (block.cpp:584-585)
+      gemm(RF_, fw_, h, y2, h, Major::K, R.w1, fw_, Major::MN, R.gin, fw_, Epi::BiasGelu, R.b1,
+           R.fin);
+      gemm(RF_, h, fw_, R.fin, fw_, Major::K, R.w2, h, Major::MN, R.part, h, Epi::Store);  // 586
+    }
+    scatter(tag);  // block.cpp:588
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      const uint64_t base = sp_ ? (uint64_t)((rank0_ + r) * RL_ * h) : 0;
+      launch(K_ELEM, 1, 0, (3.0 * eb + 1.0) * RL_ * h, [&] {
+        k::bias_dropout_residual<T>(scattered(r), R.b2, R.r1, y[r], R.mmask, nullptr, nullptr,
+                                    nullptr, nullptr, nullptr, RL_, h, k_mlp_, base, eps,
+                                    nonfinite, st_);
+      });
+    }
+  }
+
+  void run_backward(const void* const* dyv, void* const* dxv) {
+    const int64_t h = h_;
+    const double eb = sizeof(T);
+    const int nch_l = k::num_chunks(RL_, kChunkRows), nch_f = k::num_chunks(RF_, kChunkRows);
+    const float inv_keep = k_mlp_.inv_keep;
+    // ---- MLP branch (block.cpp:642-681)
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      const T* dy = static_cast<const T*>(dyv[r]);
+      launch(K_ELEM, 2, 0, (2.0 * eb + 1.0) * RL_ * h, [&] {
+        k::dropout_bwd_colsum<T>(dy, R.mmask, inv_keep, R.d_s, R.partials, RL_, h, kChunkRows, st_);
+        k::reduce_partials(R.partials, nch_l, h, R.repl + 1 * h, false, st_);  // b2 partial
+      });
+    }
+    if (sp_) {
+      gather([&](int r) { return (const void*)R_[r].d_s; }, [&](int r) { return (void*)R_[r].dfull; },
+             kSchedule);  // block.cpp:653
+      gather([&](int r) { return (const void*)R_[r].y2; }, [&](int r) { return (void*)R_[r].yfull; },
+             kRegather);  // block.cpp:655
+    }
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      const T* dmo = sp_ ? R.dfull : R.d_s;
+      const T* y2 = sp_ ? R.yfull : R.y2;
+      // FC2 dgrad fused with GELU backward (block.cpp:660, 662)
+      gemm(RF_, fw_, h, dmo, h, Major::K, R.w2, h, Major::K, R.dgin, fw_, Epi::GeluBwd, nullptr,
+           nullptr, R.gin, fw_);
+      // FC2 wgrad (block.cpp:661)
+      gemm(fw_, h, RF_, R.fin, fw_, Major::MN, dmo, h, Major::MN, R.dw2, h, Epi::F32);
+      // b1 grad (block.cpp:663)
+      launch(K_ELEM, 2, 0, eb * RF_ * fw_, [&] {
+        k::colsum_partial<T>(R.dgin, RF_, fw_, fw_, R.partials, kChunkRows, st_);
+        k::reduce_partials(R.partials, nch_f, fw_, R.db1, false, st_);
+      });
+      // FC1 wgrad on the re-gathered Y2 (block.cpp:664) and dgrad (665)
+      gemm(h, fw_, RF_, y2, h, Major::MN, R.dgin, fw_, Major::MN, R.dw1, fw_, Epi::F32);
+      gemm(RF_, h, fw_, R.dgin, fw_, Major::K, R.w1, fw_, Major::K, R.part, h, Epi::Store);
+    }
+    scatter(kSchedule);  // g-dual: block.cpp:668-669
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      const T* dy = static_cast<const T*>(dyv[r]);
+      launch(K_ELEM, 2, 0, 5.0 * eb * RL_ * h, [&] {
+        k::layernorm_bwd<T>(scattered(r), R.r1, R.mu2, R.rs2, R.g2, dy, R.dr1, R.partials,
+                            R.partials + (int64_t)nch_l * h, RL_, h, kChunkRows, st_);
+      });
+      launch(K_ELEM, 2, 0, 0, [&] {
+        k::reduce_partials(R.partials, nch_l, h, R.repl + 4 * h, false, st_);
+        k::reduce_partials(R.partials + (int64_t)nch_l * h, nch_l, h, R.repl + 5 * h, false, st_);
+      });
+    }
+    // ---- attention branch (block.cpp:683-726)
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      launch(K_ELEM, 2, 0, (2.0 * eb + 1.0) * RL_ * h, [&] {
+        k::dropout_bwd_colsum<T>(R.dr1, R.amask, inv_keep, R.d_s, R.partials, RL_, h, kChunkRows, st_);
+        k::reduce_partials(R.partials, nch_l, h, R.repl + 0 * h, false, st_);  // bo partial
+      });
+    }
+    if (sp_) {
+      gather([&](int r) { return (const void*)R_[r].d_s; }, [&](int r) { return (void*)R_[r].dfull; },
+             kSchedule);  // block.cpp:691
+      gather([&](int r) { return (const void*)R_[r].y1_s; }, [&](int r) { return (void*)R_[r].yfull; },
+             kRegather);  // block.cpp:692
+    }
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      const T* dao = sp_ ? R.dfull : R.d_s;
+      const T* y1 = sp_ ? R.yfull : R.y1_s;
+      gemm(RF_, lw_, h, dao, h, Major::K, R.wo, h, Major::K, R.dproj, lw_, Epi::Store);  // 699
+      gemm(lw_, h, RF_, R.api, lw_, Major::MN, dao, h, Major::MN, R.dwo, h, Epi::F32);    // 700
+      k::AttnArgs a = attn_args(r);
+      launch(K_ATTN, 3, attn_flops(true), 0,
+             [&] { k::attn_bwd<T>(a, R.dproj, R.dqkv, R.delta, st_); });  // 701-702
+      launch(K_ELEM, 2, 0, eb * RF_ * 3 * lw_, [&] {
+        k::colsum_partial<T>(R.dqkv, RF_, 3 * lw_, 3 * lw_, R.partials, kChunkRows, st_);
+        k::reduce_partials(R.partials, nch_f, 3 * lw_, R.dbqkv, false, st_);  // 703-705
+      });
+      gemm(h, 3 * lw_, RF_, y1, h, Major::MN, R.dqkv, 3 * lw_, Major::MN, R.dwqkv, 3 * lw_,
+           Epi::F32);  // 706-708
+      // dY1 = dQ·Wqᵀ + dK·Wkᵀ + dV·Wvᵀ as one GEMM over the fused 3h/t weight (709-711)
+      gemm(RF_, h, 3 * lw_, R.dqkv, 3 * lw_, Major::K, R.wqkv, 3 * lw_, Major::K, R.part, h,
+           Epi::Store);
+    }
+    scatter(kSchedule);  // block.cpp:714-715
+    for (int r = 0; r < L_; ++r) {
+      Rank& R = R_[r];
+      launch(K_ELEM, 2, 0, 5.0 * eb * RL_ * h, [&] {
+        k::layernorm_bwd<T>(scattered(r), R.x_s, R.mu1, R.rs1, R.g1, R.dr1,
+                            static_cast<T*>(dxv[r]), R.partials, R.partials + (int64_t)nch_l * h,
+                            RL_, h, kChunkRows, st_);
+      });
+      launch(K_ELEM, 2, 0, 0, [&] {
+        k::reduce_partials(R.partials, nch_l, h, R.repl + 2 * h, false, st_);
+        k::reduce_partials(R.partials + (int64_t)nch_l * h, nch_l, h, R.repl + 3 * h, false, st_);
+      });
+    }
+    // replicated-parameter gradients: one packed all-reduce (the 6 GradSync ARs, 741-746)
+    if (sp_ && t_ > 1) {
+      std::vector<float*> bufs(L_);
+      for (int r = 0; r < L_; ++r) bufs[r] = R_[r].repl;
+      for (int i = 0; i < 6; ++i) comm_->log(kGradSync, 2, h);
+      launch(K_COMM, 1, 0, 2.0 * 6 * h * 4 * (t_ - 1) / t_,
+             [&] { comm_->all_reduce_f32(bufs.data(), 6 * h, st_); });
+    }
+  }
+
+  spl_layer_desc d_;
+  int dev_;
+  std::unique_ptr<Comm> comm_;
+  int t_ = 1, L_ = 1, rank0_ = 0;
+  int64_t s_ = 0, b_ = 0, h_ = 0, a_ = 0, hd_ = 0, lh_ = 0, lw_ = 0, fw_ = 0, RF_ = 0, RL_ = 0;
+  bool sp_ = true;
+  int kind_ = 0;
+  float scale_ = 1.f;
+  DropKey k_soft_{}, k_attn_{}, k_mlp_{};
+  cudaStream_t st_ = nullptr;
+  cudaEvent_t tstart_ = nullptr, tstop_ = nullptr;
+  std::vector<Rank> R_;
+  std::vector<Alloc> allocs_;
+  std::vector<T*> stage_;
+  void* pinned_ = nullptr;
+  int* nonfinite_ = nullptr;
+  bool have_fwd_ = false;
+  bool graphs_ = false;
+  // profiling
+  struct Pending {
+    cudaEvent_t a, b;
+    int cls;
+  };
+  bool profiling_ = false;
+  std::vector<cudaEvent_t> evpool_;
+  size_t ev_next_ = 0;
+  std::vector<Pending> pending_;
+  double prof_ms_[K_NCLASS] = {}, prof_flops_[K_NCLASS] = {}, prof_bytes_[K_NCLASS] = {};
+  int64_t prof_n_[K_NCLASS] = {};
+  int64_t launches_ = 0;
+};
+
+}  // namespace
+
+std::unique_ptr<LayerBase> make_layer(const spl_layer_desc& d, int device,
+                                      std::unique_ptr<Comm> comm) {
+  if (d.dtype == SPL_DTYPE_F32) return std::make_unique<Layer<float>>(d, device, std::move(comm));
+  if (d.dtype == SPL_DTYPE_BF16) return std::make_unique<Layer<bf16>>(d, device, std::move(comm));
+  raise(1, "unknown dtype");
+}
+
+// ---------------------------------------------------------------- accountant
+// activation_memory.cpp:23-77: per sbh, 4 replicated + 12 tensor-sharded activation
+// elements and 2 replicated masks; per a·s²·b, 2 activations + 1 mask (interior). SP divides
+// the replicated part by t, selective drops the interior, full keeps A·sbh (not divided by
+// t, activation_memory.cpp:59-63). All terms share the denominator t: exact in __int128.
+int per_layer_bytes_exact(int64_t a, int64_t h, int64_t s, int64_t b, int64_t t, int kind,
+                          int sp, int64_t act, int64_t mask, __int128* num, __int128* den) {
+  if (a < 1 || h < 1 || s < 1 || b < 1 || t < 1) return 1;
+  if (h % a || h % t || s % t) return 1;
+  if (act < 1 || mask < 1 || kind < 0 || kind > 2) return 1;
+  const __int128 sbh = (__int128)s * b * h;
+  if (kind == SPL_RECOMPUTE_FULL) {
+    *num = (__int128)act * sbh;
+    *den = 1;
+    return 0;
+  }
+  const __int128 rep = ((__int128)4 * act + (__int128)2 * mask) * sbh;
+  const __int128 shd = (__int128)12 * act * sbh;
+  __int128 n = sp ? rep + shd : rep * t + shd;
+  if (kind == SPL_RECOMPUTE_NONE) n += ((__int128)2 * act + mask) * ((__int128)a * s * s * b);
+  __int128 d = t, x = n, y = d;
+  while (y) {
+    __int128 q = x % y;
+    x = y;
+    y = q;
+  }
+  *num = n / x;
+  *den = d / x;
+  return 0;
+}
+
+}  // namespace spl

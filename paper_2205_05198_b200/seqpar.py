@@ -1,0 +1,311 @@
+"""Python mirror of the reference's seqpar layer API over the C ABI (include/spl.h).
+
+Reference interface (/root/reference/proj/core/include/actplan/seqpar/block.hpp):
+  BlockConfig (28-42), seqpar_block_forward (158-162), seqpar_block_backward (173-174),
+  SeqparForward (136-154), SeqparBackward (164-171), ActivationLedger (61-73),
+  CommLog (collectives.hpp:28-52), per_layer_bytes (activation_memory.hpp:83-84).
+Same names, argument meaning and error classes: std::invalid_argument -> ValueError,
+std::domain_error -> ArithmeticError. Host tensors are fp64 numpy arrays in the reference
+layouts ({s,b,h}; params packed in LayerParams::named_tensors() order); the layer itself runs
+on the GPU in the chosen dtype, device memory held as torch tensors (plumbing only).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+PARAM_NAMES = ["wq", "wk", "wv", "bq", "bk", "bv", "wo", "bo", "w1", "b1", "w2", "b2",
+               "ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias"]
+
+
+@dataclass
+class BlockConfig:
+    heads: int
+    hidden: int
+    seq: int
+    batch: int
+    dropout_p: float = 0.0
+    causal: bool = False
+    seed: int = 42
+    layer_index: int = 0
+    microbatch: int = 1
+    layer_norm_eps: float = 1e-5
+    act_bytes: int = 2
+    mask_bytes: int = 1
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden // self.heads
+
+
+def param_count(h: int) -> int:
+    return 12 * h * h + 13 * h
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _tdtype(dtype: str):
+    torch = _torch()
+    return torch.float32 if _lib.DTYPE[dtype] == 0 else torch.bfloat16
+
+
+class SeqparLayer:
+    """One layer handle: t simulated ranks on one GPU (nccl=None), or one rank of an NCCL
+    group (nccl=(rank, unique_id_bytes))."""
+
+    def __init__(self, cfg: BlockConfig, t: int, recompute: str = "none",
+                 sequence_parallel: bool = True, dtype: str = "bf16", device: int = 0,
+                 check_finite: bool = True, nccl: tuple[int, bytes] | None = None):
+        self.cfg, self.t, self.recompute, self.sp, self.dtype = cfg, t, recompute, sequence_parallel, dtype
+        self.device = device
+        d = _lib.LayerDesc()
+        lib().spl_desc_default(C.byref(d))
+        d.heads, d.hidden, d.seq, d.batch = cfg.heads, cfg.hidden, cfg.seq, cfg.batch
+        d.dropout_p, d.causal, d.seed = cfg.dropout_p, int(cfg.causal), cfg.seed
+        d.layer_index, d.microbatch, d.ln_eps = cfg.layer_index, cfg.microbatch, cfg.layer_norm_eps
+        d.recompute = _lib.RECOMPUTE[recompute]
+        d.sequence_parallel = int(sequence_parallel)
+        d.dtype = _lib.DTYPE[dtype]
+        d.check_finite = int(check_finite)
+        d.act_bytes, d.mask_bytes = cfg.act_bytes, cfg.mask_bytes
+        self._h = C.c_void_p()
+        if nccl is None:
+            check(lib().spl_create_local(C.byref(d), device, t, C.byref(self._h)))
+        else:
+            rank, uid = nccl
+            check(lib().spl_create_nccl(C.byref(d), device, t, rank, uid, C.byref(self._h)))
+        self.local = lib().spl_local_ranks(self._h)
+        self.rank0 = 0 if nccl is None else nccl[0]
+
+    # ---- lifecycle
+    def close(self):
+        if self._h:
+            lib().spl_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().spl_nccl_unique_id(buf))
+        return buf.raw
+
+    # ---- shapes
+    @property
+    def shard_rows(self) -> int:
+        c = self.cfg
+        return (c.seq // self.t if self.sp else c.seq)
+
+    def shard_shape(self):
+        return (self.shard_rows, self.cfg.batch, self.cfg.hidden)
+
+    # ---- params
+    def load_params(self, packed: np.ndarray):
+        p = np.ascontiguousarray(packed, np.float64)
+        assert p.size == param_count(self.cfg.hidden)
+        check(lib().spl_load_params(self._h, p.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def init_params(self, seed: int):
+        check(lib().spl_init_params(self._h, seed))
+
+    # ---- compute (device tensors)
+    def forward(self, x: list, y: list | None = None) -> list:
+        torch = _torch()
+        if len(x) != self.local:
+            raise ValueError("expected one input shard per rank")
+        for xi in x:
+            if tuple(xi.shape) != self.shard_shape() or xi.dtype != _tdtype(self.dtype):
+                raise ValueError(f"input shard must be {self.shard_shape()} {self.dtype}")
+        if y is None:
+            y = [torch.empty_like(xi) for xi in x]
+        xs = (C.c_void_p * self.local)(*[xi.data_ptr() for xi in x])
+        ys = (C.c_void_p * self.local)(*[yi.data_ptr() for yi in y])
+        check(lib().spl_forward(self._h, xs, ys))
+        return y
+
+    def backward(self, dy: list, dx: list | None = None) -> list:
+        torch = _torch()
+        if len(dy) != self.local:
+            raise ValueError("expected one gradient shard per rank")
+        for di in dy:
+            if tuple(di.shape) != self.shard_shape() or di.dtype != _tdtype(self.dtype):
+                raise ValueError("dy shard shape mismatch")
+        if dx is None:
+            dx = [torch.empty_like(di) for di in dy]
+        ds = (C.c_void_p * self.local)(*[di.data_ptr() for di in dy])
+        xs = (C.c_void_p * self.local)(*[xi.data_ptr() for xi in dx])
+        check(lib().spl_backward(self._h, ds, xs))
+        return dx
+
+    def step_host(self, x_host, dy_host, y_host, dx_host):
+        check(lib().spl_step_host(self._h, x_host.data_ptr(), dy_host.data_ptr(),
+                                  y_host.data_ptr(), dx_host.data_ptr()))
+
+    # ---- read-back
+    def grads(self) -> np.ndarray:
+        out = np.empty(param_count(self.cfg.hidden), np.float64)
+        check(lib().spl_get_grads(self._h, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def w1_grad_shard(self, r: int) -> np.ndarray:
+        h = self.cfg.hidden
+        out = np.empty((h, 4 * h // self.t), np.float64)
+        check(lib().spl_get_w1_grad_shard(self._h, r, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def saved(self, r: int, name: str, shape) -> np.ndarray:
+        out = np.empty(shape, np.float64)
+        check(lib().spl_get_saved(self._h, r, name.encode(), out.ctypes.data_as(C.POINTER(C.c_double)),
+                                  out.size))
+        return out
+
+    def interior(self, r: int) -> np.ndarray:
+        c = self.cfg
+        out = np.empty((3, c.heads // self.t, c.batch, c.seq, c.seq), np.float64)
+        check(lib().spl_attention_interior(self._h, r, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def ledger(self, r: int = 0) -> dict:
+        n = C.c_int(32)
+        arr = (_lib.LedgerEntry * 32)()
+        check(lib().spl_ledger(self._h, r, arr, C.byref(n)))
+        return {arr[i].name.decode(): (arr[i].elements, arr[i].bytes, arr[i].physical_bytes)
+                for i in range(n.value)}
+
+    def saved_bytes(self, r: int = 0) -> tuple[int, int, int]:
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().spl_saved_bytes(self._h, r, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def comm_log(self) -> dict:
+        arr = (C.c_int64 * 16)()
+        check(lib().spl_comm_log(self._h, arr))
+        tags = ["schedule", "regather", "grad_sync", "recompute"]
+        return {t: dict(all_gathers=arr[4 * i], reduce_scatters=arr[4 * i + 1],
+                        all_reduces=arr[4 * i + 2], ring_elements=arr[4 * i + 3])
+                for i, t in enumerate(tags)}
+
+    def comm_log_reset(self):
+        check(lib().spl_comm_log_reset(self._h))
+
+    # ---- timing / profiling
+    def timer_start(self):
+        check(lib().spl_timer_start(self._h))
+
+    def timer_stop(self) -> float:
+        ms = C.c_float()
+        check(lib().spl_timer_stop(self._h, C.byref(ms)))
+        return ms.value
+
+    def synchronize(self):
+        check(lib().spl_synchronize(self._h))
+
+    def profile(self, on: bool):
+        check(lib().spl_profile_enable(self._h, int(on)))
+
+    def profile_read(self) -> dict:
+        ms, n = (C.c_double * 5)(), (C.c_int64 * 5)()
+        fl, by = (C.c_double * 5)(), (C.c_double * 5)()
+        check(lib().spl_profile_read(self._h, ms, n, fl, by))
+        return {k: dict(ms=ms[i], launches=n[i], flops=fl[i], bytes=by[i])
+                for i, k in enumerate(_lib.KCLASS)}
+
+    def launch_count(self, reset: bool = False) -> int:
+        v = C.c_int64()
+        check(lib().spl_launch_count(self._h, C.byref(v), int(reset)))
+        return v.value
+
+    def set_graphs(self, on: bool):
+        check(lib().spl_set_graphs(self._h, int(on)))
+
+
+# ---------------------------------------------------------------- reference-shaped API
+@dataclass
+class SeqparForward:
+    """Mirror of SeqparForward (block.hpp:136-154): output shards, per-rank ledgers, CommLog,
+    and the device layer holding the saved state."""
+    t: int
+    cfg: BlockConfig
+    y_shards: list
+    ledgers: list
+    comm: dict
+    layer: SeqparLayer = field(repr=False)
+
+
+@dataclass
+class SeqparBackward:
+    """Mirror of SeqparBackward (block.hpp:164-171)."""
+    dx_shards: list
+    param_grads: np.ndarray
+    w1_grad_shards: list
+    comm: dict
+
+
+def _to_dev(a: np.ndarray, dtype: str, device: int):
+    torch = _torch()
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device=f"cuda:{device}", dtype=_tdtype(dtype))
+
+
+def _to_host(t) -> np.ndarray:
+    return t.detach().to("cpu", dtype=_torch().float64).numpy()
+
+
+def seqpar_block_forward(x_shards: list, params: np.ndarray, t: int, cfg: BlockConfig,
+                         recompute: str = "none", sequence_parallel: bool = True,
+                         dtype: str = "f32", device: int = 0) -> SeqparForward:
+    """seqpar_block_forward(x_shards, params, t, cfg) (block.cpp:512-602) on the GPU."""
+    if t < 1:
+        raise ValueError("t must be >= 1")
+    if len(x_shards) != t:
+        raise ValueError("expected one input shard per rank")
+    layer = SeqparLayer(cfg, t, recompute, sequence_parallel, dtype, device)
+    layer.load_params(params)
+    for xs in x_shards:
+        if tuple(xs.shape) != layer.shard_shape():
+            raise ValueError("input shard must be {s/t, b, h}")
+    y = layer.forward([_to_dev(xs, dtype, device) for xs in x_shards])
+    ledgers = [layer.ledger(r) for r in range(t)]
+    return SeqparForward(t, cfg, [_to_host(v) for v in y], ledgers, layer.comm_log(), layer)
+
+
+def seqpar_block_backward(dy_shards: list, fwd: SeqparForward, params: np.ndarray) -> SeqparBackward:
+    """seqpar_block_backward(dy_shards, fwd, params) (block.cpp:622-749) on the GPU."""
+    layer = fwd.layer
+    if len(dy_shards) != fwd.t:
+        raise ValueError("expected one gradient shard per rank")
+    for d in dy_shards:
+        if tuple(d.shape) != layer.shard_shape():
+            raise ValueError("dy shard shape mismatch")
+    layer.comm_log_reset()
+    dx = layer.backward([_to_dev(d, layer.dtype, layer.device) for d in dy_shards])
+    return SeqparBackward([_to_host(v) for v in dx], layer.grads(),
+                          [layer.w1_grad_shard(r) for r in range(fwd.t)], layer.comm_log())
+
+
+def per_layer_bytes(a: int, h: int, s: int, b: int, t: int, kind: str, sequence_parallel: bool,
+                    act: int = 2, mask: int = 1) -> int:
+    """per_layer_bytes (activation_memory.cpp:79-82) through the C ABI."""
+    out = C.c_int64()
+    check(lib().spl_per_layer_bytes(a, h, s, b, t, _lib.RECOMPUTE[kind], int(sequence_parallel),
+                                    act, mask, C.byref(out)))
+    return out.value
+
+
+def per_layer_bytes_exact(a, h, s, b, t, kind, sequence_parallel, act=2, mask=1):
+    n, d = C.c_int64(), C.c_int64()
+    check(lib().spl_per_layer_bytes_exact(a, h, s, b, t, _lib.RECOMPUTE[kind], int(sequence_parallel),
+                                          act, mask, C.byref(n), C.byref(d)))
+    return n.value, d.value
