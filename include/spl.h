@@ -77,6 +77,12 @@ int spl_destroy(spl_handle* h);
 int spl_local_ranks(const spl_handle* h);
 const char* spl_last_error(void);
 
+/* Stream ordering: every call is asynchronous on an internal stream that first waits for
+ * all work previously issued on the caller stream and that the caller stream then waits on
+ * (event fork/join), so caller-stream producers/consumers of x, y, dy, dx need no extra
+ * synchronisation. Default caller stream: the legacy default stream (0). */
+int spl_set_stream(spl_handle* h, void* cuda_stream);
+
 /* Parameters. Replaces passing `const LayerParams&` (block.hpp:47-59) to every call:
  * the full-layout fp64 params are sliced per rank (shard_params, block.cpp:122-135) and
  * cast once. packed_f64 holds 12h²+13h doubles in named_tensors() order. */

@@ -60,6 +60,7 @@ def lib():
         "spl_destroy": (I32, [H]),
         "spl_local_ranks": (I32, [H]),
         "spl_last_error": (C.c_char_p, []),
+        "spl_set_stream": (I32, [H, VP]),
         "spl_load_params": (I32, [H, P(D)]),
         "spl_init_params": (I32, [H, C.c_uint64]),
         "spl_forward": (I32, [H, P(VP), P(VP)]),

@@ -113,6 +113,13 @@ int spl_destroy(spl_handle* h) {
 
 int spl_local_ranks(const spl_handle* h) { return h && h->layer ? h->layer->local_ranks() : 0; }
 
+int spl_set_stream(spl_handle* h, void* stream) {
+  return guard([&] {
+    check_handle(h);
+    h->layer->set_caller_stream(static_cast<cudaStream_t>(stream));
+  });
+}
+
 int spl_load_params(spl_handle* h, const double* p) {
   return guard([&] {
     check_handle(h);

@@ -61,8 +61,8 @@ class Layer final : public LayerBase {
     k_mlp_ = make_drop_key(d.seed, d.layer_index, kMlpDrop, d.microbatch, d.dropout_p);
     SPL_CUDA(cudaSetDevice(dev_));
     SPL_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
-    SPL_CUDA(cudaEventCreate(&tstart_));
-    SPL_CUDA(cudaEventCreate(&tstop_));
+    SPL_CUDA(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming));
+    SPL_CUDA(cudaEventCreateWithFlags(&ev_out_, cudaEventDisableTiming));
     allocate();
   }
 
@@ -72,12 +72,24 @@ class Layer final : public LayerBase {
     for (auto& a : allocs_) cudaFree(a.ptr);
     if (pinned_) cudaFreeHost(pinned_);
     for (auto& e : evpool_) cudaEventDestroy(e);
-    cudaEventDestroy(tstart_);
-    cudaEventDestroy(tstop_);
+    cudaEventDestroy(ev_in_);
+    cudaEventDestroy(ev_out_);
     cudaStreamDestroy(st_);
   }
 
   int local_ranks() const override { return L_; }
+  void set_caller_stream(cudaStream_t s) override { caller_ = s; }
+
+  // fork: our stream waits for the caller's prior work; join: the caller waits for ours.
+  void enter() {
+    SPL_CUDA(cudaSetDevice(dev_));
+    SPL_CUDA(cudaEventRecord(ev_in_, caller_));
+    SPL_CUDA(cudaStreamWaitEvent(st_, ev_in_, 0));
+  }
+  void leave() {
+    SPL_CUDA(cudaEventRecord(ev_out_, st_));
+    SPL_CUDA(cudaStreamWaitEvent(caller_, ev_out_, 0));
+  }
   Comm& comm() override { return *comm_; }
   cudaStream_t stream() const override { return st_; }
 
@@ -168,7 +180,7 @@ class Layer final : public LayerBase {
 
   // ------------------------------------------------------------------ forward
   void forward(const void* const* x, void* const* y) override {
-    SPL_CUDA(cudaSetDevice(dev_));
+    enter();
     for (int r = 0; r < L_; ++r) {
       require(x[r] != nullptr && y[r] != nullptr, "expected one input shard per rank");
       SPL_CUDA(cudaMemcpyAsync(R_[r].x_s, x[r], (size_t)(RL_ * h_) * sizeof(T),
@@ -188,10 +200,11 @@ class Layer final : public LayerBase {
       }
     }
     have_fwd_ = true;
+    leave();
   }
 
   void backward(const void* const* dy, void* const* dx) override {
-    SPL_CUDA(cudaSetDevice(dev_));
+    enter();
     if (!have_fwd_) raise(5, "missing saved forward state");
     for (int r = 0; r < L_; ++r) require(dy[r] != nullptr && dx[r] != nullptr, "expected one gradient shard per rank");
     if (kind_ == SPL_RECOMPUTE_FULL) {
@@ -201,6 +214,7 @@ class Layer final : public LayerBase {
       run_forward(ys.data(), kRecompute, nullptr);
     }
     run_backward(dy, dx);
+    leave();
   }
 
   void step_host(const void* x, const void* dy, void* y, void* dx) override {
@@ -847,7 +861,8 @@ class Layer final : public LayerBase {
   float scale_ = 1.f;
   DropKey k_soft_{}, k_attn_{}, k_mlp_{};
   cudaStream_t st_ = nullptr;
-  cudaEvent_t tstart_ = nullptr, tstop_ = nullptr;
+  cudaEvent_t ev_in_ = nullptr, ev_out_ = nullptr;
+  cudaStream_t caller_ = 0;  // legacy default stream unless set
   std::vector<Rank> R_;
   std::vector<Alloc> allocs_;
   std::vector<T*> stage_;

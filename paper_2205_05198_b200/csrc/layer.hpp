@@ -51,6 +51,7 @@ class LayerBase {
   virtual int64_t launch_count(bool reset) = 0;
   virtual void set_graphs(bool on) = 0;
   virtual int local_ranks() const = 0;
+  virtual void set_caller_stream(cudaStream_t s) = 0;
 };
 
 std::unique_ptr<LayerBase> make_layer(const spl_layer_desc& d, int device,

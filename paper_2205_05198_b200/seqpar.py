@@ -122,8 +122,13 @@ class SeqparLayer:
         check(lib().spl_init_params(self._h, seed))
 
     # ---- compute (device tensors)
+    def _bind_stream(self):
+        torch = _torch()
+        check(lib().spl_set_stream(self._h, C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+
     def forward(self, x: list, y: list | None = None) -> list:
         torch = _torch()
+        self._bind_stream()
         if len(x) != self.local:
             raise ValueError("expected one input shard per rank")
         for xi in x:
@@ -138,6 +143,7 @@ class SeqparLayer:
 
     def backward(self, dy: list, dx: list | None = None) -> list:
         torch = _torch()
+        self._bind_stream()
         if len(dy) != self.local:
             raise ValueError("expected one gradient shard per rank")
         for di in dy:

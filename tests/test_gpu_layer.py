@@ -60,13 +60,22 @@ def run(spl, cfg, t, p, x, dy, recompute="none", sp=True, dtype="f32"):
     return L, cat(y), cat(dx), L.grads()
 
 
+def grads_close(orc, h, got, want, tol):
+    """Per-tensor rel-L2, the denominator floored at 3% of a global-RMS-sized tensor, so
+    tensors whose exact gradient is ~0 (the key bias: softmax is shift-invariant, its fp64
+    gradient is 1e-15) compare on the layer's gradient scale instead of on rounding noise."""
+    G, R = orc.unpack(h, got), orc.unpack(h, want)
+    rms = float(np.sqrt(np.mean(want ** 2)))
+    for name in G:
+        err = np.linalg.norm(G[name] - R[name])
+        assert err <= tol * (np.linalg.norm(R[name]) + 0.03 * rms * np.sqrt(R[name].size)), (name, err)
+
+
 def check_f32(spl, orc, res, ref, p):
     L, y, dx, g = res
     assert np.max(np.abs(y - ref.y)) <= 1e-5 * np.max(np.abs(ref.y))
     assert rel_l2(dx, ref.dx) <= 1e-4
-    G, R = orc.unpack(256 if False else L.cfg.hidden, g), orc.unpack(L.cfg.hidden, ref.grads)
-    for name in G:
-        assert rel_l2(G[name], R[name]) <= 1e-4, name
+    grads_close(orc, L.cfg.hidden, g, ref.grads, 1e-4)
 
 
 @pytest.mark.parametrize("t", [1, 2, 4])
@@ -121,9 +130,7 @@ def test_tiny_bf16_parity(spl, orc, t, recompute):
     L, y, dx, g = run(spl, cfg, t, p, x, dy, recompute, dtype="bf16")
     assert rel_l2(y, ref.y) <= 1e-2
     assert rel_l2(dx, ref.dx) <= 1e-2
-    G, R = orc.unpack(cfg.hidden, g), orc.unpack(cfg.hidden, ref.grads)
-    for name in G:
-        assert rel_l2(G[name], R[name]) <= 2e-2, name
+    grads_close(orc, cfg.hidden, g, ref.grads, 2e-2)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
