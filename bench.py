@@ -1,0 +1,318 @@
+"""Layer fwd+bwd benchmark of the B200 sequence-parallel layer (arXiv 2205.05198 hot path).
+
+    python bench.py --gpus N --steps K --warmup W            # our arm (t = N, one rank/GPU)
+    python bench.py --impl reference --gpus N ...             # the reference CPU path
+
+Workload (BASELINE.json configs[1]): the 22B-shape layer h=6144 a=64 s=2048 b=4, bf16,
+dropout p=0.1, sequence parallel + selective recomputation, tensor-parallel degree t = N
+(N=1: the whole layer on one GPU). A step = one layer forward + backward over one micro-batch
+(s·b = 8192 tokens). value = tokens/s of the whole t-group = s·b / step time (max over ranks).
+Inputs are synthetic (seeded U(-1,1)); params are LayerParams::random generated on the device.
+The per-step working set (0.9 GB of weights alone at t=1) exceeds the 126 MB L2, so no
+explicit flush is done between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {  # name: (heads, hidden, seq, batch)
+    "tiny": (8, 256, 128, 2),
+    "22B": (64, 6144, 2048, 4),
+    "175B": (96, 12288, 2048, 1),
+    "530B": (128, 20480, 2048, 1),
+    "1T": (160, 25600, 2048, 1),
+}
+METRIC = "layer fwd+bwd tokens/s & MFU at t=1/2/4/8; activation bytes/GPU vs 34sbh/t"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def model_flops(a, h, s, b):
+    # flops.cpp:29-34 x3 (fwd + bwd): 72 b s h^2 + 12 b s^2 h per layer (whole t-group)
+    return 72.0 * b * s * h * h + 12.0 * b * s * s * h
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline_sample(cfg_name, threads=0):
+    """The oracle (fp64 restatement of the reference seqpar layer, test infrastructure) timed
+    on the host cores on a bounded sample of the workload: the same layer width (h, a) with
+    one sequence of s_sample tokens; fwd+bwd, tokens/s."""
+    import oracle as orc
+    a, h, s, b = CONFIGS[cfg_name]
+    s_sample = min(s, 512) if cfg_name != "tiny" else s
+    b_sample = 1 if cfg_name != "tiny" else b
+    cores = orc.set_threads(threads)
+    cfg = orc.BlockConfig(heads=a, hidden=h, seq=s_sample, batch=b_sample, dropout_p=0.1, seed=42)
+    p = orc.params_random(h, 7)
+    x = orc.random_uniform(1, (s_sample, b_sample, h), -1, 1)
+    dy = orc.random_uniform(2, (s_sample, b_sample, h), -1, 1)
+    t0 = time.perf_counter()
+    orc.seqpar_layer(cfg, 1, p, x, dy)
+    dt = time.perf_counter() - t0
+    return {"value": s_sample * b_sample / dt, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "sample": f"oracle fp64 seqpar fwd+bwd, h={h} a={a} s={s_sample} b={b_sample}, t=1 "
+                      f"({dt:.2f} s)", "seconds": dt}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (the oracle port — the reference needs
+    Eigen/Boost, absent here) on all host threads, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as orc
+    a, h, s, b = CONFIGS[args.config]
+    s_sample = min(s, 512) if args.config != "tiny" else s
+    b_sample = 1 if args.config != "tiny" else b
+    cores = orc.set_threads(0)
+    cfg = orc.BlockConfig(heads=a, hidden=h, seq=s_sample, batch=b_sample, dropout_p=0.1, seed=42)
+    p = orc.params_random(h, 7)
+    x = orc.random_uniform(1, (s_sample, b_sample, h), -1, 1)
+    dy = orc.random_uniform(2, (s_sample, b_sample, h), -1, 1)
+    budget = 150.0  # seconds for the whole run
+    t0 = time.perf_counter()
+    orc.seqpar_layer(cfg, 1, p, x, dy)
+    one = time.perf_counter() - t0
+    steps = max(1, min(args.steps, int(budget / max(one, 1e-3)) - min(args.warmup, 1)))
+    for _ in range(max(0, min(args.warmup, 1) - 1)):
+        orc.seqpar_layer(cfg, 1, p, x, dy)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        orc.seqpar_layer(cfg, 1, p, x, dy)
+    dt = (time.perf_counter() - t0) / steps
+    v = s_sample * b_sample / dt
+    sample = (f"oracle fp64 seqpar fwd+bwd (reference algorithm; reference build needs Eigen3/"
+              f"Boost, absent), h={h} a={a} s={s_sample} b={b_sample} t=1, {steps} steps")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": steps, "warmup": min(args.warmup, 1),
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} layer fwd+bwd (sampled)", "heads": a, "hidden": h,
+                       "seq": s, "batch": b},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="22B", choices=list(CONFIGS))
+    ap.add_argument("--recompute", default="selective", choices=["none", "selective", "full"])
+    ap.add_argument("--no-sp", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import paper_2205_05198_b200 as spl
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    t = world
+    assert t == args.gpus or world == 1, "launch one process per GPU (torchrun) for --gpus > 1"
+    torch.cuda.set_device(local_rank)
+    dist = None
+    nccl = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        uid = [spl.SeqparLayer.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        nccl = (rank, uid[0])
+    a, h, s, b = CONFIGS[args.config]
+    sp = not args.no_sp
+    cfg = spl.BlockConfig(a, h, s, b, dropout_p=0.1, causal=False, seed=42)
+    L = spl.SeqparLayer(cfg, t, args.recompute, sp, "bf16", device=local_rank,
+                        check_finite=False, nccl=nccl)
+    L.init_params(1234)
+    shp = L.shard_shape()
+    gen = torch.Generator(device=f"cuda:{local_rank}").manual_seed(100 + rank)
+    x = [(torch.rand(shp, generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)]
+    dy = [(torch.rand(shp, generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)]
+    y = [torch.empty_like(x[0])]
+    dx = [torch.empty_like(x[0])]
+
+    def step():
+        L.forward(x, y)
+        L.backward(dy, dx)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    L.launch_count(reset=True)
+    # device-timed region on the layer's stream (forward/backward join the caller stream)
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(args.steps):
+        step()
+    stop.record()
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(stop)
+    launches = L.launch_count(reset=True)
+    clk = clocks.stop()
+    if dist is not None:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / args.steps
+    tokens = s * b
+    value = tokens / (ms_step / 1e3)
+
+    # per-kernel-class times: a second pass with events around every launch
+    barrier()
+    L.profile(True)
+    for _ in range(args.steps):
+        step()
+    prof = L.profile_read()
+    L.profile(False)
+
+    # end-to-end through the host-buffer C-ABI call (H2D x,dy + D2H y,dx every step)
+    e2e = None
+    if not args.no_e2e:
+        nbytes = x[0].numel() * 2
+        hx = x[0].cpu().pin_memory()
+        hdy = dy[0].cpu().pin_memory()
+        hy = torch.empty_like(hx).pin_memory()
+        hdx = torch.empty_like(hx).pin_memory()
+        L.step_host(hx, hdy, hy, hdx)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            L.step_host(hx, hdy, hy, hdx)
+        el = time.perf_counter() - t0
+        if dist is not None:
+            tt = torch.tensor([el], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            el = float(tt.item())
+        e2e = {"value": tokens / (el / args.steps), "unit": "tokens/s",
+               "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": 2 * nbytes}
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    pk, pk_kind = peaks()
+    g = prof["gemm"]
+    gemm_tflops = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
+    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    total_prof_ms = sum(v["ms"] for v in prof.values())
+    led, phys, unc = L.saved_bytes(0)
+    mf = model_flops(a, h, s, b)
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded U(-1,1) inputs, LayerParams::random on device)",
+        "config": {"workload": f"{args.config}-shape layer fwd+bwd, t={t}, SP={'on' if sp else 'off'}, "
+                               f"{args.recompute} recompute",
+                   "heads": a, "hidden": h, "seq": s, "batch": b, "t": t, "dropout_p": 0.1,
+                   "causal": False, "parallelism": f"tp{t}+sp" if sp else f"tp{t}",
+                   "l2": "working set > L2 (weights alone 0.9 GB/t); no flush"},
+        "mfu": mf / (ms_step / 1e3) / t / (peak * 1e12),
+        "mfu_vs_nominal_2250": mf / (ms_step / 1e3) / t / 2.25e15,
+        "activation_bytes_per_gpu": {"ledger": led, "physical": phys, "uncounted_stats": unc,
+                                     "formula_34sbh_over_t": 34 * s * b * h // t,
+                                     "per_layer_bytes": spl.per_layer_bytes(a, h, s, b, t, args.recompute, sp)},
+        "roofline": {"kernel": "tcgen05 GEMM (all layer GEMMs)", "bound": "tensor",
+                     "achieved": gemm_tflops, "peak": peak, "unit": "TFLOP/s",
+                     "frac": gemm_tflops / peak if peak else None, "traffic": None,
+                     "peak_kind": f"{pk_kind} bf16_tflops_sustained",
+                     "share_of_step": g["ms"] / total_prof_ms if total_prof_ms else None},
+        "kernel_classes": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                               "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] and v["flops"] else None,
+                               "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] and v["bytes"] else None}
+                           for k, v in prof.items()},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if args.gpus == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline_sample(args.config)
+        cb.pop("seconds", None)
+        line["cpu_baseline"] = cb
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

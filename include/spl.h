@@ -161,6 +161,16 @@ int spl_profile_read(spl_handle* h, double ms[5], int64_t launches[5], double fl
 /* Number of kernel launches of this library recorded since the last reset. */
 int spl_launch_count(spl_handle* h, int64_t* count, int reset);
 
+/* Kernel-level entry (tests / microbenchmarks): C[M,N] = A[M,K]·B[K,N] in bf16 with fp32
+ * accumulation on the layer's GEMM kernels. A(m,k) = A[m*lda+k] (a_mn=0) or A[k*lda+m]
+ * (a_mn=1); B(k,n) = B[n*ldb+k] (b_mn=0) or B[k*ldb+n] (b_mn=1). epi: 0 store, 1 +bias,
+ * 2 +bias and GELU (second output C2), 3 ×GELU'(aux), 4 fp32 output. Device pointers;
+ * asynchronous on `stream`. Returns the backend used in *backend (1 = tcgen05). */
+int spl_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int a_mn,
+                  const void* B, int64_t ldb, int b_mn, void* C, int64_t ldc, int epi,
+                  const float* bias, void* C2, const void* aux, int64_t ldaux, void* stream,
+                  int* backend);
+
 /* Capture forward+backward into CUDA graphs after the first call (1) or run eagerly (0). */
 int spl_set_graphs(spl_handle* h, int on);
 

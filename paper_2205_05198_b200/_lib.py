@@ -83,6 +83,8 @@ def lib():
         "spl_profile_read": (I32, [H, P(D), P(I64), P(D), P(D)]),
         "spl_launch_count": (I32, [H, P(I64), I32]),
         "spl_set_graphs": (I32, [H, I32]),
+        "spl_gemm_bf16": (I32, [I64, I64, I64, VP, I64, I32, VP, I64, I32, VP, I64, I32, VP, VP,
+                                VP, I64, VP, P(I32)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

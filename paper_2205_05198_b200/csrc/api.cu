@@ -311,4 +311,21 @@ int spl_set_graphs(spl_handle* h, int on) {
   });
 }
 
+int spl_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int a_mn,
+                  const void* B, int64_t ldb, int b_mn, void* C, int64_t ldc, int epi,
+                  const float* bias, void* C2, const void* aux, int64_t ldaux, void* stream,
+                  int* backend) {
+  return guard([&] {
+    spl::require(epi >= 0 && epi <= 4, "unknown epilogue");
+    spl::k::GemmArgs g;
+    g.M = M; g.N = N; g.K = K;
+    g.A = A; g.lda = lda; g.amaj = a_mn ? spl::k::Major::MN : spl::k::Major::K;
+    g.B = B; g.ldb = ldb; g.bmaj = b_mn ? spl::k::Major::MN : spl::k::Major::K;
+    g.C = C; g.ldc = ldc; g.epi = (spl::k::Epi)epi;
+    g.bias = bias; g.C2 = C2; g.aux = aux; g.ldaux = ldaux;
+    if (backend) *backend = spl::k::gemm_backend<spl::bf16>(g);
+    spl::k::gemm<spl::bf16>(g, static_cast<cudaStream_t>(stream));
+  });
+}
+
 }  // extern "C"

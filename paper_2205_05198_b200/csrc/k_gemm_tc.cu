@@ -1,7 +1,450 @@
-// tcgen05 / TMEM / TMA bf16 GEMM for sm_100a (placeholder until the kernel lands).
-#include "kernels.hpp"
+// bf16 GEMM on the 5th-generation tensor cores (sm_100a): TMA -> shared memory (128B swizzle)
+// -> tcgen05.mma (single elected thread) -> fp32 accumulator in TMEM -> tcgen05.ld epilogue
+// with the fused layer epilogues (bias, bias+GELU dual output, GELU-backward, fp32 wgrad).
+//
+// One kernel template covers the three GEMM orientations of the layer
+// (C[M,N] = A[M,K]·B[K,N]):
+//   forward  (QKV, proj, FC1, FC2):  A K-major (activations),  B MN-major (weights [in,out])
+//   dgrad    (dY·Wᵀ):                A K-major,                 B K-major
+//   wgrad    (Xᵀ·dY):                A MN-major,                B MN-major
+// The majorness is a UMMA instruction-descriptor bit plus the matching smem descriptor
+// (LBO/SBO) and TMA box, so no operand is ever transposed in memory.
+//
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
+// warps 2..5 = epilogue (warp w reads TMEM lanes 32*(w%4)..+31 = tile rows).
+// Tile 128 x BN x 64, STAGES-deep mbarrier ring between TMA and MMA.
+#include <cuda.h>
+
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "gemm_epilogue.cuh"
 
 namespace spl::k {
-bool gemm_tc_supported(const GemmArgs&) { return false; }
-void gemm_tc(const GemmArgs&, cudaStream_t) { raise(3, "tcgen05 gemm not built"); }
+
+namespace {
+
+constexpr int BM = 128, BK = 64, UK = 16;
+constexpr int kThreads = 192;
+
+template <int BN>
+struct TileCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = BN;  // fp32 accumulator, one column per N
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// 32 consecutive fp32 columns of this thread's TMEM lane.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 version bits.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;  // layout: SWIZZLE_128B
+  return d;
+}
+
+// kind::f16 instruction descriptor: fp32 accumulate, bf16 A/B, majorness, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// ------------------------------------------------------------------ epilogue store
+template <int EPI>
+__device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t m, int64_t n0,
+                                            const float (&v)[32]) {
+  if (m >= g.M) return;
+  const bool full = n0 + 32 <= g.N;
+  if constexpr (EPI == (int)Epi::F32) {
+    float* c = static_cast<float*>(g.C) + m * g.ldc + n0;
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4)
+        *reinterpret_cast<float4*>(c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
+      for (int i = 0; i < 32 && n0 + i < g.N; ++i) c[i] = v[i];
+    }
+    return;
+  } else {
+    float o[32];
+    float o2[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[i] = v[i];
+    if constexpr (EPI == (int)Epi::Bias || EPI == (int)Epi::BiasGelu) {
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 b = *reinterpret_cast<const float4*>(g.bias + n0 + i);
+          o[i] += b.x; o[i + 1] += b.y; o[i + 2] += b.z; o[i + 3] += b.w;
+        }
+      } else {
+        for (int i = 0; i < 32 && n0 + i < g.N; ++i) o[i] += g.bias[n0 + i];
+      }
+    }
+    if constexpr (EPI == (int)Epi::BiasGelu) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float pre = __bfloat162float(__float2bfloat16_rn(o[i]));
+        o2[i] = gelu_erf(pre);
+      }
+    }
+    if constexpr (EPI == (int)Epi::GeluBwd) {
+      const bf16* ax = static_cast<const bf16*>(g.aux) + m * g.ldaux + n0;
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          const uint4 t = *reinterpret_cast<const uint4*>(ax + i);
+          const bf16* e = reinterpret_cast<const bf16*>(&t);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[i + j] *= gelu_erf_grad(__bfloat162float(e[j]));
+        }
+      } else {
+        for (int i = 0; i < 32 && n0 + i < g.N; ++i) o[i] *= gelu_erf_grad(__bfloat162float(ax[i]));
+      }
+    }
+    bf16* c = static_cast<bf16*>(g.C) + m * g.ldc + n0;
+    bf16* c2 = EPI == (int)Epi::BiasGelu ? static_cast<bf16*>(g.C2) + m * g.ldc + n0 : nullptr;
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 t;
+        bf16* e = reinterpret_cast<bf16*>(&t);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e[j] = __float2bfloat16_rn(o[i + j]);
+        *reinterpret_cast<uint4*>(c + i) = t;
+        if constexpr (EPI == (int)Epi::BiasGelu) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) e[j] = __float2bfloat16_rn(o2[i + j]);
+          *reinterpret_cast<uint4*>(c2 + i) = t;
+        }
+      }
+    } else {
+      for (int i = 0; i < 32 && n0 + i < g.N; ++i) {
+        c[i] = __float2bfloat16_rn(o[i]);
+        if constexpr (EPI == (int)Epi::BiasGelu) c2[i] = __float2bfloat16_rn(o2[i]);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ the kernel
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_b, const GemmArgs g) {
+  using Cfg = TileCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* tiles = smem;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + Cfg::STAGES;
+  uint64_t* tmem_full = empty_bar + Cfg::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int nk = (int)((g.K + BK - 1) / BK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"((uint32_t)Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % Cfg::STAGES;
+        const uint32_t ph = (uint32_t)(kb / Cfg::STAGES) & 1u;
+        mbar_wait(&empty_bar[s], ph ^ 1u);
+        uint8_t* sa = tiles + s * Cfg::STAGE_BYTES;
+        uint8_t* sb = sa + Cfg::A_BYTES;
+        mbar_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
+        const int k0 = kb * BK;
+        if (A_MN) {  // [K rows][M cols]: two 64-wide M atoms of 64 k-rows
+          tma_load_2d(sa, &map_a, &full_bar[s], (int)m0, k0);
+          tma_load_2d(sa + 8192, &map_a, &full_bar[s], (int)m0 + 64, k0);
+        } else {  // [M rows][K cols]: one 128-row box
+          tma_load_2d(sa, &map_a, &full_bar[s], k0, (int)m0);
+        }
+        if (B_MN) {  // [K rows][N cols]: BN/64 atoms
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j)
+            tma_load_2d(sb + j * 8192, &map_b, &full_bar[s], (int)n0 + 64 * j, k0);
+        } else {  // [N rows][K cols]: one BN-row box
+          tma_load_2d(sb, &map_b, &full_bar[s], k0, (int)n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = make_idesc(BM, BN, A_MN, B_MN);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % Cfg::STAGES;
+        const uint32_t ph = (uint32_t)(kb / Cfg::STAGES) & 1u;
+        mbar_wait(&full_bar[s], ph);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(tiles + s * Cfg::STAGE_BYTES);
+        const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / UK; ++kk) {
+          // K-major: advance 16 elements (32 B) inside the 128 B swizzle row;
+          // MN-major: advance 16 k-rows (2 KB), i.e. two 8-row core-matrix groups.
+          const uint64_t ad = A_MN ? smem_desc(sa + kk * 2048, 8192, 1024)
+                                   : smem_desc(sa + kk * 32, 16, 1024);
+          const uint64_t bd = B_MN ? smem_desc(sb + kk * 2048, 8192, 1024)
+                                   : smem_desc(sb + kk * 32, 16, 1024);
+          umma_bf16(tmem_base, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+        }
+        umma_commit(&empty_bar[s]);  // frees the smem stage once these MMAs have read it
+      }
+      umma_commit(tmem_full);  // accumulator complete
+    }
+  } else {
+    // ---------------- epilogue: TMEM -> registers -> fused op -> global
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row = q * 32 + lane;
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float v[32];
+      tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), v);
+      if (n0 + c * 32 < g.N) store_chunk<EPI>(g, m0 + row, n0 + c * 32, v);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"((uint32_t)Cfg::TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SPL_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (p == nullptr || q != cudaDriverEntryPointSuccess)
+      raise(3, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  return fn;
+}
+
+struct MapKey {
+  const void* ptr;
+  uint64_t inner, outer, ld;
+  uint32_t box0, box1;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && inner == o.inner && outer == o.outer && ld == o.ld && box0 == o.box0 &&
+           box1 == o.box1;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = std::hash<const void*>()(k.ptr);
+    h ^= std::hash<uint64_t>()(k.inner * 1315423911u + k.outer * 2654435761u + k.ld) + 0x9e3779b9 +
+         (h << 6) + (h >> 2);
+    h ^= (size_t)k.box0 * 31 + k.box1;
+    return h;
+  }
+};
+
+// 2-D bf16 tensor map over a row-major matrix [outer][inner] with row stride ld elements.
+CUtensorMap make_map(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box0,
+                     uint32_t box1) {
+  static std::mutex mu;
+  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  const MapKey key{ptr, inner, outer, ld, box0, box1};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {box0, box1};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(3, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, m);
+  return m;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+void launch_tc(const GemmArgs& g, cudaStream_t st) {
+  using Cfg = TileCfg<BN>;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI>;
+  static bool attr = [&] {
+    SPL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    return true;
+  }();
+  (void)attr;
+  // A: K-major [M][K] boxes {64, 128}; MN-major [K][M] boxes {64, 64}
+  const CUtensorMap ma = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64, BK)
+                              : make_map(g.A, g.K, g.M, g.lda, BK, BM);
+  const CUtensorMap mb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, BK)
+                              : make_map(g.B, g.K, g.N, g.ldb, BK, BN);
+  dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM));
+  kern<<<grid, kThreads, Cfg::SMEM, st>>>(ma, mb, g);
+  SPL_CHECK_LAUNCH();
+}
+
+template <int BN>
+void dispatch_bn(const GemmArgs& g, cudaStream_t st) {
+  const bool amn = g.amaj == Major::MN, bmn = g.bmaj == Major::MN;
+  switch (g.epi) {
+    case Epi::Store:
+      if (!amn && bmn) return launch_tc<BN, false, true, (int)Epi::Store>(g, st);
+      if (!amn && !bmn) return launch_tc<BN, false, false, (int)Epi::Store>(g, st);
+      break;
+    case Epi::Bias:
+      if (!amn && bmn) return launch_tc<BN, false, true, (int)Epi::Bias>(g, st);
+      break;
+    case Epi::BiasGelu:
+      if (!amn && bmn) return launch_tc<BN, false, true, (int)Epi::BiasGelu>(g, st);
+      break;
+    case Epi::GeluBwd:
+      if (!amn && !bmn) return launch_tc<BN, false, false, (int)Epi::GeluBwd>(g, st);
+      break;
+    case Epi::F32:
+      if (amn && bmn) return launch_tc<BN, true, true, (int)Epi::F32>(g, st);
+      break;
+  }
+  raise(3, "gemm_tc: unsupported operand majors for this epilogue");
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+}  // namespace
+
+bool gemm_tc_supported(const GemmArgs& g) {
+  if (g.M < 1 || g.N < 32 || g.K < 1) return false;
+  if (g.N % 32 != 0) return false;
+  if (g.lda % 8 || g.ldb % 8 || g.ldc % 8) return false;
+  if (!aligned16(g.A) || !aligned16(g.B) || !aligned16(g.C)) return false;
+  if (g.epi == Epi::BiasGelu && !aligned16(g.C2)) return false;
+  if (g.epi == Epi::GeluBwd && (g.ldaux % 8 || !aligned16(g.aux))) return false;
+  const bool amn = g.amaj == Major::MN, bmn = g.bmaj == Major::MN;
+  switch (g.epi) {
+    case Epi::Store: return !amn;
+    case Epi::Bias:
+    case Epi::BiasGelu: return !amn && bmn;
+    case Epi::GeluBwd: return !amn && !bmn;
+    case Epi::F32: return amn && bmn;
+  }
+  return false;
+}
+
+void gemm_tc(const GemmArgs& g, cudaStream_t st) {
+  if (g.N >= 256) dispatch_bn<256>(g, st);
+  else dispatch_bn<128>(g, st);
+}
+
 }  // namespace spl::k

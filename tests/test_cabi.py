@@ -12,7 +12,7 @@ from paper_2205_05198_b200 import _lib
 def test_library_loads_and_exports_header():
     L = spl.lib()
     syms = _lib.header_symbols()
-    assert len(syms) >= 30
+    assert len(syms) >= 31
     for s in syms:
         assert hasattr(L, s), s
     out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout

@@ -1,0 +1,81 @@
+"""tcgen05 GEMM (k_gemm_tc.cu) against an fp64 torch product of the same bf16 operands, for
+the three orientations and five fused epilogues the layer uses, including M/N/K tails.
+Tolerances: fp32-output (wgrad) rel-L2 <= 1e-5; bf16 outputs rel-L2 <= 5e-3 (one bf16
+rounding of the result)."""
+import ctypes as C
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2205_05198_b200 as spl
+    return spl, torch
+
+
+def gelu(x, torch):
+    return 0.5 * x * (1 + torch.erf(x / 2 ** 0.5))
+
+
+def gelu_grad(x, torch):
+    return 0.5 * (1 + torch.erf(x / 2 ** 0.5)) + x * torch.exp(-0.5 * x * x) / (2 * torch.pi) ** 0.5
+
+
+def run_gemm(spl, torch, M, N, K, a_mn, b_mn, epi, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    A = (torch.rand((K, M) if a_mn else (M, K), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    B = (torch.rand((K, N) if b_mn else (N, K), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    Am = (A.t() if a_mn else A).double()
+    Bm = (B if b_mn else B.t()).double()
+    ref = Am @ Bm
+    bias = (torch.rand(N, generator=g, device="cuda") - 0.5).float()
+    aux = (torch.rand((M, N), generator=g, device="cuda") * 4 - 2).to(torch.bfloat16)
+    out_dt = torch.float32 if epi == 4 else torch.bfloat16
+    Cm = torch.full((M, N), float("nan"), device="cuda", dtype=out_dt)
+    C2 = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    backend = C.c_int(-1)
+    rc = spl.lib().spl_gemm_bf16(M, N, K, A.data_ptr(), A.shape[1], int(a_mn), B.data_ptr(), B.shape[1],
+                                 int(b_mn), Cm.data_ptr(), N, epi, C.cast(bias.data_ptr(), C.POINTER(C.c_float)),
+                                 C2.data_ptr(), aux.data_ptr(), N,
+                                 C.c_void_p(torch.cuda.current_stream().cuda_stream), C.byref(backend))
+    assert rc == 0, spl.lib().spl_last_error()
+    torch.cuda.synchronize()
+    if epi in (1, 2):
+        ref = ref + bias.double()
+    if epi == 3:
+        ref = ref * gelu_grad(aux.double(), torch)
+    return backend.value, Cm.double(), C2.double(), ref
+
+
+def rel(a, b):
+    return float((a - b).norm() / b.norm())
+
+
+SHAPES = [(128, 256, 64), (256, 768, 256), (200, 96, 72), (384, 1024, 520), (1024, 2304, 768), (136, 320, 1000)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("orient,epis", [((False, True), (0, 1, 2)), ((False, False), (0, 3)), ((True, True), (4,))])
+def test_gemm_tc(env, M, N, K, orient, epis):
+    spl, torch = env
+    for epi in epis:
+        be, out, out2, ref = run_gemm(spl, torch, M, N, K, *orient, epi)
+        assert be == 1, "expected the tcgen05 backend"
+        assert not torch.isnan(out).any()
+        tol = 1e-5 if epi == 4 else 5e-3
+        assert rel(out, ref) <= tol, (epi, rel(out, ref))
+        if epi == 2:
+            assert rel(out2, gelu(out, torch)) <= 5e-3
+
+
+def test_gemm_large_k(env):
+    spl, torch = env
+    be, out, _, ref = run_gemm(spl, torch, 512, 512, 6144, False, True, 0)
+    assert be == 1 and rel(out, ref) <= 5e-3
+    be, out, _, ref = run_gemm(spl, torch, 512, 256, 8192, True, True, 4)
+    assert be == 1 and rel(out, ref) <= 1e-5
