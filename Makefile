@@ -1,9 +1,6 @@
 # libspl: B200 (sm_100a) sequence-parallel layer. `make -j` builds the shared library in-tree
 # (it travels to the GPU box with the gpurun snapshot) plus the oracle checker.
 NVCC ?= /usr/local/cuda/bin/nvcc
-ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
-           --expt-relaxed-constexpr -Iinclude $(NCCL_INC) -Xptxas -warn-spills
 # NCCL: the torch-bundled 2.28 (same soname libnccl.so.2 as the system 2.27) so that libspl and
 # torch share one NCCL in a process whichever loads first.
 NCCL_HOME ?= $(shell python -c "import nvidia.nccl as n; print(list(n.__path__)[0])" 2>/dev/null)
@@ -14,6 +11,9 @@ else
 NCCL_INC := -I$(NCCL_HOME)/include
 NCCL_LINK := -L$(NCCL_HOME)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_HOME)/lib
 endif
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
+           --expt-relaxed-constexpr -Iinclude $(NCCL_INC) -Xptxas -warn-spills
 PKG := paper_2205_05198_b200
 SRC := $(wildcard $(PKG)/csrc/*.cu)
 OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))

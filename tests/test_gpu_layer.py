@@ -272,3 +272,19 @@ def test_facade_reference_api(spl, orc):
     w1 = orc.unpack(cfg.hidden, ref.grads)["w1"]
     for r in range(2):
         assert rel_l2(back.w1_grad_shards[r], w1[:, r * 512:(r + 1) * 512]) <= 1e-4
+
+
+@pytest.mark.parametrize("shape,t,causal", [
+    (dict(heads=8, hidden=768, seq=256, batch=2), 1, False),    # head_dim 96 (22B)
+    (dict(heads=8, hidden=1024, seq=192, batch=1), 2, True),    # head_dim 128 (175B), s tail
+    (dict(heads=8, hidden=1280, seq=256, batch=1), 2, False),   # head_dim 160 (530B / 1T)
+    (dict(heads=4, hidden=256, seq=160, batch=3), 1, True),     # head_dim 64, s tail
+])
+@pytest.mark.parametrize("recompute", ["selective", "none"])
+def test_bf16_head_dims(spl, orc, shape, t, causal, recompute):
+    cfg, x, dy, p = make_case(orc, shape, causal=causal, key=7)
+    ref = orc.seqpar_layer(cfg, t, p, x, dy)
+    L, y, dx, g = run(spl, cfg, t, p, x, dy, recompute, dtype="bf16")
+    assert rel_l2(y, ref.y) <= 1e-2
+    assert rel_l2(dx, ref.dx) <= 1e-2
+    grads_close(orc, cfg.hidden, g, ref.grads, 2e-2)
