@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kWarps * 32) attn_bwd_dkdv_k(AttnArgs a,
 template <typename T>
 void attn_fwd(const AttnArgs& a, cudaStream_t st) {
   require(a.hd <= kMaxHD, "attention: head_dim > 256 unsupported");
-  if (a.sm == nullptr && attn_tc_supported<T>(a)) {
+  if (attn_tc_supported<T>(a)) {
     attn_fwd_tc<T>(a, st);
     return;
   }
@@ -344,7 +344,7 @@ void attn_fwd(const AttnArgs& a, cudaStream_t st) {
 template <typename T>
 void attn_bwd(const AttnArgs& a, const void* dout, void* dqkv, float* delta, cudaStream_t st) {
   require(a.hd <= kMaxHD, "attention: head_dim > 256 unsupported");
-  if (a.sm == nullptr && attn_tc_supported<T>(a)) {
+  if (attn_tc_supported<T>(a)) {
     attn_bwd_tc<T>(a, dout, dqkv, delta, st);
     return;
   }

@@ -73,64 +73,87 @@ __device__ __forceinline__ void load_tile(bf16* sm, const bf16* base, int64_t r0
   }
 }
 
+// ---------------------------------------------------------------- counter RNG, hot-loop form
+// keep(i) = (hash_counter(folded, i) >> 11) >= ceil(p*2^53)  (rng.cpp:31-37, block.cpp:63)
+//   hash_counter(k, i) = mix64(mix64(k) ^ mix64(i + C)),  mix64(x) = post(x + G)
+// With base = row_index*s + C + G precomputed per row, one element costs
+//   post(base + key) ^ mixed, + G, post, 64-bit compare against thresh << 11.
+constexpr uint64_t kG = 0x9e3779b97f4a7c15ULL;
+constexpr uint64_t kC = 0x632be59bd9b4e019ULL;
+// x * C mod 2^64 in three 32-bit multiplies (IMAD.WIDE + 2 IMAD)
+template <uint64_t C>
+__device__ __forceinline__ uint64_t mulc(uint64_t x) {
+  const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+  const uint64_t w = (uint64_t)xl * (uint32_t)C;
+  const uint32_t hi = (uint32_t)(w >> 32) + xl * (uint32_t)(C >> 32) + xh * (uint32_t)C;
+  return ((uint64_t)hi << 32) | (uint32_t)w;
+}
+__device__ __forceinline__ uint64_t mix_post(uint64_t x) {
+  x = mulc<0xbf58476d1ce4e5b9ULL>(x ^ (x >> 30));
+  x = mulc<0x94d049bb133111ebULL>(x ^ (x >> 27));
+  return x ^ (x >> 31);
+}
+// 2^x, one MUFU.EX2 (flush-to-zero; the softmax operands are <= 0)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+struct Rng {
+  uint64_t mixed;  // mix64(folded key)
+  uint64_t tsh;    // thresh << 11
+  bool on;         // p > 0
+  __device__ explicit Rng(const DropKey& k) : mixed(k.mixed), tsh(k.thresh << 11), on(k.thresh != 0) {}
+  __device__ __forceinline__ uint64_t row_base(uint64_t row_index, uint64_t s) const {
+    return row_index * s + kC + kG;
+  }
+  __device__ __forceinline__ bool keep(uint64_t base, uint32_t key) const {
+    if (!on) return true;
+    return mix_post((mix_post(base + key) ^ mixed) + kG) >= tsh;
+  }
+};
+
+// 8 bits at positions 0,4,...,28 of x -> bits 0..7
+__device__ __forceinline__ uint32_t compress4(uint32_t x) {
+  x &= 0x11111111u;
+  x = (x | (x >> 3)) & 0x03030303u;
+  x = (x | (x >> 6)) & 0x000F000Fu;
+  return (x | (x >> 12)) & 0xFFu;
+}
+
 // =====================================================================================
 // forward
 // =====================================================================================
-template <int HD>
+template <int HD, bool CAUSAL, bool MAT>
 __global__ void __launch_bounds__(128) fa_fwd(AttnArgs a) {
   constexpr int BM = 64, BN = 64, LDS = HD + 8, NT = 128;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   bf16* Qs = reinterpret_cast<bf16*>(smem_raw);
-  bf16* Ks = Qs + BM * LDS;           // [2][BN][LDS]
-  bf16* Vs = Ks + 2 * BN * LDS;       // [2][BN][LDS]
+  bf16* Ks = Qs + BM * LDS;      // [2][BN][LDS]
+  bf16* Vs = Ks + 2 * BN * LDS;  // [2][BN][LDS]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
-  const int64_t q0 = (int64_t)blockIdx.x * BM;
-  const int64_t hl = blockIdx.y / a.b, bj = blockIdx.y % a.b;
-  const bf16* qkv = static_cast<const bf16*>(a.qkv);
-  const bf16* base = qkv + bj * a.ld;  // row i of this batch at base + i*b*ld
+  const int q0 = blockIdx.x * BM;
+  const int hl = blockIdx.y / (int)a.b, bj = blockIdx.y % (int)a.b;
+  const int S = (int)a.s;
+  const bf16* base = static_cast<const bf16*>(a.qkv) + (int64_t)bj * a.ld;
   const int64_t rstride = a.b * a.ld;
-  const int64_t qcol = a.qoff + hl * HD, kcol = a.koff + hl * HD, vcol = a.voff + hl * HD;
-
-  const int64_t kv_end = a.causal ? (a.s < q0 + BM ? a.s : q0 + BM) : a.s;
-  const int nkv = (int)((kv_end + BN - 1) / BN);
-
-  load_tile<HD, BM, NT>(Qs, base, q0, a.s, rstride, qcol);
-  load_tile<HD, BN, NT>(Ks, base, 0, a.s, rstride, kcol);
-  load_tile<HD, BN, NT>(Vs, base, 0, a.s, rstride, vcol);
-  cp_commit();
+  const int64_t qcol = a.qoff + (int64_t)hl * HD, kcol = a.koff + (int64_t)hl * HD,
+                vcol = a.voff + (int64_t)hl * HD;
+  const Rng rng(a.drop);
+  // MAT (materialised interior, causal included) visits every key tile; otherwise causal
+  // stops at the diagonal.
+  const int kv_end = (CAUSAL && !MAT) ? min(S, q0 + BM) : S;
+  const int nkv = (kv_end + BN - 1) / BN;
+  const int row0 = q0 + warp * 16 + g;  // this thread's rows: row0, row0 + 8
+  const uint64_t rowidx = ((uint64_t)(a.head_offset + hl) * a.b + bj) * a.s;
+  const uint64_t rb[2] = {rng.row_base(rowidx + row0, a.s), rng.row_base(rowidx + row0 + 8, a.s)};
+  const float sl2 = a.scale * kLog2e;
 
   uint32_t qf[HD / 16][4];
-  float o[HD / 8][4];
-#pragma unroll
-  for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
-  const float sl2 = a.scale * kLog2e;
-  const int64_t row0 = q0 + warp * 16 + g;  // this thread's rows: row0, row0 + 8
-  const int64_t ghead = a.head_offset + hl;
-  const uint64_t mbase = (uint64_t)((ghead * a.b + bj) * a.s);
-  const uint64_t mrow0 = (mbase + (uint64_t)row0) * (uint64_t)a.s;
-  const uint64_t mrow1 = (mbase + (uint64_t)row0 + 8) * (uint64_t)a.s;
 
-  for (int jb = 0; jb < nkv; ++jb) {
-    const int buf = jb & 1;
-    if (jb + 1 < nkv) {
-      load_tile<HD, BN, NT>(Ks + (buf ^ 1) * BN * LDS, base, (int64_t)(jb + 1) * BN, a.s, rstride, kcol);
-      load_tile<HD, BN, NT>(Vs + (buf ^ 1) * BN * LDS, base, (int64_t)(jb + 1) * BN, a.s, rstride, vcol);
-      cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
-    if (jb == 0) {
-#pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk)
-        ldsm_x4(qf[kk], Qs + (warp * 16 + (lane & 15)) * LDS + kk * 16 + (lane >> 4) * 8);
-    }
-    const bf16* Kb = Ks + buf * BN * LDS;
-    const bf16* Vb = Vs + buf * BN * LDS;
-    float sacc[BN / 8][4];
+  auto scores = [&](const bf16* Kb, float (&sacc)[BN / 8][4], int k0) {
 #pragma unroll
     for (int i = 0; i < BN / 8; ++i) sacc[i][0] = sacc[i][1] = sacc[i][2] = sacc[i][3] = 0.f;
 #pragma unroll
@@ -143,59 +166,153 @@ __global__ void __launch_bounds__(128) fa_fwd(AttnArgs a) {
         mma16816(sacc[nb + 1], qf[kk], b[2], b[3]);
       }
     }
-    // scale, bounds/causal mask, online softmax (log2 domain)
-    const int64_t k0 = (int64_t)jb * BN;
-    float mx[2] = {m[0], m[1]};
+    const bool edge = (k0 + BN > S) || (CAUSAL && k0 + BN - 1 > q0 + warp * 16);
 #pragma unroll
-    for (int nb = 0; nb < BN / 8; ++nb) {
+    for (int nb = 0; nb < BN / 8; ++nb)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int64_t key = k0 + nb * 8 + 2 * tq + (e & 1);
-        const int64_t qr = row0 + (e >> 1) * 8;
         float v = sacc[nb][e] * sl2;
-        if (key >= a.s || (a.causal && key > qr)) v = -INFINITY;
+        if (edge) {
+          const int key = k0 + nb * 8 + 2 * tq + (e & 1);
+          const int qr = row0 + (e >> 1) * 8;
+          if (key >= S || (CAUSAL && key > qr)) v = -INFINITY;
+        }
         sacc[nb][e] = v;
-        mx[e >> 1] = fmaxf(mx[e >> 1], v);
+      }
+  };
+
+  load_tile<HD, BM, NT>(Qs, base, q0, a.s, rstride, qcol);
+  if (MAT) {
+    // ---- pass 1: exact row max and sum (K tiles only)
+    load_tile<HD, BN, NT>(Ks, base, 0, a.s, rstride, kcol);
+    cp_commit();
+    for (int jb = 0; jb < nkv; ++jb) {
+      const int buf = jb & 1;
+      if (jb + 1 < nkv) {
+        load_tile<HD, BN, NT>(Ks + (buf ^ 1) * BN * LDS, base, (int64_t)(jb + 1) * BN, a.s, rstride, kcol);
+        cp_commit();
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
+      }
+      __syncthreads();
+      if (jb == 0) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          ldsm_x4(qf[kk], Qs + (warp * 16 + (lane & 15)) * LDS + kk * 16 + (lane >> 4) * 8);
+      }
+      float sacc[BN / 8][4];
+      scores(Ks + buf * BN * LDS, sacc, jb * BN);
+      float mx[2] = {m[0], m[1]};
+#pragma unroll
+      for (int nb = 0; nb < BN / 8; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) mx[e >> 1] = fmaxf(mx[e >> 1], sacc[nb][e]);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+        l[r] *= (m[r] == -INFINITY) ? 0.f : ex2(m[r] - mx[r]);
+        m[r] = mx[r];
+      }
+#pragma unroll
+      for (int nb = 0; nb < BN / 8; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float mr = m[e >> 1] == -INFINITY ? 0.f : m[e >> 1];
+          l[e >> 1] += ex2(sacc[nb][e] - mr);
+        }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      l[r] += __shfl_xor_sync(0xffffffffu, l[r], 1);
+      l[r] += __shfl_xor_sync(0xffffffffu, l[r], 2);
+    }
+  }
+  load_tile<HD, BN, NT>(Ks, base, 0, a.s, rstride, kcol);
+  load_tile<HD, BN, NT>(Vs, base, 0, a.s, rstride, vcol);
+  cp_commit();
+  float o[HD / 8][4];
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  const float inv_l[2] = {MAT ? 1.f / l[0] : 1.f, MAT ? 1.f / l[1] : 1.f};
+
+  for (int jb = 0; jb < nkv; ++jb) {
+    const int buf = jb & 1;
+    if (jb + 1 < nkv) {
+      load_tile<HD, BN, NT>(Ks + (buf ^ 1) * BN * LDS, base, (int64_t)(jb + 1) * BN, a.s, rstride, kcol);
+      load_tile<HD, BN, NT>(Vs + (buf ^ 1) * BN * LDS, base, (int64_t)(jb + 1) * BN, a.s, rstride, vcol);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    if (!MAT && jb == 0) {
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+        ldsm_x4(qf[kk], Qs + (warp * 16 + (lane & 15)) * LDS + kk * 16 + (lane >> 4) * 8);
+    }
+    const int k0 = jb * BN;
+    float sacc[BN / 8][4];
+    scores(Ks + buf * BN * LDS, sacc, k0);
+    if (!MAT) {
+      float mx[2] = {m[0], m[1]};
+#pragma unroll
+      for (int nb = 0; nb < BN / 8; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) mx[e >> 1] = fmaxf(mx[e >> 1], sacc[nb][e]);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+        const float corr = (m[r] == -INFINITY) ? 0.f : ex2(m[r] - mx[r]);
+        m[r] = mx[r];
+        l[r] *= corr;
+#pragma unroll
+        for (int i = 0; i < HD / 8; ++i) {
+          o[i][2 * r] *= corr;
+          o[i][2 * r + 1] *= corr;
+        }
       }
     }
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-    }
-    float corr[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const float mnew = mx[r];
-      corr[r] = (m[r] == -INFINITY) ? 0.f : exp2f(m[r] - mnew);
-      m[r] = mnew;
-      l[r] *= corr[r];
-    }
-#pragma unroll
-    for (int i = 0; i < HD / 8; ++i) {
-      o[i][0] *= corr[0]; o[i][1] *= corr[0];
-      o[i][2] *= corr[1]; o[i][3] *= corr[1];
-    }
+    const float mr[2] = {m[0] == -INFINITY ? 0.f : m[0], m[1] == -INFINITY ? 0.f : m[1]};
     uint32_t pa[BN / 16][4];
 #pragma unroll
     for (int nb = 0; nb < BN / 8; ++nb) {
-      float p[4];
+      float p[4], pd[4];
+      bool kp[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int r = e >> 1;
-        const float mr = m[r] == -INFINITY ? 0.f : m[r];
-        const float pv = exp2f(sacc[nb][e] - mr);
-        l[r] += pv;
-        const int64_t key = k0 + nb * 8 + 2 * tq + (e & 1);
-        bool keep = false;
-        if (pv != 0.f) keep = drop_keep(a.drop, (r ? mrow1 : mrow0) + (uint64_t)key);
-        p[e] = keep ? pv * a.drop.inv_keep : 0.f;
+        float pv = ex2(sacc[nb][e] - mr[r]);
+        if (!MAT) l[r] += pv;
+        else pv *= inv_l[r];
+        const uint32_t key = (uint32_t)(k0 + nb * 8 + 2 * tq + (e & 1));
+        kp[e] = rng.keep(rb[r], key) && (MAT ? key < (uint32_t)S : pv != 0.f);
+        p[e] = pv;
+        pd[e] = kp[e] ? pv * a.drop.inv_keep : 0.f;
+      }
+      if (MAT) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int qr = row0 + r * 8;
+          const int key = k0 + nb * 8 + 2 * tq;
+          if (qr < S && key < S) {  // S even in MAT mode (checked by the dispatcher)
+            const int64_t mi = (((int64_t)hl * a.b + bj) * a.s + qr) * a.s + key;
+            *reinterpret_cast<uint32_t*>(static_cast<bf16*>(a.sm) + mi) = pack_bf16(p[2 * r], p[2 * r + 1]);
+            *reinterpret_cast<uint32_t*>(static_cast<bf16*>(a.sd) + mi) = pack_bf16(pd[2 * r], pd[2 * r + 1]);
+            *reinterpret_cast<uint16_t*>(a.mask + mi) =
+                (uint16_t)((kp[2 * r] ? 1 : 0) | ((kp[2 * r + 1] ? 1 : 0) << 8));
+          }
+        }
       }
       const int kk2 = nb >> 1, hi = nb & 1;
-      pa[kk2][hi * 2 + 0] = pack_bf16(p[0], p[1]);
-      pa[kk2][hi * 2 + 1] = pack_bf16(p[2], p[3]);
+      pa[kk2][hi * 2 + 0] = pack_bf16(pd[0], pd[1]);
+      pa[kk2][hi * 2 + 1] = pack_bf16(pd[2], pd[3]);
     }
-    // O += P̃ · V
+    const bf16* Vb = Vs + buf * BN * LDS;
 #pragma unroll
     for (int kk2 = 0; kk2 < BN / 16; ++kk2) {
 #pragma unroll
@@ -208,25 +325,26 @@ __global__ void __launch_bounds__(128) fa_fwd(AttnArgs a) {
     }
     __syncthreads();
   }
-  // finalize
+  if (!MAT) {
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    l[r] += __shfl_xor_sync(0xffffffffu, l[r], 1);
-    l[r] += __shfl_xor_sync(0xffffffffu, l[r], 2);
+    for (int r = 0; r < 2; ++r) {
+      l[r] += __shfl_xor_sync(0xffffffffu, l[r], 1);
+      l[r] += __shfl_xor_sync(0xffffffffu, l[r], 2);
+    }
   }
   bf16* out = static_cast<bf16*>(a.o);
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const int64_t qr = row0 + r * 8;
-    if (qr >= a.s) continue;
-    const float inv = 1.f / l[r];
-    bf16* orow = out + (qr * a.b + bj) * a.ldo + hl * HD;
+    const int qr = row0 + r * 8;
+    if (qr >= S) continue;
+    const float inv = MAT ? 1.f : 1.f / l[r];
+    bf16* orow = out + ((int64_t)qr * a.b + bj) * a.ldo + (int64_t)hl * HD;
 #pragma unroll
-    for (int db = 0; db < HD / 8; ++db) {
-      const uint32_t v = pack_bf16(o[db][2 * r] * inv, o[db][2 * r + 1] * inv);
-      *reinterpret_cast<uint32_t*>(orow + db * 8 + 2 * tq) = v;
-    }
-    if (tq == 0 && a.lse) a.lse[(hl * a.b + bj) * a.s + qr] = (m[r] + log2f(l[r])) * kLn2;
+    for (int db = 0; db < HD / 8; ++db)
+      *reinterpret_cast<uint32_t*>(orow + db * 8 + 2 * tq) =
+          pack_bf16(o[db][2 * r] * inv, o[db][2 * r + 1] * inv);
+    if (tq == 0 && a.lse)
+      a.lse[((int64_t)hl * a.b + bj) * a.s + qr] = (m[r] + log2f(l[r])) * kLn2;
   }
 }
 
@@ -253,9 +371,9 @@ __global__ void fa_delta(AttnArgs a, const bf16* __restrict__ dout, float* __res
 }
 
 // =====================================================================================
-// backward: dK, dV (key-parallel)
+// backward: dK, dV (key-parallel). Recompute regimes also emit the keep bits for fa_bwd_dq.
 // =====================================================================================
-template <int HD>
+template <int HD, bool CAUSAL, bool STORED>
 __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __restrict__ dout,
                                                    bf16* __restrict__ dqkv,
                                                    const float* __restrict__ delta) {
@@ -267,30 +385,47 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __res
   bf16* Ds = Qs + 2 * BQ * LDS;    // [2][BQ][LDS] dO
   float* lse_s = reinterpret_cast<float*>(Ds + 2 * BQ * LDS);  // [2][BQ]
   float* dl_s = lse_s + 2 * BQ;                                // [2][BQ]
+  uint16_t* kb16 = reinterpret_cast<uint16_t*>(dl_s + 2 * BQ); // [2][BQ][4] keep bits
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
-  const int64_t k0 = (int64_t)blockIdx.x * BK_;
-  const int64_t hl = blockIdx.y / a.b, bj = blockIdx.y % a.b;
-  const bf16* qkv = static_cast<const bf16*>(a.qkv);
-  const bf16* base = qkv + bj * a.ld;
-  const bf16* dbase = dout + bj * a.ldo;
+  const int k0 = blockIdx.x * BK_;
+  const int hl = blockIdx.y / (int)a.b, bj = blockIdx.y % (int)a.b;
+  const int S = (int)a.s;
+  const bf16* base = static_cast<const bf16*>(a.qkv) + (int64_t)bj * a.ld;
+  const bf16* dbase = dout + (int64_t)bj * a.ldo;
   const int64_t rstride = a.b * a.ld, dstride = a.b * a.ldo;
-  const int64_t qcol = a.qoff + hl * HD, kcol = a.koff + hl * HD, vcol = a.voff + hl * HD;
-  const int64_t rowbase = (hl * a.b + bj) * a.s;  // lse/delta row index base
+  const int64_t qcol = a.qoff + (int64_t)hl * HD, kcol = a.koff + (int64_t)hl * HD,
+                vcol = a.voff + (int64_t)hl * HD;
+  const int64_t rowbase = ((int64_t)hl * a.b + bj) * a.s;  // lse/delta/bits row index base
   const float sl2 = a.scale * kLog2e;
-  const uint64_t mbase = (uint64_t)(((a.head_offset + hl) * a.b + bj) * a.s);
+  const Rng rng(a.drop);
+  const uint64_t growbase = ((uint64_t)(a.head_offset + hl) * a.b + bj) * a.s;
+  const int W = (S + 31) / 32;
 
-  const int64_t q_start = a.causal ? (k0 / BQ) * BQ : 0;
-  const int nq = (int)((a.s - q_start + BQ - 1) / BQ);
+  const int q_start = CAUSAL ? (k0 / BQ) * BQ : 0;
+  const int nq = (S - q_start + BQ - 1) / BQ;
 
   auto load_q = [&](int it, int buf) {
-    const int64_t qb = q_start + (int64_t)it * BQ;
+    const int qb = q_start + it * BQ;
     load_tile<HD, BQ, NT>(Qs + buf * BQ * LDS, base, qb, a.s, rstride, qcol);
-    load_tile<HD, BQ, NT>(Ds + buf * BQ * LDS, dbase, qb, a.s, dstride, hl * HD);
+    load_tile<HD, BQ, NT>(Ds + buf * BQ * LDS, dbase, qb, a.s, dstride, (int64_t)hl * HD);
     if (threadIdx.x < BQ) {
-      const int64_t q = qb + threadIdx.x;
-      lse_s[buf * BQ + threadIdx.x] = q < a.s ? a.lse[rowbase + q] : INFINITY;
-      dl_s[buf * BQ + threadIdx.x] = q < a.s ? delta[rowbase + q] : 0.f;
+      const int q = qb + threadIdx.x;
+      lse_s[buf * BQ + threadIdx.x] = (q < S && !STORED) ? a.lse[rowbase + q] * kLog2e : INFINITY;
+      dl_s[buf * BQ + threadIdx.x] = q < S ? delta[rowbase + q] : 0.f;
+    }
+  };
+  // flush the keep bits of q-tile `it` (buffer buf) to global
+  auto flush_bits = [&](int it, int buf) {
+    if (STORED || a.keepbits == nullptr) return;
+    if (threadIdx.x < BQ * 2) {
+      const int qi = threadIdx.x >> 1, wi = threadIdx.x & 1;
+      const int q = q_start + it * BQ + qi;
+      const int word = k0 / 32 + wi;
+      if (q < S && word < W) {
+        const uint16_t* src = kb16 + (buf * BQ + qi) * 4 + wi * 2;
+        a.keepbits[(rowbase + q) * W + word] = (uint32_t)src[0] | ((uint32_t)src[1] << 16);
+      }
     }
   };
   load_tile<HD, BK_, NT>(Ks, base, k0, a.s, rstride, kcol);
@@ -303,11 +438,12 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __res
   for (int i = 0; i < HD / 8; ++i)
 #pragma unroll
     for (int e = 0; e < 4; ++e) dk[i][e] = dv[i][e] = 0.f;
-  const int64_t key0 = k0 + warp * 16 + g;  // rows of this thread: key0, key0 + 8
+  const int key0 = k0 + warp * 16 + g;  // rows of this thread: key0, key0 + 8
 
   for (int it = 0; it < nq; ++it) {
     const int buf = it & 1;
-    __syncthreads();  // previous iteration done with buf^1 (and lse/delta slots)
+    __syncthreads();  // all warps done with iteration it-1 (its bits are complete)
+    if (it > 0) flush_bits(it - 1, buf ^ 1);
     if (it + 1 < nq) {
       load_q(it + 1, buf ^ 1);
       cp_commit();
@@ -320,8 +456,7 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __res
     const bf16* Db = Ds + buf * BQ * LDS;
     const float* lq = lse_s + buf * BQ;
     const float* dq_ = dl_s + buf * BQ;
-    const int64_t qb = q_start + (int64_t)it * BQ;
-    // Sᵀ = K Qᵀ and dPᵀ = V dOᵀ : [16 keys × 32 queries] per warp
+    const int qb = q_start + it * BQ;
     float st[BQ / 8][4], dpt[BQ / 8][4];
 #pragma unroll
     for (int i = 0; i < BQ / 8; ++i)
@@ -343,25 +478,49 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __res
         mma16816(dpt[nb + 1], va, c[2], c[3]);
       }
     }
-    // Pᵀ, keepᵀ, dSᵀ
+    const bool edge = (qb + BQ > S) || (k0 + BK_ > S) || (CAUSAL && qb < k0 + warp * 16 + 16);
     uint32_t pa[BQ / 16][4], da[BQ / 16][4];
 #pragma unroll
     for (int nb = 0; nb < BQ / 8; ++nb) {
       float pd[4], ds[4];
+      uint32_t ball[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int qi = nb * 8 + 2 * tq + (e & 1);
-        const int64_t q = qb + qi;
-        const int64_t key = key0 + (e >> 1) * 8;
-        float p = 0.f;
-        bool keep = false;
-        if (q < a.s && key < a.s && !(a.causal && key > q)) {
-          p = exp2f(st[nb][e] * sl2 - lq[qi] * kLog2e);
-          if (p != 0.f) keep = drop_keep(a.drop, (mbase + (uint64_t)q) * (uint64_t)a.s + (uint64_t)key);
+      for (int par = 0; par < 2; ++par) {
+        const int qi = nb * 8 + 2 * tq + par;
+        const int q = qb + qi;
+        const float lqv = lq[qi], dqv = dq_[qi];
+        const uint64_t rbq = STORED ? 0 : rng.row_base(growbase + q, a.s);
+#pragma unroll
+        for (int kr = 0; kr < 2; ++kr) {
+          const int e = kr * 2 + par;
+          const int key = key0 + kr * 8;
+          const bool valid = !edge || (q < S && key < S && !(CAUSAL && key > q));
+          float p = 0.f, pdv = 0.f;
+          bool keep = false;
+          if (STORED) {
+            if (valid) {
+              const int64_t mi = (rowbase + q) * a.s + key;
+              p = __bfloat162float(static_cast<const bf16*>(a.sm)[mi]);
+              keep = a.mask[mi] != 0;
+              pdv = __bfloat162float(static_cast<const bf16*>(a.sd)[mi]);
+            }
+          } else {
+            p = valid ? ex2(st[nb][e] * sl2 - lqv) : 0.f;
+            keep = rng.keep(rbq, (uint32_t)key) && p != 0.f;
+            pdv = keep ? p * a.drop.inv_keep : 0.f;
+            ball[e] = __ballot_sync(0xffffffffu, keep);
+          }
+          pd[e] = pdv;
+          const float dp = keep ? dpt[nb][e] * a.drop.inv_keep : 0.f;
+          ds[e] = p * (dp - dqv);
         }
-        pd[e] = keep ? p * a.drop.inv_keep : 0.f;
-        const float dp = keep ? dpt[nb][e] * a.drop.inv_keep : 0.f;
-        ds[e] = p * (dp - dq_[qi]);
+      }
+      if (!STORED && g == 0) {
+#pragma unroll
+        for (int par = 0; par < 2; ++par) {
+          const uint32_t lo = compress4(ball[par] >> tq), hi = compress4(ball[2 + par] >> tq);
+          kb16[(buf * BQ + nb * 8 + 2 * tq + par) * 4 + warp] = (uint16_t)(lo | (hi << 8));
+        }
       }
       const int kk2 = nb >> 1, hi = nb & 1;
       pa[kk2][hi * 2 + 0] = pack_bf16(pd[0], pd[1]);
@@ -369,7 +528,6 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __res
       da[kk2][hi * 2 + 0] = pack_bf16(ds[0], ds[1]);
       da[kk2][hi * 2 + 1] = pack_bf16(ds[2], ds[3]);
     }
-    // dV += P̃ᵀ dO ; dK += dSᵀ Q
 #pragma unroll
     for (int kk2 = 0; kk2 < BQ / 16; ++kk2) {
 #pragma unroll
@@ -384,11 +542,14 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __res
       }
     }
   }
+  __syncthreads();
+  flush_bits(nq - 1, (nq - 1) & 1);
+  // the causal tiles skipped above (q < k0) hold no keep bits the dQ kernel reads
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const int64_t key = key0 + r * 8;
-    if (key >= a.s) continue;
-    bf16* row = dqkv + (key * a.b + bj) * a.ld;
+    const int key = key0 + r * 8;
+    if (key >= S) continue;
+    bf16* row = dqkv + ((int64_t)key * a.b + bj) * a.ld;
 #pragma unroll
     for (int db = 0; db < HD / 8; ++db) {
       *reinterpret_cast<uint32_t*>(row + kcol + db * 8 + 2 * tq) =
@@ -400,9 +561,9 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __res
 }
 
 // =====================================================================================
-// backward: dQ (query-parallel)
+// backward: dQ (query-parallel); keep bits from fa_bwd_dkdv (or the stored mask)
 // =====================================================================================
-template <int HD>
+template <int HD, bool CAUSAL, bool STORED>
 __global__ void __launch_bounds__(128) fa_bwd_dq(AttnArgs a, const bf16* __restrict__ dout,
                                                  bf16* __restrict__ dqkv,
                                                  const float* __restrict__ delta) {
@@ -414,35 +575,35 @@ __global__ void __launch_bounds__(128) fa_bwd_dq(AttnArgs a, const bf16* __restr
   bf16* Vs = Ks + 2 * BN * LDS;   // [2][BN][LDS]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
-  const int64_t q0 = (int64_t)blockIdx.x * BM;
-  const int64_t hl = blockIdx.y / a.b, bj = blockIdx.y % a.b;
-  const bf16* qkv = static_cast<const bf16*>(a.qkv);
-  const bf16* base = qkv + bj * a.ld;
-  const bf16* dbase = dout + bj * a.ldo;
+  const int q0 = blockIdx.x * BM;
+  const int hl = blockIdx.y / (int)a.b, bj = blockIdx.y % (int)a.b;
+  const int S = (int)a.s;
+  const bf16* base = static_cast<const bf16*>(a.qkv) + (int64_t)bj * a.ld;
+  const bf16* dbase = dout + (int64_t)bj * a.ldo;
   const int64_t rstride = a.b * a.ld, dstride = a.b * a.ldo;
-  const int64_t qcol = a.qoff + hl * HD, kcol = a.koff + hl * HD, vcol = a.voff + hl * HD;
-  const int64_t rowbase = (hl * a.b + bj) * a.s;
+  const int64_t qcol = a.qoff + (int64_t)hl * HD, kcol = a.koff + (int64_t)hl * HD,
+                vcol = a.voff + (int64_t)hl * HD;
+  const int64_t rowbase = ((int64_t)hl * a.b + bj) * a.s;
   const float sl2 = a.scale * kLog2e;
-  const uint64_t mbase = (uint64_t)(((a.head_offset + hl) * a.b + bj) * a.s);
-  const int64_t kv_end = a.causal ? (a.s < q0 + BM ? a.s : q0 + BM) : a.s;
-  const int nkv = (int)((kv_end + BN - 1) / BN);
+  const int kv_end = CAUSAL ? min(S, q0 + BM) : S;
+  const int nkv = (kv_end + BN - 1) / BN;
+  const int W = (S + 31) / 32;
+  const bool bits_on = a.drop.thresh != 0;
 
   load_tile<HD, BM, NT>(Qs, base, q0, a.s, rstride, qcol);
-  load_tile<HD, BM, NT>(Ds, dbase, q0, a.s, dstride, hl * HD);
+  load_tile<HD, BM, NT>(Ds, dbase, q0, a.s, dstride, (int64_t)hl * HD);
   load_tile<HD, BN, NT>(Ks, base, 0, a.s, rstride, kcol);
   load_tile<HD, BN, NT>(Vs, base, 0, a.s, rstride, vcol);
   cp_commit();
 
-  const int64_t row0 = q0 + warp * 16 + g;
+  const int row0 = q0 + warp * 16 + g;
   float lse[2], dl[2];
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const int64_t q = row0 + r * 8;
-    lse[r] = q < a.s ? a.lse[rowbase + q] * kLog2e : INFINITY;
-    dl[r] = q < a.s ? delta[rowbase + q] : 0.f;
+    const int q = row0 + r * 8;
+    lse[r] = (q < S && !STORED) ? a.lse[rowbase + q] * kLog2e : INFINITY;
+    dl[r] = q < S ? delta[rowbase + q] : 0.f;
   }
-  const uint64_t mrow[2] = {(mbase + (uint64_t)row0) * (uint64_t)a.s,
-                            (mbase + (uint64_t)row0 + 8) * (uint64_t)a.s};
   uint32_t qf[HD / 16][4], df[HD / 16][4];
   float dq[HD / 8][4];
 #pragma unroll
@@ -466,6 +627,15 @@ __global__ void __launch_bounds__(128) fa_bwd_dq(AttnArgs a, const bf16* __restr
         ldsm_x4(df[kk], Ds + (warp * 16 + (lane & 15)) * LDS + kk * 16 + (lane >> 4) * 8);
       }
     }
+    const int kb0 = jb * BN;
+    uint32_t word[2] = {0xffffffffu, 0xffffffffu};
+    if (!STORED && bits_on) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int q = row0 + r * 8;
+        word[r] = q < S ? a.keepbits[(rowbase + q) * W + kb0 / 32] : 0u;
+      }
+    }
     const bf16* Kb = Ks + buf * BN * LDS;
     const bf16* Vb = Vs + buf * BN * LDS;
     float sc[BN / 8][4], dp[BN / 8][4];
@@ -486,7 +656,7 @@ __global__ void __launch_bounds__(128) fa_bwd_dq(AttnArgs a, const bf16* __restr
         mma16816(dp[nb + 1], df[kk], c[2], c[3]);
       }
     }
-    const int64_t kb0 = (int64_t)jb * BN;
+    const bool edge = (kb0 + BN > S) || (q0 + BM > S) || (CAUSAL && kb0 + BN - 1 > q0 + warp * 16);
     uint32_t da[BN / 16][4];
 #pragma unroll
     for (int nb = 0; nb < BN / 8; ++nb) {
@@ -494,13 +664,21 @@ __global__ void __launch_bounds__(128) fa_bwd_dq(AttnArgs a, const bf16* __restr
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int r = e >> 1;
-        const int64_t key = kb0 + nb * 8 + 2 * tq + (e & 1);
-        const int64_t q = row0 + r * 8;
+        const int kl = nb * 8 + 2 * tq + (e & 1);
+        const int key = kb0 + kl;
+        const int q = row0 + r * 8;
+        const bool valid = !edge || (q < S && key < S && !(CAUSAL && key > q));
         float p = 0.f;
         bool keep = false;
-        if (q < a.s && key < a.s && !(a.causal && key > q)) {
-          p = exp2f(sc[nb][e] * sl2 - lse[r]);
-          if (p != 0.f) keep = drop_keep(a.drop, mrow[r] + (uint64_t)key);
+        if (valid) {
+          if (STORED) {
+            const int64_t mi = (rowbase + q) * a.s + key;
+            p = __bfloat162float(static_cast<const bf16*>(a.sm)[mi]);
+            keep = a.mask[mi] != 0;
+          } else {
+            p = ex2(sc[nb][e] * sl2 - lse[r]);
+            keep = (word[r] >> kl) & 1u;
+          }
         }
         const float d = keep ? dp[nb][e] * a.drop.inv_keep : 0.f;
         ds[e] = p * (d - dl[r]);
@@ -523,9 +701,9 @@ __global__ void __launch_bounds__(128) fa_bwd_dq(AttnArgs a, const bf16* __restr
   }
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
-    const int64_t q = row0 + r * 8;
-    if (q >= a.s) continue;
-    bf16* row = dqkv + (q * a.b + bj) * a.ld + qcol;
+    const int q = row0 + r * 8;
+    if (q >= S) continue;
+    bf16* row = dqkv + ((int64_t)q * a.b + bj) * a.ld + qcol;
 #pragma unroll
     for (int db = 0; db < HD / 8; ++db)
       *reinterpret_cast<uint32_t*>(row + db * 8 + 2 * tq) =
@@ -533,38 +711,38 @@ __global__ void __launch_bounds__(128) fa_bwd_dq(AttnArgs a, const bf16* __restr
   }
 }
 
-template <int HD>
-void launch_fwd(const AttnArgs& a, cudaStream_t st) {
+template <int HD, bool CAUSAL, bool MAT>
+void launch_fwd_t(const AttnArgs& a, cudaStream_t st) {
   constexpr int LDS = HD + 8;
   const int smem = (64 * LDS + 4 * 64 * LDS) * 2;
   static bool once = [&] {
-    SPL_CUDA(cudaFuncSetAttribute(fa_fwd<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SPL_CUDA(cudaFuncSetAttribute(fa_fwd<HD, CAUSAL, MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     return true;
   }();
   (void)once;
   dim3 grid((unsigned)((a.s + 63) / 64), (unsigned)(a.lh * a.b));
-  fa_fwd<HD><<<grid, 128, smem, st>>>(a);
+  fa_fwd<HD, CAUSAL, MAT><<<grid, 128, smem, st>>>(a);
   SPL_CHECK_LAUNCH();
 }
 
-template <int HD>
-void launch_bwd(const AttnArgs& a, const bf16* dout, bf16* dqkv, float* delta, cudaStream_t st) {
+template <int HD, bool CAUSAL, bool STORED>
+void launch_bwd_t(const AttnArgs& a, const bf16* dout, bf16* dqkv, float* delta, cudaStream_t st) {
   constexpr int LDS = HD + 8;
   const int64_t rows = a.lh * a.b * a.s;
   fa_delta<HD><<<(unsigned)((rows + 3) / 4), 128, 0, st>>>(a, dout, delta);
   SPL_CHECK_LAUNCH();
-  const int smem_kv = (2 * 64 * LDS + 4 * 32 * LDS) * 2 + 4 * 32 * 4;
+  const int smem_kv = (2 * 64 * LDS + 4 * 32 * LDS) * 2 + 4 * 32 * 4 + 2 * 32 * 4 * 2;
   const int smem_q = (2 * 64 * LDS + 4 * 32 * LDS) * 2;
   static bool once = [&] {
-    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_dkdv<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv));
-    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_dq<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q));
+    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_dkdv<HD, CAUSAL, STORED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv));
+    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_dq<HD, CAUSAL, STORED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q));
     return true;
   }();
   (void)once;
   dim3 grid((unsigned)((a.s + 63) / 64), (unsigned)(a.lh * a.b));
-  fa_bwd_dkdv<HD><<<grid, 128, smem_kv, st>>>(a, dout, dqkv, delta);
+  fa_bwd_dkdv<HD, CAUSAL, STORED><<<grid, 128, smem_kv, st>>>(a, dout, dqkv, delta);
   SPL_CHECK_LAUNCH();
-  fa_bwd_dq<HD><<<grid, 128, smem_q, st>>>(a, dout, dqkv, delta);
+  fa_bwd_dq<HD, CAUSAL, STORED><<<grid, 128, smem_q, st>>>(a, dout, dqkv, delta);
   SPL_CHECK_LAUNCH();
 }
 
@@ -582,8 +760,10 @@ void attn_bwd_tc(const AttnArgs& a, const void* dout, void* dqkv, float* delta, 
 template <>
 bool attn_tc_supported<bf16>(const AttnArgs& a) {
   const bool hd_ok = a.hd == 32 || a.hd == 64 || a.hd == 96 || a.hd == 128 || a.hd == 160;
+  const bool mat = a.sm != nullptr;
   return hd_ok && a.ld % 8 == 0 && a.ldo % 8 == 0 && a.qoff % 8 == 0 && a.koff % 8 == 0 &&
-         a.voff % 8 == 0 && aligned16(a.qkv) && aligned16(a.o) && a.lse != nullptr;
+         a.voff % 8 == 0 && aligned16(a.qkv) && aligned16(a.o) && a.s < (1 << 30) &&
+         (mat ? (a.s % 2 == 0 && a.mask != nullptr && a.sd != nullptr) : a.lse != nullptr);
 }
 
 #define SPL_HD_SWITCH(HDV, ...)                                   \
@@ -598,14 +778,30 @@ bool attn_tc_supported<bf16>(const AttnArgs& a) {
 
 template <>
 void attn_fwd_tc<bf16>(const AttnArgs& a, cudaStream_t st) {
-  SPL_HD_SWITCH(a.hd, launch_fwd<HD>(a, st));
+  const bool mat = a.sm != nullptr;
+  SPL_HD_SWITCH(a.hd, {
+    if (a.causal) {
+      if (mat) launch_fwd_t<HD, true, true>(a, st); else launch_fwd_t<HD, true, false>(a, st);
+    } else {
+      if (mat) launch_fwd_t<HD, false, true>(a, st); else launch_fwd_t<HD, false, false>(a, st);
+    }
+  });
 }
 
 template <>
 void attn_bwd_tc<bf16>(const AttnArgs& a, const void* dout, void* dqkv, float* delta,
                        cudaStream_t st) {
-  SPL_HD_SWITCH(a.hd, launch_bwd<HD>(a, static_cast<const bf16*>(dout), static_cast<bf16*>(dqkv),
-                                     delta, st));
+  const bool stored = a.sm != nullptr;
+  if (!stored) require(a.keepbits != nullptr || a.drop.thresh == 0, "attention backward: keep-bit workspace missing");
+  const bf16* d = static_cast<const bf16*>(dout);
+  bf16* g = static_cast<bf16*>(dqkv);
+  SPL_HD_SWITCH(a.hd, {
+    if (a.causal) {
+      if (stored) launch_bwd_t<HD, true, true>(a, d, g, delta, st); else launch_bwd_t<HD, true, false>(a, d, g, delta, st);
+    } else {
+      if (stored) launch_bwd_t<HD, false, true>(a, d, g, delta, st); else launch_bwd_t<HD, false, false>(a, d, g, delta, st);
+    }
+  });
 }
 
 }  // namespace spl::k

@@ -124,7 +124,11 @@ struct AttnArgs {
   void* sm = nullptr;
   uint8_t* mask = nullptr;
   void* sd = nullptr;
+  // backward workspace for the recompute regimes: keep bits [lh*b*s][ceil(s/32)] written by
+  // the dK/dV kernel (one RNG pass) and read by the dQ kernel.
+  uint32_t* keepbits = nullptr;
 };
+inline int64_t keepbits_words(int64_t lh, int64_t b, int64_t s) { return lh * b * s * ((s + 31) / 32); }
 // Forward. If a.sm != nullptr the interior is materialised (softmax_out, mask, dropout_out).
 template <typename T>
 void attn_fwd(const AttnArgs& a, cudaStream_t st);

@@ -460,6 +460,7 @@ class Layer final : public LayerBase {
     T *yfull = nullptr, *part = nullptr, *rs_out = nullptr, *dfull = nullptr, *dgin = nullptr,
       *dqkv = nullptr, *dproj = nullptr, *d_s = nullptr, *dr1 = nullptr, *y_re = nullptr;
     float *delta = nullptr, *partials = nullptr;
+    uint32_t* keepbits = nullptr;
   };
 
   void validate() {
@@ -508,6 +509,7 @@ class Layer final : public LayerBase {
     const int64_t npart = std::max<int64_t>(2 * (int64_t)nch_l * h_, nch_f * std::max<int64_t>(3 * lw_, fw_));
     T *yfull = nullptr, *dfull = nullptr, *dgin = nullptr, *dqkv = nullptr, *dproj = nullptr;
     float *delta = nullptr, *partials = nullptr;
+    uint32_t* keepbits = nullptr;
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
       R.wqkv = alloc<T>(h_ * 3 * lw_, kParam, r);
@@ -565,7 +567,10 @@ class Layer final : public LayerBase {
         dproj = alloc<T>(RF_ * lw_, kWork, r);
         delta = alloc<float>(lh_ * b_ * s_, kWork, r);
         partials = alloc<float>(npart, kWork, r);
+        if (kind_ != SPL_RECOMPUTE_NONE)  // backward-only keep bits (transient, 1 bit/elem)
+          keepbits = alloc<uint32_t>(k::keepbits_words(lh_, b_, s_), kWork, r);
       }
+      R.keepbits = keepbits;
       R.dgin = dgin;
       R.dqkv = dqkv;
       R.dproj = dproj;
@@ -636,6 +641,7 @@ class Layer final : public LayerBase {
     a.drop = k_soft_;
     a.lse = R.lse;
     a.sm = R.sm; a.mask = R.mask_i; a.sd = R.sd;
+    a.keepbits = R.keepbits;
     return a;
   }
 
