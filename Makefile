@@ -19,7 +19,7 @@ SRC := $(wildcard $(PKG)/csrc/*.cu)
 OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
 HDR := $(wildcard $(PKG)/csrc/*.hpp $(PKG)/csrc/*.cuh) include/spl.h
 
-all: $(PKG)/libspl.so oracle
+all: $(PKG)/libspl.so oracle build/test_facade
 
 build/%.o: $(PKG)/csrc/%.cu $(HDR)
 	@mkdir -p build
@@ -27,6 +27,10 @@ build/%.o: $(PKG)/csrc/%.cu $(HDR)
 
 $(PKG)/libspl.so: $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) $(NCCL_LINK)
+
+build/test_facade: tests/cpp/test_facade.cpp include/spl_seqpar.hpp include/spl.h $(PKG)/libspl.so
+	g++ -std=c++17 -O2 -Wall -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -lspl \
+	    -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
 
 oracle:
 	$(MAKE) -C oracle

@@ -93,6 +93,26 @@ class ClockSampler:
         return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def share_unique_id(make_id, rank):
+    """Rank 0 creates the NCCL unique id (libspl's spl_nccl_unique_id) and every rank gets
+    it through torch.distributed (plumbing only; the data path is libspl's own NCCL comm)."""
+    import torch.distributed as dist
+    obj = [make_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def max_over_ranks(value, device="cuda"):
+    """Max of a per-rank float over the process group (timing = slowest rank)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return value
+    t = torch.tensor([float(value)], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def cpu_baseline_sample(cfg_name, threads=0):
     """The oracle (fp64 restatement of the reference seqpar layer, test infrastructure) timed
     on the host cores on a bounded sample of the workload: the same layer width (h, a) with
@@ -184,9 +204,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
-        uid = [spl.SeqparLayer.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        nccl = (rank, uid[0])
+        nccl = (rank, share_unique_id(spl.SeqparLayer.nccl_unique_id, rank))
     a, h, s, b = CONFIGS[args.config]
     sp = not args.no_sp
     cfg = spl.BlockConfig(a, h, s, b, dropout_p=0.1, causal=False, seed=42)
@@ -227,10 +245,7 @@ def main():
     ms = start.elapsed_time(stop)
     launches = L.launch_count(reset=True)
     clk = clocks.stop()
-    if dist is not None:
-        tt = torch.tensor([ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = max_over_ranks(ms)
     ms_step = ms / args.steps
     tokens = s * b
     value = tokens / (ms_step / 1e3)
@@ -257,10 +272,7 @@ def main():
         for _ in range(args.steps):
             L.step_host(hx, hdy, hy, hdx)
         el = time.perf_counter() - t0
-        if dist is not None:
-            tt = torch.tensor([el], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            el = float(tt.item())
+        el = max_over_ranks(el)
         e2e = {"value": tokens / (el / args.steps), "unit": "tokens/s",
                "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": 2 * nbytes}
 

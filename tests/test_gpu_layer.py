@@ -288,3 +288,23 @@ def test_bf16_head_dims(spl, orc, shape, t, causal, recompute):
     assert rel_l2(y, ref.y) <= 1e-2
     assert rel_l2(dx, ref.dx) <= 1e-2
     grads_close(orc, cfg.hidden, g, ref.grads, 2e-2)
+
+
+def test_nccl_rank_handle_matches_local(spl, orc):
+    """One NCCL rank (t=1 group) runs the same schedule as the simulated-rank handle; this is
+    the handle bench.py uses per GPU under torchrun (collectives become ncclAllGather /
+    ncclReduceScatter / ncclAllReduce)."""
+    import torch
+    cfg, x, dy, p = make_case(orc, TINY)
+    c = to_spl_cfg(spl, cfg)
+    uid = spl.SeqparLayer.nccl_unique_id()
+    A = spl.SeqparLayer(c, 1, "selective", True, "bf16", nccl=(0, uid))
+    B = spl.SeqparLayer(c, 1, "selective", True, "bf16")
+    for L in (A, B):
+        L.load_params(p)
+    xs = [torch.from_numpy(x).to("cuda", torch.bfloat16)]
+    ds = [torch.from_numpy(dy).to("cuda", torch.bfloat16)]
+    ya, yb = A.forward(xs), B.forward(xs)
+    da, db = A.backward(ds), B.backward(ds)
+    assert torch.equal(ya[0], yb[0]) and torch.equal(da[0], db[0])
+    assert np.array_equal(A.grads(), B.grads())
