@@ -204,29 +204,53 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t m, int64_
 }
 
 // ------------------------------------------------------------------ the kernel
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Grouped tile order: GROUP consecutive M blocks sweep all N blocks, so the CTAs resident at
+// one time share B (weight) tiles and a few A row-panels in L2.
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& mb, int& nb) {
+  constexpr int GROUP = 8;
+  const int per_group = GROUP * tiles_n;
+  const int group = tile / per_group;
+  const int first_m = group * GROUP;
+  const int gsize = min(tiles_m - first_m, GROUP);
+  const int r = tile % per_group;
+  mb = first_m + r % gsize;
+  nb = r / gsize;
+}
+
+// Persistent: one CTA per SM loops over output tiles. Two TMEM accumulators (2 x BN fp32
+// columns) let the epilogue of tile i overlap the MMA main loop of tile i+1.
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
-                   const __grid_constant__ CUtensorMap map_b, const GemmArgs g) {
+                   const __grid_constant__ CUtensorMap map_b, const GemmArgs g, int tiles_m,
+                   int tiles_n) {
   using Cfg = TileCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* tiles = smem;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty_bar = full_bar + Cfg::STAGES;
-  uint64_t* tmem_full = empty_bar + Cfg::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty_bar + Cfg::STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;               // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
   const int nk = (int)((g.K + BK - 1) / BK);
+  const int ntiles = tiles_m * tiles_n;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
@@ -234,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"((uint32_t)Cfg::TMEM_COLS));
+                 "r"((uint32_t)(2 * Cfg::TMEM_COLS)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -245,26 +269,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % Cfg::STAGES;
-        const uint32_t ph = (uint32_t)(kb / Cfg::STAGES) & 1u;
-        mbar_wait(&empty_bar[s], ph ^ 1u);
-        uint8_t* sa = tiles + s * Cfg::STAGE_BYTES;
-        uint8_t* sb = sa + Cfg::A_BYTES;
-        mbar_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
-        const int k0 = kb * BK;
-        if (A_MN) {  // [K rows][M cols]: two 64-wide M atoms of 64 k-rows
-          tma_load_2d(sa, &map_a, &full_bar[s], (int)m0, k0);
-          tma_load_2d(sa + 8192, &map_a, &full_bar[s], (int)m0 + 64, k0);
-        } else {  // [M rows][K cols]: one 128-row box
-          tma_load_2d(sa, &map_a, &full_bar[s], k0, (int)m0);
-        }
-        if (B_MN) {  // [K rows][N cols]: BN/64 atoms
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int mb, nb;
+        tile_coords(tile, tiles_m, tiles_n, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % Cfg::STAGES;
+          const uint32_t ph = (uint32_t)(it / Cfg::STAGES) & 1u;
+          mbar_wait(&empty_bar[s], ph ^ 1u);
+          uint8_t* sa = tiles + s * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          mbar_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (A_MN) {  // [K rows][M cols]: two 64-wide M atoms of 64 k-rows
+            tma_load_2d(sa, &map_a, &full_bar[s], m0, k0);
+            tma_load_2d(sa + 8192, &map_a, &full_bar[s], m0 + 64, k0);
+          } else {  // [M rows][K cols]: one 128-row box
+            tma_load_2d(sa, &map_a, &full_bar[s], k0, m0);
+          }
+          if (B_MN) {  // [K rows][N cols]: BN/64 atoms
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j)
-            tma_load_2d(sb + j * 8192, &map_b, &full_bar[s], (int)n0 + 64 * j, k0);
-        } else {  // [N rows][K cols]: one BN-row box
-          tma_load_2d(sb, &map_b, &full_bar[s], k0, (int)n0);
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(sb + j * 8192, &map_b, &full_bar[s], n0 + 64 * j, k0);
+          } else {  // [N rows][K cols]: one BN-row box
+            tma_load_2d(sb, &map_b, &full_bar[s], k0, n0);
+          }
         }
       }
     }
@@ -272,38 +302,57 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ---------------- MMA issuer
       constexpr uint32_t idesc = make_idesc(BM, BN, A_MN, B_MN);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % Cfg::STAGES;
-        const uint32_t ph = (uint32_t)(kb / Cfg::STAGES) & 1u;
-        mbar_wait(&full_bar[s], ph);
+      int it = 0, local = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++local) {
+        const int acc = local & 1;
+        const uint32_t aph = (uint32_t)(local >> 1) & 1u;
+        mbar_wait(&tempty[acc], aph ^ 1u);  // epilogue drained this accumulator
         tc_fence_after();
-        const uint32_t sa = smem_u32(tiles + s * Cfg::STAGE_BYTES);
-        const uint32_t sb = sa + Cfg::A_BYTES;
+        const uint32_t tacc = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % Cfg::STAGES;
+          const uint32_t ph = (uint32_t)(it / Cfg::STAGES) & 1u;
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(tiles + s * Cfg::STAGE_BYTES);
+          const uint32_t sb = sa + Cfg::A_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < BK / UK; ++kk) {
-          // K-major: advance 16 elements (32 B) inside the 128 B swizzle row;
-          // MN-major: advance 16 k-rows (2 KB), i.e. two 8-row core-matrix groups.
-          const uint64_t ad = A_MN ? smem_desc(sa + kk * 2048, 8192, 1024)
-                                   : smem_desc(sa + kk * 32, 16, 1024);
-          const uint64_t bd = B_MN ? smem_desc(sb + kk * 2048, 8192, 1024)
-                                   : smem_desc(sb + kk * 32, 16, 1024);
-          umma_bf16(tmem_base, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < BK / UK; ++kk) {
+            // K-major: advance 16 elements (32 B) inside the 128 B swizzle row;
+            // MN-major: advance 16 k-rows (2 KB), i.e. two 8-row core-matrix groups.
+            const uint64_t ad = A_MN ? smem_desc(sa + kk * 2048, 8192, 1024)
+                                     : smem_desc(sa + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc(sb + kk * 2048, 8192, 1024)
+                                     : smem_desc(sb + kk * 32, 16, 1024);
+            umma_bf16(tacc, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[s]);  // frees the smem stage once these MMAs have read it
         }
-        umma_commit(&empty_bar[s]);  // frees the smem stage once these MMAs have read it
+        umma_commit(&tfull[acc]);  // accumulator complete
       }
-      umma_commit(tmem_full);  // accumulator complete
     }
   } else {
     // ---------------- epilogue: TMEM -> registers -> fused op -> global
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = q * 32 + lane;
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
+    int local = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++local) {
+      int mb, nb;
+      tile_coords(tile, tiles_m, tiles_n, mb, nb);
+      const int64_t m0 = (int64_t)mb * BM, n0 = (int64_t)nb * BN;
+      const int acc = local & 1;
+      const uint32_t aph = (uint32_t)(local >> 1) & 1u;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      float v[32];
-      tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), v);
-      if (n0 + c * 32 < g.N) store_chunk<EPI>(g, m0 + row, n0 + c * 32, v);
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
+        if (n0 + c * 32 < g.N) store_chunk<EPI>(g, m0 + row, n0 + c * 32, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
   tc_fence_before();
@@ -311,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"((uint32_t)Cfg::TMEM_COLS));
+                 "r"((uint32_t)(2 * Cfg::TMEM_COLS)));
   }
 }
 
@@ -391,8 +440,10 @@ void launch_tc(const GemmArgs& g, cudaStream_t st) {
                               : make_map(g.A, g.K, g.M, g.lda, BK, BM);
   const CUtensorMap mb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, BK)
                               : make_map(g.B, g.K, g.N, g.ldb, BK, BN);
-  dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM));
-  kern<<<grid, kThreads, Cfg::SMEM, st>>>(ma, mb, g);
+  const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);
+  const int ntiles = tiles_m * tiles_n;
+  const int grid = ntiles < kNumSMs ? ntiles : kNumSMs;
+  kern<<<grid, kThreads, Cfg::SMEM, st>>>(ma, mb, g, tiles_m, tiles_n);
   SPL_CHECK_LAUNCH();
 }
 

@@ -667,9 +667,10 @@ class Layer final : public LayerBase {
 
   // g (forward) / ḡ-dual (backward): shards {RL,h} -> full {RF,h}
   void gather(std::function<const void*(int)> shard, std::function<void*(int)> full, CommTag tag) {
+    comm_->log(tag, 0, RF_ * h_);
+    if (t_ == 1) return;  // identity; callers read the shard itself (see gathered())
     auto s = cptrs(shard);
     auto f = mptrs(full);
-    comm_->log(tag, 0, RF_ * h_);
     launch(K_COMM, 1, 0, (double)RF_ * h_ * sizeof(T) * (t_ - 1) / t_,
            [&] { comm_->all_gather(s.data(), f.data(), RL_ * h_, dt(), st_); });
   }
@@ -677,9 +678,10 @@ class Layer final : public LayerBase {
   // all-reduce in place (f̄ / f), the result left in part.
   void scatter(CommTag tag) {
     if (sp_) {
+      comm_->log(tag, 1, RF_ * h_);
+      if (t_ == 1) return;  // identity: scattered(r) returns part
       auto p = cptrs([&](int r) { return (const void*)R_[r].part; });
       auto o = mptrs([&](int r) { return (void*)R_[r].rs_out; });
-      comm_->log(tag, 1, RF_ * h_);
       launch(K_COMM, 1, 0, (double)RF_ * h_ * sizeof(T) * (t_ - 1) / t_,
              [&] { comm_->reduce_scatter(p.data(), o.data(), RL_ * h_, dt(), st_); });
     } else if (t_ > 1) {
@@ -689,7 +691,10 @@ class Layer final : public LayerBase {
              [&] { comm_->all_reduce(p.data(), RF_ * h_, dt(), st_); });
     }
   }
-  T* scattered(int r) { return sp_ ? R_[r].rs_out : R_[r].part; }
+  T* scattered(int r) { return (sp_ && t_ > 1) ? R_[r].rs_out : R_[r].part; }
+  // the gathered {s,b,h} view of a sequence-sharded tensor (the shard itself when t == 1)
+  const T* gathered(int r, const T* shard) const { return (sp_ && t_ > 1) ? R_[r].yfull : shard; }
+  const T* gathered_d(int r, const T* shard) const { return (sp_ && t_ > 1) ? R_[r].dfull : shard; }
 
   // ------------------------------------------------------------------ schedules
   void run_forward(T* const* y, CommTag tag, int* nonfinite) {
@@ -708,7 +713,7 @@ class Layer final : public LayerBase {
                     [&](int r) { return (void*)R_[r].yfull; }, tag);
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
-      const T* y1 = sp_ ? R.yfull : R.y1_s;
+      const T* y1 = gathered(r, R.y1_s);
       // fused QKV projection, column-parallel (block.cpp:556-558)
       gemm(RF_, 3 * lw_, h, y1, h, Major::K, R.wqkv, 3 * lw_, Major::MN, R.qkv, 3 * lw_,
            Epi::Bias, R.bqkv);
@@ -732,7 +737,7 @@ class Layer final : public LayerBase {
                     [&](int r) { return (void*)R_[r].yfull; }, tag);  // block.cpp:580
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
-      const T* y2 = sp_ ? R.yfull : R.y2;
+      const T* y2 = gathered(r, R.y2);
       // FC1 + bias + GELU, keeping both pre- and post-activation (block.cpp:584-585)
       gemm(RF_, fw_, h, y2, h, Major::K, R.w1, fw_, Major::MN, R.gin, fw_, Epi::BiasGelu, R.b1,
            R.fin);
@@ -772,8 +777,8 @@ class Layer final : public LayerBase {
     }
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
-      const T* dmo = sp_ ? R.dfull : R.d_s;
-      const T* y2 = sp_ ? R.yfull : R.y2;
+      const T* dmo = gathered_d(r, R.d_s);
+      const T* y2 = gathered(r, R.y2);
       // FC2 dgrad fused with GELU backward (block.cpp:660, 662)
       gemm(RF_, fw_, h, dmo, h, Major::K, R.w2, h, Major::K, R.dgin, fw_, Epi::GeluBwd, nullptr,
            nullptr, R.gin, fw_);
@@ -817,8 +822,8 @@ class Layer final : public LayerBase {
     }
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
-      const T* dao = sp_ ? R.dfull : R.d_s;
-      const T* y1 = sp_ ? R.yfull : R.y1_s;
+      const T* dao = gathered_d(r, R.d_s);
+      const T* y1 = gathered(r, R.y1_s);
       gemm(RF_, lw_, h, dao, h, Major::K, R.wo, h, Major::K, R.dproj, lw_, Epi::Store);  // 699
       gemm(lw_, h, RF_, R.api, lw_, Major::MN, dao, h, Major::MN, R.dwo, h, Epi::F32);    // 700
       k::AttnArgs a = attn_args(r);
