@@ -122,6 +122,89 @@ __device__ __forceinline__ uint32_t compress4(uint32_t x) {
 }
 
 // =====================================================================================
+// softmax-dropout keep bits: bits[(hl*b + bj)*s + q][w] bit j = keep(q, 32w + j)
+// The mask depends only on (seed, layer, op, microbatch) and the global {a,b,s,s} index, not
+// on the data, so this RNG pass runs on a side stream concurrently with the tensor-core GEMMs
+// that precede attention (it uses the ALU/FMA pipes the GEMM leaves idle).
+// =====================================================================================
+// One warp per (head, batch, query) row, lanes over the row's 32-key words. Within a word the
+// high half of (row_base + key) and of the first xor-shift are loop-invariant (the carry out of
+// the low half is checked once per word), so a key costs ~40 integer instructions.
+template <uint32_t CL, uint32_t CH>
+__device__ __forceinline__ void mul_c(uint32_t& lo, uint32_t& hi) {  // (hi:lo) *= (CH:CL)
+  const uint64_t w = (uint64_t)lo * CL;
+  hi = (uint32_t)(w >> 32) + lo * CH + hi * CL;
+  lo = (uint32_t)w;
+}
+__device__ __forceinline__ void xs(uint32_t& lo, uint32_t& hi, int k) {  // x ^= x >> k, k < 32
+  lo ^= __funnelshift_r(lo, hi, k);
+  hi ^= hi >> k;
+}
+__device__ __forceinline__ bool keep_fast(uint32_t lo, uint32_t hi0, uint32_t hi_xs,
+                                          uint32_t mixed_lo, uint32_t mixed_hi, uint32_t t_lo,
+                                          uint32_t t_hi) {
+  // first mix_post with the (loop-invariant) high half's xor-shift pre-applied:
+  // hi_xs = hi0 ^ (hi0 >> 30)
+  lo ^= __funnelshift_r(lo, hi0, 30);
+  uint32_t hi = hi_xs;
+  mul_c<0x1ce4e5b9u, 0xbf58476du>(lo, hi);
+  xs(lo, hi, 27);
+  mul_c<0x133111ebu, 0x94d049bbu>(lo, hi);
+  xs(lo, hi, 31);
+  // ^ mix64(key), + G
+  lo ^= mixed_lo;
+  hi ^= mixed_hi;
+  const uint64_t v = (((uint64_t)hi << 32) | lo) + 0x9e3779b97f4a7c15ULL;
+  lo = (uint32_t)v;
+  hi = (uint32_t)(v >> 32);
+  xs(lo, hi, 30);
+  mul_c<0x1ce4e5b9u, 0xbf58476du>(lo, hi);
+  xs(lo, hi, 27);
+  mul_c<0x133111ebu, 0x94d049bbu>(lo, hi);
+  xs(lo, hi, 31);
+  return hi > t_hi || (hi == t_hi && lo >= t_lo);
+}
+
+__global__ void __launch_bounds__(256) keep_bits_k(DropKey key, int64_t head_offset, int lh,
+                                                   int b, int s, int W, int causal,
+                                                   uint32_t* __restrict__ bits) {
+  const Rng rng(key);
+  const uint32_t mixed_lo = (uint32_t)rng.mixed, mixed_hi = (uint32_t)(rng.mixed >> 32);
+  const uint32_t t_lo = (uint32_t)rng.tsh, t_hi = (uint32_t)(rng.tsh >> 32);
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int nrows = lh * b * s;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < nrows; row += warps) {
+    const int q = row % s;
+    const int t = row / s;
+    const int bj = t % b, hl = t / b;
+    const uint64_t base = rng.row_base(((uint64_t)(head_offset + hl) * b + bj) * s + q, s);
+    uint32_t* out = bits + (int64_t)row * W;
+    for (int w = lane; w < W; w += 32) {
+      const int kbeg = 32 * w;
+      uint32_t word = 0;
+      if (!(causal && kbeg > q)) {
+        const uint64_t bw = base + (uint64_t)kbeg;
+        const uint32_t blo = (uint32_t)bw, bhi = (uint32_t)(bw >> 32);
+        const int kend = kbeg + 32 <= s ? 32 : s - kbeg;
+        if (blo <= 0xffffffffu - 31u) {  // no carry into the high half inside this word
+          const uint32_t hx = bhi ^ (bhi >> 30);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            word |= (keep_fast(blo + j, bhi, hx, mixed_lo, mixed_hi, t_lo, t_hi) ? 1u : 0u) << j;
+        } else {
+#pragma unroll 1
+          for (int j = 0; j < 32; ++j)
+            word |= (rng.keep(base, (uint32_t)(kbeg + j)) ? 1u : 0u) << j;
+        }
+        if (kend < 32) word &= (1u << kend) - 1u;
+      }
+      out[w] = word;
+    }
+  }
+}
+
+// =====================================================================================
 // forward
 // =====================================================================================
 template <int HD, bool CAUSAL, bool MAT>
@@ -140,14 +223,14 @@ __global__ void __launch_bounds__(128) fa_fwd(AttnArgs a) {
   const int64_t rstride = a.b * a.ld;
   const int64_t qcol = a.qoff + (int64_t)hl * HD, kcol = a.koff + (int64_t)hl * HD,
                 vcol = a.voff + (int64_t)hl * HD;
-  const Rng rng(a.drop);
+  const bool drop_on = a.drop.thresh != 0;
+  const int W = (S + 31) / 32;
+  const int64_t brow = ((int64_t)hl * a.b + bj) * a.s;  // keep-bit / lse row base
   // MAT (materialised interior, causal included) visits every key tile; otherwise causal
   // stops at the diagonal.
   const int kv_end = (CAUSAL && !MAT) ? min(S, q0 + BM) : S;
   const int nkv = (kv_end + BN - 1) / BN;
   const int row0 = q0 + warp * 16 + g;  // this thread's rows: row0, row0 + 8
-  const uint64_t rowidx = ((uint64_t)(a.head_offset + hl) * a.b + bj) * a.s;
-  const uint64_t rb[2] = {rng.row_base(rowidx + row0, a.s), rng.row_base(rowidx + row0 + 8, a.s)};
   const float sl2 = a.scale * kLog2e;
 
   uint32_t qf[HD / 16][4];
@@ -278,6 +361,14 @@ __global__ void __launch_bounds__(128) fa_fwd(AttnArgs a) {
       }
     }
     const float mr[2] = {m[0] == -INFINITY ? 0.f : m[0], m[1] == -INFINITY ? 0.f : m[1]};
+    uint32_t kw[2][2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        const int qr = row0 + r * 8, wd = k0 / 32 + w;
+        kw[r][w] = !drop_on ? 0xffffffffu : (qr < S && wd < W) ? a.keepbits[(brow + qr) * W + wd] : 0u;
+      }
     uint32_t pa[BN / 16][4];
 #pragma unroll
     for (int nb = 0; nb < BN / 8; ++nb) {
@@ -289,8 +380,9 @@ __global__ void __launch_bounds__(128) fa_fwd(AttnArgs a) {
         float pv = ex2(sacc[nb][e] - mr[r]);
         if (!MAT) l[r] += pv;
         else pv *= inv_l[r];
-        const uint32_t key = (uint32_t)(k0 + nb * 8 + 2 * tq + (e & 1));
-        kp[e] = rng.keep(rb[r], key) && (MAT ? key < (uint32_t)S : pv != 0.f);
+        const int kl = nb * 8 + 2 * tq + (e & 1);
+        const bool bit = (kw[r][kl >> 5] >> (kl & 31)) & 1u;
+        kp[e] = bit && (MAT ? k0 + kl < S : pv != 0.f);
         p[e] = pv;
         pd[e] = kp[e] ? pv * a.drop.inv_keep : 0.f;
       }
@@ -343,8 +435,7 @@ __global__ void __launch_bounds__(128) fa_fwd(AttnArgs a) {
     for (int db = 0; db < HD / 8; ++db)
       *reinterpret_cast<uint32_t*>(orow + db * 8 + 2 * tq) =
           pack_bf16(o[db][2 * r] * inv, o[db][2 * r + 1] * inv);
-    if (tq == 0 && a.lse)
-      a.lse[((int64_t)hl * a.b + bj) * a.s + qr] = (m[r] + log2f(l[r])) * kLn2;
+    if (tq == 0 && a.lse) a.lse[brow + qr] = (m[r] + log2f(l[r])) * kLn2;
   }
 }
 
@@ -385,7 +476,6 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __res
   bf16* Ds = Qs + 2 * BQ * LDS;    // [2][BQ][LDS] dO
   float* lse_s = reinterpret_cast<float*>(Ds + 2 * BQ * LDS);  // [2][BQ]
   float* dl_s = lse_s + 2 * BQ;                                // [2][BQ]
-  uint16_t* kb16 = reinterpret_cast<uint16_t*>(dl_s + 2 * BQ); // [2][BQ][4] keep bits
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
   const int k0 = blockIdx.x * BK_;
@@ -398,9 +488,10 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __res
                 vcol = a.voff + (int64_t)hl * HD;
   const int64_t rowbase = ((int64_t)hl * a.b + bj) * a.s;  // lse/delta/bits row index base
   const float sl2 = a.scale * kLog2e;
-  const Rng rng(a.drop);
-  const uint64_t growbase = ((uint64_t)(a.head_offset + hl) * a.b + bj) * a.s;
+  const bool drop_on = a.drop.thresh != 0;
   const int W = (S + 31) / 32;
+  const int kword = k0 / 32 + warp / 2;          // the 32-key word holding this warp's keys
+  const int kbit = (warp & 1) * 16 + g;          // bit of key0 in that word (key0 + 8: +8)
 
   const int q_start = CAUSAL ? (k0 / BQ) * BQ : 0;
   const int nq = (S - q_start + BQ - 1) / BQ;
@@ -413,19 +504,6 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __res
       const int q = qb + threadIdx.x;
       lse_s[buf * BQ + threadIdx.x] = (q < S && !STORED) ? a.lse[rowbase + q] * kLog2e : INFINITY;
       dl_s[buf * BQ + threadIdx.x] = q < S ? delta[rowbase + q] : 0.f;
-    }
-  };
-  // flush the keep bits of q-tile `it` (buffer buf) to global
-  auto flush_bits = [&](int it, int buf) {
-    if (STORED || a.keepbits == nullptr) return;
-    if (threadIdx.x < BQ * 2) {
-      const int qi = threadIdx.x >> 1, wi = threadIdx.x & 1;
-      const int q = q_start + it * BQ + qi;
-      const int word = k0 / 32 + wi;
-      if (q < S && word < W) {
-        const uint16_t* src = kb16 + (buf * BQ + qi) * 4 + wi * 2;
-        a.keepbits[(rowbase + q) * W + word] = (uint32_t)src[0] | ((uint32_t)src[1] << 16);
-      }
     }
   };
   load_tile<HD, BK_, NT>(Ks, base, k0, a.s, rstride, kcol);
@@ -442,8 +520,7 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __res
 
   for (int it = 0; it < nq; ++it) {
     const int buf = it & 1;
-    __syncthreads();  // all warps done with iteration it-1 (its bits are complete)
-    if (it > 0) flush_bits(it - 1, buf ^ 1);
+    __syncthreads();  // all warps done with iteration it-1
     if (it + 1 < nq) {
       load_q(it + 1, buf ^ 1);
       cp_commit();
@@ -483,13 +560,13 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __res
 #pragma unroll
     for (int nb = 0; nb < BQ / 8; ++nb) {
       float pd[4], ds[4];
-      uint32_t ball[4];
 #pragma unroll
       for (int par = 0; par < 2; ++par) {
         const int qi = nb * 8 + 2 * tq + par;
         const int q = qb + qi;
         const float lqv = lq[qi], dqv = dq_[qi];
-        const uint64_t rbq = STORED ? 0 : rng.row_base(growbase + q, a.s);
+        const uint32_t kwd = (STORED || !drop_on) ? 0xffffffffu
+                             : (q < S && kword < W) ? a.keepbits[(rowbase + q) * W + kword] : 0u;
 #pragma unroll
         for (int kr = 0; kr < 2; ++kr) {
           const int e = kr * 2 + par;
@@ -506,20 +583,12 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __res
             }
           } else {
             p = valid ? ex2(st[nb][e] * sl2 - lqv) : 0.f;
-            keep = rng.keep(rbq, (uint32_t)key) && p != 0.f;
+            keep = ((kwd >> (kbit + kr * 8)) & 1u) && p != 0.f;
             pdv = keep ? p * a.drop.inv_keep : 0.f;
-            ball[e] = __ballot_sync(0xffffffffu, keep);
           }
           pd[e] = pdv;
           const float dp = keep ? dpt[nb][e] * a.drop.inv_keep : 0.f;
           ds[e] = p * (dp - dqv);
-        }
-      }
-      if (!STORED && g == 0) {
-#pragma unroll
-        for (int par = 0; par < 2; ++par) {
-          const uint32_t lo = compress4(ball[par] >> tq), hi = compress4(ball[2 + par] >> tq);
-          kb16[(buf * BQ + nb * 8 + 2 * tq + par) * 4 + warp] = (uint16_t)(lo | (hi << 8));
         }
       }
       const int kk2 = nb >> 1, hi = nb & 1;
@@ -542,9 +611,6 @@ __global__ void __launch_bounds__(128) fa_bwd_dkdv(AttnArgs a, const bf16* __res
       }
     }
   }
-  __syncthreads();
-  flush_bits(nq - 1, (nq - 1) & 1);
-  // the causal tiles skipped above (q < k0) hold no keep bits the dQ kernel reads
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const int key = key0 + r * 8;
@@ -731,7 +797,7 @@ void launch_bwd_t(const AttnArgs& a, const bf16* dout, bf16* dqkv, float* delta,
   const int64_t rows = a.lh * a.b * a.s;
   fa_delta<HD><<<(unsigned)((rows + 3) / 4), 128, 0, st>>>(a, dout, delta);
   SPL_CHECK_LAUNCH();
-  const int smem_kv = (2 * 64 * LDS + 4 * 32 * LDS) * 2 + 4 * 32 * 4 + 2 * 32 * 4 * 2;
+  const int smem_kv = (2 * 64 * LDS + 4 * 32 * LDS) * 2 + 4 * 32 * 4;
   const int smem_q = (2 * 64 * LDS + 4 * 32 * LDS) * 2;
   static bool once = [&] {
     SPL_CUDA(cudaFuncSetAttribute(fa_bwd_dkdv<HD, CAUSAL, STORED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv));
@@ -778,6 +844,7 @@ bool attn_tc_supported<bf16>(const AttnArgs& a) {
 
 template <>
 void attn_fwd_tc<bf16>(const AttnArgs& a, cudaStream_t st) {
+  require(a.keepbits != nullptr || a.drop.thresh == 0, "attention forward: keep-bit buffer missing");
   const bool mat = a.sm != nullptr;
   SPL_HD_SWITCH(a.hd, {
     if (a.causal) {
@@ -792,7 +859,7 @@ template <>
 void attn_bwd_tc<bf16>(const AttnArgs& a, const void* dout, void* dqkv, float* delta,
                        cudaStream_t st) {
   const bool stored = a.sm != nullptr;
-  if (!stored) require(a.keepbits != nullptr || a.drop.thresh == 0, "attention backward: keep-bit workspace missing");
+  if (!stored) require(a.keepbits != nullptr || a.drop.thresh == 0, "attention backward: keep-bit buffer missing");
   const bf16* d = static_cast<const bf16*>(dout);
   bf16* g = static_cast<bf16*>(dqkv);
   SPL_HD_SWITCH(a.hd, {
@@ -802,6 +869,18 @@ void attn_bwd_tc<bf16>(const AttnArgs& a, const void* dout, void* dqkv, float* d
       if (stored) launch_bwd_t<HD, false, true>(a, d, g, delta, st); else launch_bwd_t<HD, false, false>(a, d, g, delta, st);
     }
   });
+}
+
+void attn_keep_bits(const AttnArgs& a, cudaStream_t st) {
+  if (a.drop.thresh == 0 || a.keepbits == nullptr) return;
+  require(a.lh * a.b * a.s < (1ll << 31), "keep bits: too many rows");
+  const int W = (int)((a.s + 31) / 32);
+  const int64_t rows = a.lh * a.b * a.s;
+  int64_t grid = (rows + 7) / 8;  // 8 warps (rows) per CTA
+  if (grid > kNumSMs * 16) grid = kNumSMs * 16;
+  keep_bits_k<<<(unsigned)grid, 256, 0, st>>>(a.drop, a.head_offset, (int)a.lh, (int)a.b,
+                                              (int)a.s, W, a.causal, a.keepbits);
+  SPL_CHECK_LAUNCH();
 }
 
 }  // namespace spl::k

@@ -124,8 +124,8 @@ struct AttnArgs {
   void* sm = nullptr;
   uint8_t* mask = nullptr;
   void* sd = nullptr;
-  // backward workspace for the recompute regimes: keep bits [lh*b*s][ceil(s/32)] written by
-  // the dK/dV kernel (one RNG pass) and read by the dQ kernel.
+  // softmax-dropout keep bits [lh*b*s][ceil(s/32)] from attn_keep_bits (bf16 tensor-core path);
+  // a transient buffer refilled before each attention forward and backward.
   uint32_t* keepbits = nullptr;
 };
 inline int64_t keepbits_words(int64_t lh, int64_t b, int64_t s) { return lh * b * s * ((s + 31) / 32); }
@@ -137,5 +137,7 @@ void attn_fwd(const AttnArgs& a, cudaStream_t st);
 // the stored interior when a.sm != nullptr (no-recompute). delta: [lh*b*s] fp32 scratch.
 template <typename T>
 void attn_bwd(const AttnArgs& a, const void* dout, void* dqkv, float* delta, cudaStream_t st);
+// The counter-RNG pass alone: fills a.keepbits (data-independent; may run on a side stream).
+void attn_keep_bits(const AttnArgs& a, cudaStream_t st);
 
 }  // namespace spl::k

@@ -11,6 +11,7 @@
 // Local ranks r of a handle map to global TP ranks rank0 + r.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <type_traits>
@@ -61,9 +62,14 @@ class Layer final : public LayerBase {
     k_mlp_ = make_drop_key(d.seed, d.layer_index, kMlpDrop, d.microbatch, d.dropout_p);
     SPL_CUDA(cudaSetDevice(dev_));
     SPL_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    SPL_CUDA(cudaStreamCreateWithFlags(&st_rng_, cudaStreamNonBlocking));
+    SPL_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    SPL_CUDA(cudaEventCreateWithFlags(&ev_bits_, cudaEventDisableTiming));
     SPL_CUDA(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming));
     SPL_CUDA(cudaEventCreateWithFlags(&ev_out_, cudaEventDisableTiming));
     allocate();
+    const char* e = std::getenv("SPL_KEEPBITS_SERIAL");
+    bits_serial_ = e != nullptr && e[0] == '1';
   }
 
   ~Layer() override {
@@ -74,6 +80,10 @@ class Layer final : public LayerBase {
     for (auto& e : evpool_) cudaEventDestroy(e);
     cudaEventDestroy(ev_in_);
     cudaEventDestroy(ev_out_);
+    cudaEventDestroy(ev_fork_);
+    cudaEventDestroy(ev_bits_);
+    cudaStreamSynchronize(st_rng_);
+    cudaStreamDestroy(st_rng_);
     cudaStreamDestroy(st_);
   }
 
@@ -361,6 +371,7 @@ class Layer final : public LayerBase {
     a.sm = sm;
     a.mask = mk;
     a.sd = sd;
+    k::attn_keep_bits(a, st_);
     k::attn_fwd<T>(a, st_);
     k::cast_to_f64<T>(sm, dbuf, n, st_);
     k::u8_to_f64(mk, dbuf + n, n, st_);
@@ -509,7 +520,6 @@ class Layer final : public LayerBase {
     const int64_t npart = std::max<int64_t>(2 * (int64_t)nch_l * h_, nch_f * std::max<int64_t>(3 * lw_, fw_));
     T *yfull = nullptr, *dfull = nullptr, *dgin = nullptr, *dqkv = nullptr, *dproj = nullptr;
     float *delta = nullptr, *partials = nullptr;
-    uint32_t* keepbits = nullptr;
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
       R.wqkv = alloc<T>(h_ * 3 * lw_, kParam, r);
@@ -567,10 +577,11 @@ class Layer final : public LayerBase {
         dproj = alloc<T>(RF_ * lw_, kWork, r);
         delta = alloc<float>(lh_ * b_ * s_, kWork, r);
         partials = alloc<float>(npart, kWork, r);
-        if (kind_ != SPL_RECOMPUTE_NONE)  // backward-only keep bits (transient, 1 bit/elem)
-          keepbits = alloc<uint32_t>(k::keepbits_words(lh_, b_, s_), kWork, r);
       }
-      R.keepbits = keepbits;
+      // transient keep bits of the softmax dropout (1 bit / interior element), refilled on the
+      // side stream at the start of every forward and backward call
+      if (std::is_same_v<T, bf16> && d_.dropout_p > 0.0)
+        R.keepbits = alloc<uint32_t>(k::keepbits_words(lh_, b_, s_), kWork, r);
       R.dgin = dgin;
       R.dqkv = dqkv;
       R.dproj = dproj;
@@ -592,6 +603,10 @@ class Layer final : public LayerBase {
   // ---- launch bookkeeping
   template <typename F>
   void launch(KClass cls, int kernels, double flops, double bytes, F&& f) {
+    launch_on(st_, cls, kernels, flops, bytes, std::forward<F>(f));
+  }
+  template <typename F>
+  void launch_on(cudaStream_t stream, KClass cls, int kernels, double flops, double bytes, F&& f) {
     launches_ += kernels;
     if (!profiling_) {
       f();
@@ -605,9 +620,9 @@ class Layer final : public LayerBase {
       }
     }
     cudaEvent_t ea = evpool_[ev_next_++], eb = evpool_[ev_next_++];
-    SPL_CUDA(cudaEventRecord(ea, st_));
+    SPL_CUDA(cudaEventRecord(ea, stream));
     f();
-    SPL_CUDA(cudaEventRecord(eb, st_));
+    SPL_CUDA(cudaEventRecord(eb, stream));
     pending_.push_back({ea, eb, cls});
     prof_n_[cls] += kernels;
     prof_flops_[cls] += flops;
@@ -696,8 +711,36 @@ class Layer final : public LayerBase {
   const T* gathered(int r, const T* shard) const { return (sp_ && t_ > 1) ? R_[r].yfull : shard; }
   const T* gathered_d(int r, const T* shard) const { return (sp_ && t_ > 1) ? R_[r].dfull : shard; }
 
+  // Fork the data-independent dropout-mask RNG onto the side stream (it overlaps the GEMMs
+  // that precede attention); join() makes the main stream wait for it.
+  void fork_keep_bits() {
+    if (R_.empty() || R_[0].keepbits == nullptr) return;
+    if (bits_serial_) {  // on the main stream, right before its consumer
+      for (int r = 0; r < L_; ++r) {
+        k::AttnArgs a = attn_args(r);
+        launch(K_OTHER, 1, 0, (double)lh_ * b_ * s_ * s_ / 8.0, [&] { k::attn_keep_bits(a, st_); });
+      }
+      return;
+    }
+    SPL_CUDA(cudaEventRecord(ev_fork_, st_));
+    SPL_CUDA(cudaStreamWaitEvent(st_rng_, ev_fork_, 0));
+    for (int r = 0; r < L_; ++r) {
+      k::AttnArgs a = attn_args(r);
+      const double elems = (double)lh_ * b_ * s_ * s_;
+      launch_on(st_rng_, K_OTHER, 1, 0, elems / 8.0, [&] { k::attn_keep_bits(a, st_rng_); });
+    }
+    SPL_CUDA(cudaEventRecord(ev_bits_, st_rng_));
+    bits_pending_ = true;
+  }
+  void join_keep_bits() {
+    if (!bits_pending_) return;
+    SPL_CUDA(cudaStreamWaitEvent(st_, ev_bits_, 0));
+    bits_pending_ = false;
+  }
+
   // ------------------------------------------------------------------ schedules
   void run_forward(T* const* y, CommTag tag, int* nonfinite) {
+    fork_keep_bits();
     const int64_t h = h_;
     const float eps = (float)d_.ln_eps;
     const double eb = sizeof(T);
@@ -719,6 +762,7 @@ class Layer final : public LayerBase {
            Epi::Bias, R.bqkv);
       // attention interior + attention over values (block.cpp:559-562)
       k::AttnArgs a = attn_args(r);
+      join_keep_bits();
       launch(K_ATTN, 1, attn_flops(false), 0, [&] { k::attn_fwd<T>(a, st_); });
       // row-parallel projection partial (block.cpp:563)
       gemm(RF_, h, lw_, R.api, lw_, Major::K, R.wo, h, Major::MN, R.part, h, Epi::Store);
@@ -757,6 +801,9 @@ class Layer final : public LayerBase {
 
   void run_backward(const void* const* dyv, void* const* dxv) {
     const int64_t h = h_;
+    // recompute regimes regenerate the keep bits (full recomputation just re-ran the forward,
+    // whose bits are still in the buffer); the no-recompute regime reads the stored mask
+    if (kind_ == SPL_RECOMPUTE_SELECTIVE) fork_keep_bits();
     const double eb = sizeof(T);
     const int nch_l = k::num_chunks(RL_, kChunkRows), nch_f = k::num_chunks(RF_, kChunkRows);
     const float inv_keep = k_mlp_.inv_keep;
@@ -827,6 +874,7 @@ class Layer final : public LayerBase {
       gemm(RF_, lw_, h, dao, h, Major::K, R.wo, h, Major::K, R.dproj, lw_, Epi::Store);  // 699
       gemm(lw_, h, RF_, R.api, lw_, Major::MN, dao, h, Major::MN, R.dwo, h, Epi::F32);    // 700
       k::AttnArgs a = attn_args(r);
+      join_keep_bits();
       launch(K_ATTN, 3, attn_flops(true), 0,
              [&] { k::attn_bwd<T>(a, R.dproj, R.dqkv, R.delta, st_); });  // 701-702
       launch(K_ELEM, 2, 0, eb * RF_ * 3 * lw_, [&] {
@@ -872,7 +920,8 @@ class Layer final : public LayerBase {
   float scale_ = 1.f;
   DropKey k_soft_{}, k_attn_{}, k_mlp_{};
   cudaStream_t st_ = nullptr;
-  cudaEvent_t ev_in_ = nullptr, ev_out_ = nullptr;
+  cudaEvent_t ev_in_ = nullptr, ev_out_ = nullptr, ev_fork_ = nullptr, ev_bits_ = nullptr;
+  cudaStream_t st_rng_ = nullptr;  // side stream: data-independent dropout keep bits
   cudaStream_t caller_ = 0;  // legacy default stream unless set
   std::vector<Rank> R_;
   std::vector<Alloc> allocs_;
@@ -880,6 +929,8 @@ class Layer final : public LayerBase {
   void* pinned_ = nullptr;
   int* nonfinite_ = nullptr;
   bool have_fwd_ = false;
+  bool bits_pending_ = false;
+  bool bits_serial_ = false;  // SPL_KEEPBITS_SERIAL=1: RNG pass on the main stream
   bool graphs_ = false;
   // profiling
   struct Pending {
