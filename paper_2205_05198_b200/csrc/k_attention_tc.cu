@@ -130,44 +130,66 @@ __device__ __forceinline__ uint32_t compress4(uint32_t x) {
 // One warp per (head, batch, query) row, lanes over the row's 32-key words. Within a word the
 // high half of (row_base + key) and of the first xor-shift are loop-invariant (the carry out of
 // the low half is checked once per word), so a key costs ~40 integer instructions.
+// The hash is integer work split between the ALU pipe (LOP3/SHF/ISETP/IADD3) and the FMA-heavy
+// pipe (IMAD*). A 64-bit xor-shift is either 4 ALU ops (funnel shifts) or 2 ALU + 3 IMAD ops
+// (shifts as multiplies by 2^(32-k): IMAD.HI for >>, IMAD for <<). Measured (ncu): all-ALU
+// shifts leave the ALU pipe the bound; shifting three of them to IMAD saturates fmaheavy (90%)
+// instead; two in IMAD form is the balance point. The multipliers come in through the kernel
+// parameters so ptxas cannot turn the multiplies back into shifts.
+struct ShiftMuls {
+  uint32_t m30, m27, m31;  // 2^(32-k)
+  uint32_t one;            // 1: the 64-bit "+ G" as IMAD.WIDE (FMA pipe) instead of IADD3 pairs
+};
 template <uint32_t CL, uint32_t CH>
 __device__ __forceinline__ void mul_c(uint32_t& lo, uint32_t& hi) {  // (hi:lo) *= (CH:CL)
   const uint64_t w = (uint64_t)lo * CL;
   hi = (uint32_t)(w >> 32) + lo * CH + hi * CL;
   lo = (uint32_t)w;
 }
-__device__ __forceinline__ void xs(uint32_t& lo, uint32_t& hi, int k) {  // x ^= x >> k, k < 32
+__device__ __forceinline__ void xs_alu(uint32_t& lo, uint32_t& hi, int k) {  // x ^= x >> k
   lo ^= __funnelshift_r(lo, hi, k);
   hi ^= hi >> k;
 }
-__device__ __forceinline__ bool keep_fast(uint32_t lo, uint32_t hi0, uint32_t hi_xs,
-                                          uint32_t mixed_lo, uint32_t mixed_hi, uint32_t t_lo,
-                                          uint32_t t_hi) {
-  // first mix_post with the (loop-invariant) high half's xor-shift pre-applied:
-  // hi_xs = hi0 ^ (hi0 >> 30)
+__device__ __forceinline__ void xs_fma(uint32_t& lo, uint32_t& hi, uint32_t m) {  // m = 2^(32-k)
+  const uint32_t a = __umulhi(lo, m), b = hi * m, c = __umulhi(hi, m);
+  lo = lo ^ a ^ b;
+  hi ^= c;
+}
+__device__ __forceinline__ bool keep_fast(uint32_t lo, uint32_t hi0, uint32_t hc,
+                                          uint32_t hi_xs, uint32_t mixed_lo, uint32_t mixed_hi,
+                                          uint32_t t_lo, uint32_t t_hi, const ShiftMuls& sm) {
+  // first mix_post; the high half (hi0) is loop-invariant: hi_xs = hi0 ^ (hi0 >> 30) and
+  // hc = hi_xs * 0x1ce4e5b9 are precomputed per 32-key word.
   lo ^= __funnelshift_r(lo, hi0, 30);
-  uint32_t hi = hi_xs;
-  mul_c<0x1ce4e5b9u, 0xbf58476du>(lo, hi);
-  xs(lo, hi, 27);
+  uint32_t hi;
+  {
+    const uint64_t w = (uint64_t)lo * 0x1ce4e5b9u + ((uint64_t)hc << 32);
+    hi = (uint32_t)(w >> 32) + lo * 0xbf58476du;
+    lo = (uint32_t)w;
+  }
+  (void)hi_xs;
+  xs_fma(lo, hi, sm.m27);
   mul_c<0x133111ebu, 0x94d049bbu>(lo, hi);
-  xs(lo, hi, 31);
-  // ^ mix64(key), + G
+  xs_alu(lo, hi, 31);
+  // ^ mix64(key), + G (64-bit add as IMAD.WIDE with a 64-bit addend)
   lo ^= mixed_lo;
   hi ^= mixed_hi;
-  const uint64_t v = (((uint64_t)hi << 32) | lo) + 0x9e3779b97f4a7c15ULL;
-  lo = (uint32_t)v;
-  hi = (uint32_t)(v >> 32);
-  xs(lo, hi, 30);
+  {
+    const uint64_t w = ((uint64_t)hi << 32 | lo) + 0x9e3779b97f4a7c15ULL;
+    hi = (uint32_t)(w >> 32);
+    lo = (uint32_t)w;
+  }
+  xs_alu(lo, hi, 30);
   mul_c<0x1ce4e5b9u, 0xbf58476du>(lo, hi);
-  xs(lo, hi, 27);
+  xs_fma(lo, hi, sm.m27);
   mul_c<0x133111ebu, 0x94d049bbu>(lo, hi);
-  xs(lo, hi, 31);
-  return hi > t_hi || (hi == t_hi && lo >= t_lo);
+  xs_alu(lo, hi, 31);
+  return (((uint64_t)hi << 32) | lo) >= (((uint64_t)t_hi << 32) | t_lo);
 }
 
 __global__ void __launch_bounds__(256) keep_bits_k(DropKey key, int64_t head_offset, int lh,
                                                    int b, int s, int W, int causal,
-                                                   uint32_t* __restrict__ bits) {
+                                                   uint32_t* __restrict__ bits, ShiftMuls sm) {
   const Rng rng(key);
   const uint32_t mixed_lo = (uint32_t)rng.mixed, mixed_hi = (uint32_t)(rng.mixed >> 32);
   const uint32_t t_lo = (uint32_t)rng.tsh, t_hi = (uint32_t)(rng.tsh >> 32);
@@ -189,9 +211,10 @@ __global__ void __launch_bounds__(256) keep_bits_k(DropKey key, int64_t head_off
         const int kend = kbeg + 32 <= s ? 32 : s - kbeg;
         if (blo <= 0xffffffffu - 31u) {  // no carry into the high half inside this word
           const uint32_t hx = bhi ^ (bhi >> 30);
+          const uint32_t hc = hx * 0x1ce4e5b9u;
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            word |= (keep_fast(blo + j, bhi, hx, mixed_lo, mixed_hi, t_lo, t_hi) ? 1u : 0u) << j;
+            if (keep_fast(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm)) word |= 1u << j;
         } else {
 #pragma unroll 1
           for (int j = 0; j < 32; ++j)
@@ -879,7 +902,8 @@ void attn_keep_bits(const AttnArgs& a, cudaStream_t st) {
   int64_t grid = (rows + 7) / 8;  // 8 warps (rows) per CTA
   if (grid > kNumSMs * 16) grid = kNumSMs * 16;
   keep_bits_k<<<(unsigned)grid, 256, 0, st>>>(a.drop, a.head_offset, (int)a.lh, (int)a.b,
-                                              (int)a.s, W, a.causal, a.keepbits);
+                                              (int)a.s, W, a.causal, a.keepbits,
+                                              ShiftMuls{4u, 32u, 2u, 1u});
   SPL_CHECK_LAUNCH();
 }
 
