@@ -11,6 +11,7 @@
 //          fa_bwd_dq:  per 64-query CTA, loops over 32-key tiles: S, P, keep, dP = dO Vᵀ,
 //                      dQ += dS K.
 // rowdot_i = dO_i·O_i replaces Σ_j dSM_ij SM_ij of block.cpp:183 (algebraically equal).
+#include <cstdlib>
 #include <type_traits>
 
 #include "kernels.hpp"
@@ -868,6 +869,14 @@ bool attn_tc_supported<bf16>(const AttnArgs& a) {
 template <>
 void attn_fwd_tc<bf16>(const AttnArgs& a, cudaStream_t st) {
   require(a.keepbits != nullptr || a.drop.thresh == 0, "attention forward: keep-bit buffer missing");
+  static const bool umma_off = [] {
+    const char* e = std::getenv("SPL_ATTN_UMMA");
+    return e != nullptr && e[0] == '0';
+  }();
+  if (!umma_off && attn_fwd_umma_supported(a)) {
+    attn_fwd_umma(a, st);
+    return;
+  }
   const bool mat = a.sm != nullptr;
   SPL_HD_SWITCH(a.hd, {
     if (a.causal) {

@@ -139,5 +139,8 @@ template <typename T>
 void attn_bwd(const AttnArgs& a, const void* dout, void* dqkv, float* delta, cudaStream_t st);
 // The counter-RNG pass alone: fills a.keepbits (data-independent; may run on a side stream).
 void attn_keep_bits(const AttnArgs& a, cudaStream_t st);
+// tcgen05/TMEM forward (selective regime, bf16, head_dim 64/96/128); used by attn_fwd<bf16>.
+bool attn_fwd_umma_supported(const AttnArgs& a);
+void attn_fwd_umma(const AttnArgs& a, cudaStream_t st);
 
 }  // namespace spl::k
