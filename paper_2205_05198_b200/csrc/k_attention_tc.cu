@@ -887,10 +887,28 @@ void attn_fwd_tc<bf16>(const AttnArgs& a, cudaStream_t st) {
   });
 }
 
+bool attn_bwd_self_rng(const AttnArgs&) { return false; }
+
+static bool umma_bwd_on(const AttnArgs& a) {
+  static const bool off = [] {
+    const char* e = std::getenv("SPL_ATTN_UMMA");
+    return e != nullptr && e[0] == '0';
+  }();
+  return !off && attn_bwd_umma_supported(a);
+}
+
 template <>
 void attn_bwd_tc<bf16>(const AttnArgs& a, const void* dout, void* dqkv, float* delta,
                        cudaStream_t st) {
   const bool stored = a.sm != nullptr;
+  if (!stored && umma_bwd_on(a)) {
+    const int64_t rows = a.lh * a.b * a.s;
+    SPL_HD_SWITCH(a.hd, fa_delta<HD><<<(unsigned)((rows + 3) / 4), 128, 0, st>>>(
+                            a, static_cast<const bf16*>(dout), delta));
+    SPL_CHECK_LAUNCH();
+    attn_bwd_umma(a, dout, dqkv, delta, st);
+    return;
+  }
   if (!stored) require(a.keepbits != nullptr || a.drop.thresh == 0, "attention backward: keep-bit buffer missing");
   const bf16* d = static_cast<const bf16*>(dout);
   bf16* g = static_cast<bf16*>(dqkv);

@@ -349,9 +349,11 @@ EncodeFn encode_fn() {
   return fn;
 }
 
+}  // namespace
+
 // 3-D map over a {s, b, width} row-major bf16 buffer (row = s_i*b + b_j, stride ld elements):
 // dims {width, b, s}; box {64, 1, rows}; 128 B swizzle.
-CUtensorMap make_seq_map(const void* ptr, int64_t width, int64_t b, int64_t s, int64_t ld, int rows) {
+CUtensorMap attn_seq_map(const void* ptr, int64_t width, int64_t b, int64_t s, int64_t ld, int rows) {
   static std::mutex mu;
   static std::unordered_map<std::string, CUtensorMap> cache;
   char key[160];
@@ -376,6 +378,8 @@ CUtensorMap make_seq_map(const void* ptr, int64_t width, int64_t b, int64_t s, i
   return m;
 }
 
+namespace {
+
 template <int HD, bool CAUSAL>
 void launch_fwd_umma(const AttnArgs& a, cudaStream_t st) {
   using Cfg = FwdCfg<HD>;
@@ -385,7 +389,7 @@ void launch_fwd_umma(const AttnArgs& a, cudaStream_t st) {
     return true;
   }();
   (void)once;
-  const CUtensorMap mq = make_seq_map(a.qkv, a.ld, a.b, a.s, a.ld, 128);
+  const CUtensorMap mq = attn_seq_map(a.qkv, a.ld, a.b, a.s, a.ld, 128);
   dim3 grid((unsigned)((a.s + 127) / 128), (unsigned)(a.lh * a.b));
   fa_fwd_umma<HD, CAUSAL><<<grid, 320, Cfg::SMEM, st>>>(mq, a);
   SPL_CHECK_LAUNCH();

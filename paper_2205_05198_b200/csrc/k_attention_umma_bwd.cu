@@ -1,0 +1,521 @@
+// Attention backward on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), bf16, for the
+// recompute regimes (selective / full): nothing of the s×s interior comes from HBM.
+//
+// fa_bwd_dkdv_umma — CTA = 128 keys of one (head, batch), loops over 64-query tiles:
+//   MMA   Sᵀ = K·Qᵀ, dPᵀ = V·dOᵀ  (M=128 keys, N=64 queries)          -> TMEM (2 buffers)
+//   warps Pᵀ = exp2(Sᵀc - lse), keep from the keep-bit buffer (attn_keep_bits: one word per
+//         (query, 32 keys) = one warp's keys, broadcast by shuffle),
+//         P̃ᵀ = Pᵀ·keep/(1-p), dSᵀ = Pᵀ∘(dPᵀ·keep/(1-p) - rowdot)   -> bf16 smem (UMMA layout)
+//   MMA   dV += P̃ᵀ·dO, dK += dSᵀ·Q  (M=128, N=HD, K=64)               -> TMEM
+// fa_bwd_dq_umma — CTA = 128 queries, loops over 64-key tiles:
+//   MMA   S = Q·Kᵀ, dP = dO·Vᵀ; warps dS (same keep bits); MMA dQ += dS·K.
+// The counter-RNG pass that fills the keep bits (attn_keep_bits) runs once per backward.
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "kernels.hpp"
+#include "tc_common.cuh"
+
+namespace spl::k {
+
+CUtensorMap attn_seq_map(const void* ptr, int64_t width, int64_t b, int64_t s, int64_t ld, int rows);
+
+namespace {
+
+using namespace tc;
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int HD>
+struct BwdCfg {
+  static constexpr int ATOMS = (HD + 63) / 64;
+  static constexpr int T128 = ATOMS * 128 * 128;  // 128-row tile bytes
+  static constexpr int T64 = ATOMS * 64 * 128;    // 64-row tile bytes
+  static constexpr int A128 = 128 * 128;          // atom stride, 128-row tile
+  static constexpr int A64 = 64 * 128;            // atom stride, 64-row tile
+  static constexpr int W_BYTES = 128 * 128;       // one [128 rows x 64] bf16 tile (1 atom)
+};
+
+// =====================================================================================
+// dK, dV (+ keep bits)
+// =====================================================================================
+template <int HD, bool CAUSAL>
+__global__ void __launch_bounds__(320, 1)
+    fa_bwd_dkdv_umma(const __grid_constant__ CUtensorMap map_kv,  // qkv, 128-row boxes
+                     const __grid_constant__ CUtensorMap map_q,   // qkv, 64-row boxes
+                     const __grid_constant__ CUtensorMap map_do,  // dO, 64-row boxes
+                     AttnArgs a,
+                     bf16* __restrict__ dqkv, const float* __restrict__ delta) {
+  using C = BwdCfg<HD>;
+  // smem: K, V (128 rows) | 2 x (Q, dO) (64 rows) | 2 x (P̃ᵀ, dSᵀ) (128 x 64) | lse/delta | bars
+  constexpr int K_OFF = 0, V_OFF = C::T128, QD_OFF = 2 * C::T128;
+  constexpr int W_OFF = QD_OFF + 4 * C::T64;
+  constexpr int LD_OFF = W_OFF + 4 * C::W_BYTES;  // [2 stages][2][64] floats
+  constexpr int BAR_OFF = LD_OFF + 2 * 2 * 64 * 4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* qd_full = bar + 1;   // [2]
+  uint64_t* qd_empty = bar + 3;  // [2]
+  uint64_t* sd_full = bar + 5;   // [2] Sᵀ, dPᵀ ready in TMEM
+  uint64_t* sd_free = bar + 7;   // [2] read by the warps
+  uint64_t* w_full = bar + 9;    // [2] P̃ᵀ, dSᵀ written to smem
+  uint64_t* w_free = bar + 11;   // [2] consumed by the dV/dK MMAs
+  uint64_t* acc_full = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k0 = blockIdx.x * 128;
+  const int hl = blockIdx.y / (int)a.b, bj = blockIdx.y % (int)a.b;
+  const int S = (int)a.s;
+  const int q_start = CAUSAL ? (k0 / 64) * 64 : 0;
+  const int nq = (S - q_start + 63) / 64;
+  const int kcol = (int)(a.koff + (int64_t)hl * HD), vcol = (int)(a.voff + (int64_t)hl * HD),
+            qcol = (int)(a.qoff + (int64_t)hl * HD), dcol = hl * HD;
+  const int64_t brow = ((int64_t)hl * a.b + bj) * a.s;
+  // TMEM columns: Sᵀ [0,64) [64,128), dPᵀ [128,192) [192,256), dV [256,+HD), dK [384,+HD)
+  constexpr uint32_t DV_COL = 256, DK_COL = 384;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&qd_full[i], 1);
+      mbar_init(&qd_empty[i], 1);
+      mbar_init(&sd_full[i], 1);
+      mbar_init(&sd_free[i], 8);
+      mbar_init(&w_full[i], 8);
+      mbar_init(&w_free[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc_warp(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(kv_full, 2 * C::T128);
+#pragma unroll
+      for (int at = 0; at < C::ATOMS; ++at) {
+        tma_load_3d(smem + K_OFF + at * C::A128, &map_kv, kv_full, kcol + 64 * at, bj, k0);
+        tma_load_3d(smem + V_OFF + at * C::A128, &map_kv, kv_full, vcol + 64 * at, bj, k0);
+      }
+      for (int it = 0; it < nq; ++it) {
+        const int st = it & 1;
+        mbar_wait(&qd_empty[st], ((it >> 1) & 1) ^ 1);
+        uint8_t* Qt = smem + QD_OFF + st * 2 * C::T64;
+        uint8_t* Dt = Qt + C::T64;
+        const int qb = q_start + it * 64;
+        mbar_expect_tx(&qd_full[st], 2 * C::T64);
+#pragma unroll
+        for (int at = 0; at < C::ATOMS; ++at) {
+          tma_load_3d(Qt + at * C::A64, &map_q, &qd_full[st], qcol + 64 * at, bj, qb);
+          tma_load_3d(Dt + at * C::A64, &map_do, &qd_full[st], dcol + 64 * at, bj, qb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_sd = make_idesc(128, 64, false, false);
+      constexpr uint32_t idesc_acc = make_idesc(128, HD, false, true);
+      const uint32_t ka = smem_u32(smem + K_OFF), va = smem_u32(smem + V_OFF);
+      mbar_wait(kv_full, 0);
+      auto issue_sd = [&](int it) {
+        const int st = it & 1;
+        mbar_wait(&qd_full[st], (it >> 1) & 1);
+        mbar_wait(&sd_free[st], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t qb = smem_u32(smem + QD_OFF + st * 2 * C::T64), db = qb + C::T64;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * C::A128 + (kk & 3) * 32;
+          const uint32_t ob = (kk >> 2) * C::A64 + (kk & 3) * 32;
+          umma_bf16(tmem + st * 64, smem_desc(ka + oa, 16, 1024), smem_desc(qb + ob, 16, 1024),
+                    idesc_sd, kk > 0 ? 1u : 0u);
+          umma_bf16(tmem + 128 + st * 64, smem_desc(va + oa, 16, 1024),
+                    smem_desc(db + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&sd_full[st]);
+      };
+      if (nq > 0) issue_sd(0);
+      for (int it = 0; it < nq; ++it) {
+        if (it + 1 < nq) issue_sd(it + 1);
+        const int st = it & 1;
+        mbar_wait(&w_full[st], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t pw = smem_u32(smem + W_OFF + st * 2 * C::W_BYTES), dw = pw + C::W_BYTES;
+        const uint32_t qb = smem_u32(smem + QD_OFF + st * 2 * C::T64), db = qb + C::T64;
+#pragma unroll
+        for (int kk = 0; kk < 64 / 16; ++kk) {
+          // dV += P̃ᵀ·dO ; dK += dSᵀ·Q  (B = dO / Q tiles read MN-major)
+          umma_bf16(tmem + DV_COL, smem_desc(pw + kk * 32, 16, 1024),
+                    smem_desc(db + kk * 2048, C::A64, 1024), idesc_acc, (it | kk) != 0 ? 1u : 0u);
+          umma_bf16(tmem + DK_COL, smem_desc(dw + kk * 32, 16, 1024),
+                    smem_desc(qb + kk * 2048, C::A64, 1024), idesc_acc, (it | kk) != 0 ? 1u : 0u);
+        }
+        umma_commit(&w_free[st]);
+        umma_commit(&qd_empty[st]);
+      }
+      umma_commit(acc_full);
+    }
+  } else {
+    // ------------------------------------------------ softmax-backward warps
+    const int qd = warp & 3;
+    const int half = (warp - 2) >> 2;  // query columns 32*half .. +31 of each 64-query tile
+    const int row = qd * 32 + lane;    // key row
+    const int key = k0 + row;
+    const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16);
+    const float sl2 = a.scale * kLog2e;
+    const float inv_keep = a.drop.inv_keep;
+    const bool drop_on = a.drop.thresh != 0;
+    const int W = (S + 31) / 32;
+    const uint32_t* kbits = a.keepbits;
+    for (int it = 0; it < nq; ++it) {
+      const int st = it & 1;
+      const int qb = q_start + it * 64;
+      // lse (log2 domain), rowdot and the keep-bit word (q, this warp's 32 keys) of this half's
+      // 32 queries: lane e holds query q0h + e
+      float lse_l, dl_l;
+      uint32_t kw_l;
+      {
+        const int q = qb + 32 * half + lane;
+        lse_l = q < S ? a.lse[brow + q] * kLog2e : INFINITY;
+        dl_l = q < S ? delta[brow + q] : 0.f;
+        kw_l = !drop_on ? 0xffffffffu
+               : (q < S && (k0 >> 5) + qd < W) ? kbits[(brow + q) * W + (k0 >> 5) + qd] : 0u;
+      }
+      mbar_wait(&sd_full[st], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t rs[32], rp[32];
+      tmem_ld32_nw(tl + st * 64 + half * 32, rs);
+      tmem_ld32_nw(tl + 128 + st * 64 + half * 32, rp);
+      tmem_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sd_free[st]);
+      mbar_wait(&w_free[st], ((it >> 1) & 1) ^ 1);
+      const int q0h = qb + 32 * half;
+      uint32_t pw[16], dw[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        float pv[2], dv[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int e = i + u;
+          const int q = q0h + e;
+          const bool valid = q < S && key < S && !(CAUSAL && key > q);
+          bool keep = (__shfl_sync(0xffffffffu, kw_l, e) >> lane) & 1u;
+          const float lqe = __shfl_sync(0xffffffffu, lse_l, e);
+          const float dqe = __shfl_sync(0xffffffffu, dl_l, e);
+          const float p = valid ? ex2(__uint_as_float(rs[e]) * sl2 - lqe) : 0.f;
+          keep = keep && valid;
+          pv[u] = keep ? p * inv_keep : 0.f;
+          const float dpk = keep ? __uint_as_float(rp[e]) * inv_keep : 0.f;
+          dv[u] = p * (dpk - dqe);
+        }
+        pw[i >> 1] = pack_bf16(pv[0], pv[1]);
+        dw[i >> 1] = pack_bf16(dv[0], dv[1]);
+      }
+      // [128 keys x 64 queries] K-major SW128 tiles: this half's queries = chunks 4h..4h+3
+      uint8_t* prow = smem + W_OFF + st * 2 * C::W_BYTES + row * 128;
+      uint8_t* drow = prow + C::W_BYTES;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int phys = (4 * half + u) ^ (row & 7);
+        *reinterpret_cast<uint4*>(prow + phys * 16) =
+            make_uint4(pw[4 * u], pw[4 * u + 1], pw[4 * u + 2], pw[4 * u + 3]);
+        *reinterpret_cast<uint4*>(drow + phys * 16) =
+            make_uint4(dw[4 * u], dw[4 * u + 1], dw[4 * u + 2], dw[4 * u + 3]);
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&w_full[st]);
+    }
+    // epilogue: dK·scale, dV -> bf16 (halves take alternate 32-column chunks)
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    bf16* rowp = dqkv + ((int64_t)(key < S ? key : 0) * a.b + bj) * a.ld;
+#pragma unroll 1
+    for (int c = half; c < HD / 32; c += 2) {
+      float v[32], w[32];
+      tmem_ld32(tl + DK_COL + c * 32, v);
+      tmem_ld32(tl + DV_COL + c * 32, w);
+      if (key < S) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          *reinterpret_cast<uint4*>(rowp + kcol + c * 32 + i) = make_uint4(
+              pack_bf16(v[i] * a.scale, v[i + 1] * a.scale), pack_bf16(v[i + 2] * a.scale, v[i + 3] * a.scale),
+              pack_bf16(v[i + 4] * a.scale, v[i + 5] * a.scale), pack_bf16(v[i + 6] * a.scale, v[i + 7] * a.scale));
+          *reinterpret_cast<uint4*>(rowp + vcol + c * 32 + i) =
+              make_uint4(pack_bf16(w[i], w[i + 1]), pack_bf16(w[i + 2], w[i + 3]),
+                         pack_bf16(w[i + 4], w[i + 5]), pack_bf16(w[i + 6], w[i + 7]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_warp(tmem, 512);
+  }
+}
+
+// =====================================================================================
+// dQ
+// =====================================================================================
+template <int HD, bool CAUSAL>
+__global__ void __launch_bounds__(320, 1)
+    fa_bwd_dq_umma(const __grid_constant__ CUtensorMap map_q,   // qkv, 128-row boxes
+                   const __grid_constant__ CUtensorMap map_do,  // dO, 128-row boxes
+                   const __grid_constant__ CUtensorMap map_kv,  // qkv, 64-row boxes
+                   AttnArgs a,
+                   bf16* __restrict__ dqkv, const float* __restrict__ delta) {
+  using C = BwdCfg<HD>;
+  // smem: Q, dO (128 rows) | 2 x (K, V) (64 rows) | 2 x dS (128 x 64) | bars
+  constexpr int Q_OFF = 0, D_OFF = C::T128, KV_OFF = 2 * C::T128;
+  constexpr int W_OFF = KV_OFF + 4 * C::T64;
+  constexpr int BAR_OFF = W_OFF + 2 * C::W_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
+  uint64_t* q_full = bar + 0;
+  uint64_t* kv_full = bar + 1;   // [2]
+  uint64_t* kv_empty = bar + 3;  // [2]
+  uint64_t* sd_full = bar + 5;   // [2]
+  uint64_t* sd_free = bar + 7;   // [2]
+  uint64_t* w_full = bar + 9;    // [2]
+  uint64_t* w_free = bar + 11;   // [2]
+  uint64_t* acc_full = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q0 = blockIdx.x * 128;
+  const int hl = blockIdx.y / (int)a.b, bj = blockIdx.y % (int)a.b;
+  const int S = (int)a.s;
+  const int kv_end = CAUSAL ? min(S, q0 + 128) : S;
+  const int nkv = (kv_end + 63) / 64;
+  const int kcol = (int)(a.koff + (int64_t)hl * HD), vcol = (int)(a.voff + (int64_t)hl * HD),
+            qcol = (int)(a.qoff + (int64_t)hl * HD), dcol = hl * HD;
+  const int64_t brow = ((int64_t)hl * a.b + bj) * a.s;
+  constexpr uint32_t DQ_COL = 256;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&sd_full[i], 1);
+      mbar_init(&sd_free[i], 8);
+      mbar_init(&w_full[i], 8);
+      mbar_init(&w_free[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc_warp(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, 2 * C::T128);
+#pragma unroll
+      for (int at = 0; at < C::ATOMS; ++at) {
+        tma_load_3d(smem + Q_OFF + at * C::A128, &map_q, q_full, qcol + 64 * at, bj, q0);
+        tma_load_3d(smem + D_OFF + at * C::A128, &map_do, q_full, dcol + 64 * at, bj, q0);
+      }
+      for (int it = 0; it < nkv; ++it) {
+        const int st = it & 1;
+        mbar_wait(&kv_empty[st], ((it >> 1) & 1) ^ 1);
+        uint8_t* Kt = smem + KV_OFF + st * 2 * C::T64;
+        uint8_t* Vt = Kt + C::T64;
+        mbar_expect_tx(&kv_full[st], 2 * C::T64);
+#pragma unroll
+        for (int at = 0; at < C::ATOMS; ++at) {
+          tma_load_3d(Kt + at * C::A64, &map_kv, &kv_full[st], kcol + 64 * at, bj, it * 64);
+          tma_load_3d(Vt + at * C::A64, &map_kv, &kv_full[st], vcol + 64 * at, bj, it * 64);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_sd = make_idesc(128, 64, false, false);
+      constexpr uint32_t idesc_acc = make_idesc(128, HD, false, true);
+      const uint32_t qa = smem_u32(smem + Q_OFF), da = smem_u32(smem + D_OFF);
+      mbar_wait(q_full, 0);
+      auto issue_sd = [&](int it) {
+        const int st = it & 1;
+        mbar_wait(&kv_full[st], (it >> 1) & 1);
+        mbar_wait(&sd_free[st], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t kb = smem_u32(smem + KV_OFF + st * 2 * C::T64), vb = kb + C::T64;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * C::A128 + (kk & 3) * 32;
+          const uint32_t ob = (kk >> 2) * C::A64 + (kk & 3) * 32;
+          umma_bf16(tmem + st * 64, smem_desc(qa + oa, 16, 1024), smem_desc(kb + ob, 16, 1024),
+                    idesc_sd, kk > 0 ? 1u : 0u);
+          umma_bf16(tmem + 128 + st * 64, smem_desc(da + oa, 16, 1024),
+                    smem_desc(vb + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&sd_full[st]);
+      };
+      if (nkv > 0) issue_sd(0);
+      for (int it = 0; it < nkv; ++it) {
+        if (it + 1 < nkv) issue_sd(it + 1);
+        const int st = it & 1;
+        mbar_wait(&w_full[st], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t dsw = smem_u32(smem + W_OFF + st * C::W_BYTES);
+        const uint32_t kb = smem_u32(smem + KV_OFF + st * 2 * C::T64);
+#pragma unroll
+        for (int kk = 0; kk < 64 / 16; ++kk)
+          umma_bf16(tmem + DQ_COL, smem_desc(dsw + kk * 32, 16, 1024),
+                    smem_desc(kb + kk * 2048, C::A64, 1024), idesc_acc, (it | kk) != 0 ? 1u : 0u);
+        umma_commit(&w_free[st]);
+        umma_commit(&kv_empty[st]);
+      }
+      umma_commit(acc_full);
+    }
+  } else {
+    const int qd = warp & 3;
+    const int half = (warp - 2) >> 2;  // key columns 32*half .. +31 of each 64-key tile
+    const int row = qd * 32 + lane;    // query row
+    const int qr = q0 + row;
+    const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16);
+    const float sl2 = a.scale * kLog2e;
+    const float inv_keep = a.drop.inv_keep;
+    const bool drop_on = a.drop.thresh != 0;
+    const int W = (S + 31) / 32;
+    const float lse2 = qr < S ? a.lse[brow + qr] * kLog2e : INFINITY;
+    const float dl = qr < S ? delta[brow + qr] : 0.f;
+    const uint32_t* kb = a.keepbits + (brow + (qr < S ? qr : 0)) * W;
+    for (int it = 0; it < nkv; ++it) {
+      const int st = it & 1;
+      const int kc0 = it * 64 + 32 * half;
+      const uint32_t word = !drop_on ? 0xffffffffu : (qr < S && kc0 < S) ? kb[kc0 >> 5] : 0u;
+      mbar_wait(&sd_full[st], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t rs[32], rp[32];
+      tmem_ld32_nw(tl + st * 64 + half * 32, rs);
+      tmem_ld32_nw(tl + 128 + st * 64 + half * 32, rp);
+      tmem_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sd_free[st]);
+      mbar_wait(&w_free[st], ((it >> 1) & 1) ^ 1);
+      const bool full = kc0 + 32 <= S && !(CAUSAL && kc0 + 31 > q0) && q0 + 128 <= S;
+      uint32_t dw[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        float dv[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int e = i + u;
+          const bool keep = (word >> e) & 1u;
+          float p = ex2(__uint_as_float(rs[e]) * sl2 - lse2);
+          if (!full && (kc0 + e >= S || qr >= S || (CAUSAL && kc0 + e > qr))) p = 0.f;
+          const float dpk = keep ? __uint_as_float(rp[e]) * inv_keep : 0.f;
+          dv[u] = p * (dpk - dl);
+        }
+        dw[i >> 1] = pack_bf16(dv[0], dv[1]);
+      }
+      uint8_t* drow = smem + W_OFF + st * C::W_BYTES + row * 128;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int phys = (4 * half + u) ^ (row & 7);
+        *reinterpret_cast<uint4*>(drow + phys * 16) =
+            make_uint4(dw[4 * u], dw[4 * u + 1], dw[4 * u + 2], dw[4 * u + 3]);
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&w_full[st]);
+    }
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    bf16* out = dqkv + ((int64_t)(qr < S ? qr : 0) * a.b + bj) * a.ld + qcol;
+#pragma unroll 1
+    for (int c = half; c < HD / 32; c += 2) {
+      float v[32];
+      tmem_ld32(tl + DQ_COL + c * 32, v);
+      if (qr < S) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          *reinterpret_cast<uint4*>(out + c * 32 + i) = make_uint4(
+              pack_bf16(v[i] * a.scale, v[i + 1] * a.scale), pack_bf16(v[i + 2] * a.scale, v[i + 3] * a.scale),
+              pack_bf16(v[i + 4] * a.scale, v[i + 5] * a.scale), pack_bf16(v[i + 6] * a.scale, v[i + 7] * a.scale));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_warp(tmem, 512);
+  }
+}
+
+template <int HD, bool CAUSAL>
+void launch_bwd_umma(const AttnArgs& a, const bf16* dout, bf16* dqkv, const float* delta,
+                     cudaStream_t st) {
+  using C = BwdCfg<HD>;
+  constexpr int smem_kv = 2 * C::T128 + 4 * C::T64 + 4 * C::W_BYTES + 2 * 2 * 64 * 4 + 256 + 1024;
+  constexpr int smem_q = 2 * C::T128 + 4 * C::T64 + 2 * C::W_BYTES + 256 + 1024;
+  static bool once = [] {
+    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_dkdv_umma<HD, CAUSAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv));
+    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_dq_umma<HD, CAUSAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q));
+    return true;
+  }();
+  (void)once;
+  const CUtensorMap m128 = attn_seq_map(a.qkv, a.ld, a.b, a.s, a.ld, 128);
+  const CUtensorMap m64 = attn_seq_map(a.qkv, a.ld, a.b, a.s, a.ld, 64);
+  const CUtensorMap d64 = attn_seq_map(dout, a.ldo, a.b, a.s, a.ldo, 64);
+  const CUtensorMap d128 = attn_seq_map(dout, a.ldo, a.b, a.s, a.ldo, 128);
+  dim3 grid((unsigned)((a.s + 127) / 128), (unsigned)(a.lh * a.b));
+  // dK/dV: K,V 128-row boxes + Q 64-row boxes from the same map family
+  fa_bwd_dkdv_umma<HD, CAUSAL><<<grid, 320, smem_kv, st>>>(m128, m64, d64, a, dqkv, delta);
+  SPL_CHECK_LAUNCH();
+  fa_bwd_dq_umma<HD, CAUSAL><<<grid, 320, smem_q, st>>>(m128, d128, m64, a, dqkv, delta);
+  SPL_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+bool attn_bwd_umma_supported(const AttnArgs& a) {
+  const bool hd_ok = a.hd == 64 || a.hd == 96 || a.hd == 128;
+  return hd_ok && a.sm == nullptr && a.lse != nullptr && a.ld % 8 == 0 && a.ldo % 8 == 0 &&
+         ((uintptr_t)a.qkv & 15) == 0 && ((uintptr_t)a.o & 15) == 0 &&
+         (a.keepbits != nullptr || a.drop.thresh == 0) && a.s < (1 << 30);
+}
+
+void attn_bwd_umma(const AttnArgs& a, const void* dout, void* dqkv, const float* delta,
+                   cudaStream_t st) {
+  const bf16* d = static_cast<const bf16*>(dout);
+  bf16* g = static_cast<bf16*>(dqkv);
+  switch (a.hd) {
+    case 64: return a.causal ? launch_bwd_umma<64, true>(a, d, g, delta, st) : launch_bwd_umma<64, false>(a, d, g, delta, st);
+    case 96: return a.causal ? launch_bwd_umma<96, true>(a, d, g, delta, st) : launch_bwd_umma<96, false>(a, d, g, delta, st);
+    case 128: return a.causal ? launch_bwd_umma<128, true>(a, d, g, delta, st) : launch_bwd_umma<128, false>(a, d, g, delta, st);
+    default: raise(3, "attn_bwd_umma: unsupported head_dim");
+  }
+}
+
+}  // namespace spl::k

@@ -142,5 +142,13 @@ void attn_keep_bits(const AttnArgs& a, cudaStream_t st);
 // tcgen05/TMEM forward (selective regime, bf16, head_dim 64/96/128); used by attn_fwd<bf16>.
 bool attn_fwd_umma_supported(const AttnArgs& a);
 void attn_fwd_umma(const AttnArgs& a, cudaStream_t st);
+// tcgen05/TMEM backward (recompute regimes): the dK/dV kernel runs the counter RNG itself and
+// writes a.keepbits for the dQ kernel. delta = rowdot(dO, O) must be computed first.
+bool attn_bwd_umma_supported(const AttnArgs& a);
+void attn_bwd_umma(const AttnArgs& a, const void* dout, void* dqkv, const float* delta,
+                   cudaStream_t st);
+// True when attn_bwd<bf16> will take the tcgen05 path, which generates its own keep bits
+// (the caller then skips the attn_keep_bits pass before the backward).
+bool attn_bwd_self_rng(const AttnArgs& a);
 
 }  // namespace spl::k
