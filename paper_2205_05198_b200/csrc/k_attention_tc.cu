@@ -171,7 +171,7 @@ __device__ __forceinline__ bool keep_fast(uint32_t lo, uint32_t hi0, uint32_t hc
   (void)hi_xs;
   xs_fma(lo, hi, sm.m27);
   mul_c<0x133111ebu, 0x94d049bbu>(lo, hi);
-  xs_alu(lo, hi, 31);
+  xs_fma(lo, hi, sm.m31);
   // ^ mix64(key), + G (64-bit add as IMAD.WIDE with a 64-bit addend)
   lo ^= mixed_lo;
   hi ^= mixed_hi;

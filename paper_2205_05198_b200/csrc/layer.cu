@@ -63,6 +63,9 @@ class Layer final : public LayerBase {
     SPL_CUDA(cudaSetDevice(dev_));
     SPL_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     SPL_CUDA(cudaStreamCreateWithFlags(&st_rng_, cudaStreamNonBlocking));
+    SPL_CUDA(cudaStreamCreateWithFlags(&st_comm_, cudaStreamNonBlocking));
+    for (auto* e : {&ev_cfork_, &ev_regather_, &ev_rs_})
+      SPL_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     SPL_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     SPL_CUDA(cudaEventCreateWithFlags(&ev_bits_, cudaEventDisableTiming));
     SPL_CUDA(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming));
@@ -86,6 +89,9 @@ class Layer final : public LayerBase {
     cudaEventDestroy(ev_bits_);
     cudaStreamSynchronize(st_rng_);
     cudaStreamDestroy(st_rng_);
+    cudaStreamSynchronize(st_comm_);
+    cudaStreamDestroy(st_comm_);
+    for (auto e : {ev_cfork_, ev_regather_, ev_rs_}) cudaEventDestroy(e);
     cudaStreamDestroy(st_);
   }
 
@@ -573,9 +579,9 @@ class Layer final : public LayerBase {
         R.rs_out = alloc<T>(RL_ * h_, kWork, r);
       }
       R.part = alloc<T>(RF_ * h_, kWork, r);
-      if (!dgin) {
-        dgin = alloc<T>(RF_ * fw_, kWork, r);
-        dqkv = alloc<T>(RF_ * 3 * lw_, kWork, r);
+      dgin = alloc<T>(RF_ * fw_, kWork, r);
+      dqkv = alloc<T>(RF_ * 3 * lw_, kWork, r);
+      if (!dproj) {
         dproj = alloc<T>(RF_ * lw_, kWork, r);
         delta = alloc<float>(lh_ * b_ * s_, kWork, r);
         partials = alloc<float>(npart, kWork, r);
@@ -708,6 +714,47 @@ class Layer final : public LayerBase {
              [&] { comm_->all_reduce(p.data(), RF_ * h_, dt(), st_); });
     }
   }
+  // Collective on the comm stream after everything issued so far on the compute stream;
+  // returns the event the consumer waits on (nullptr when there is nothing to wait for).
+  cudaEvent_t gather_async(std::function<const void*(int)> shard, std::function<void*(int)> full,
+                           CommTag tag, cudaEvent_t done) {
+    if (!(sp_ && t_ > 1)) {
+      comm_->log(tag, 0, RF_ * h_);
+      return nullptr;
+    }
+    SPL_CUDA(cudaEventRecord(ev_cfork_, st_));
+    SPL_CUDA(cudaStreamWaitEvent(st_comm_, ev_cfork_, 0));
+    auto s = cptrs(shard);
+    auto f = mptrs(full);
+    comm_->log(tag, 0, RF_ * h_);
+    launch_on(st_comm_, K_COMM, 1, 0, (double)RF_ * h_ * sizeof(T) * (t_ - 1) / t_,
+              [&] { comm_->all_gather(s.data(), f.data(), RL_ * h_, dt(), st_comm_); });
+    SPL_CUDA(cudaEventRecord(done, st_comm_));
+    return done;
+  }
+  cudaEvent_t scatter_async(CommTag tag, cudaEvent_t done) {
+    if (t_ == 1) {
+      scatter(tag);
+      return nullptr;
+    }
+    SPL_CUDA(cudaEventRecord(ev_cfork_, st_));
+    SPL_CUDA(cudaStreamWaitEvent(st_comm_, ev_cfork_, 0));
+    cudaStream_t keep = st_;
+    st_ = st_comm_;  // scatter() launches on st_
+    try {
+      scatter(tag);
+    } catch (...) {
+      st_ = keep;
+      throw;
+    }
+    st_ = keep;
+    SPL_CUDA(cudaEventRecord(done, st_comm_));
+    return done;
+  }
+  void wait_on(cudaEvent_t e) {
+    if (e != nullptr) SPL_CUDA(cudaStreamWaitEvent(st_, e, 0));
+  }
+
   T* scattered(int r) { return (sp_ && t_ > 1) ? R_[r].rs_out : R_[r].part; }
   // the gathered {s,b,h} view of a sequence-sharded tensor (the shard itself when t == 1)
   const T* gathered(int r, const T* shard) const { return (sp_ && t_ > 1) ? R_[r].yfull : shard; }
@@ -820,16 +867,16 @@ class Layer final : public LayerBase {
         k::reduce_partials(R.partials, nch_l, h, R.repl + 1 * h, false, st_);  // b2 partial
       });
     }
-    if (sp_) {
+    if (sp_)
       gather([&](int r) { return (const void*)R_[r].d_s; }, [&](int r) { return (void*)R_[r].dfull; },
              kSchedule);  // block.cpp:653
-      gather([&](int r) { return (const void*)R_[r].y2; }, [&](int r) { return (void*)R_[r].yfull; },
-             kRegather);  // block.cpp:655
-    }
+    // re-gather Y2 (block.cpp:655) on the comm stream, overlapped with the FC2 GEMMs
+    cudaEvent_t y2_ready = gather_async([&](int r) { return (const void*)R_[r].y2; },
+                                        [&](int r) { return (void*)R_[r].yfull; }, kRegather,
+                                        ev_regather_);
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
       const T* dmo = gathered_d(r, R.d_s);
-      const T* y2 = gathered(r, R.y2);
       // FC2 dgrad fused with GELU backward (block.cpp:660, 662)
       gemm(RF_, fw_, h, dmo, h, Major::K, R.w2, h, Major::K, R.dgin, fw_, Epi::GeluBwd, nullptr,
            nullptr, R.gin, fw_);
@@ -840,11 +887,16 @@ class Layer final : public LayerBase {
         k::colsum_partial<T>(R.dgin, RF_, fw_, fw_, R.partials, kChunkRows, st_);
         k::reduce_partials(R.partials, nch_f, fw_, R.db1, false, st_);
       });
-      // FC1 wgrad on the re-gathered Y2 (block.cpp:664) and dgrad (665)
-      gemm(h, fw_, RF_, y2, h, Major::MN, R.dgin, fw_, Major::MN, R.dw1, fw_, Epi::F32);
+      // FC1 dgrad (block.cpp:665) first, so its reduce-scatter overlaps the FC1 wgrad
       gemm(RF_, h, fw_, R.dgin, fw_, Major::K, R.w1, fw_, Major::K, R.part, h, Epi::Store);
     }
-    scatter(kSchedule);  // g-dual: block.cpp:668-669
+    cudaEvent_t rs_done = scatter_async(kSchedule, ev_rs_);  // g-dual: block.cpp:668-669
+    wait_on(y2_ready);
+    for (int r = 0; r < L_; ++r) {  // FC1 wgrad on the re-gathered Y2 (block.cpp:664)
+      Rank& R = R_[r];
+      gemm(h, fw_, RF_, gathered(r, R.y2), h, Major::MN, R.dgin, fw_, Major::MN, R.dw1, fw_, Epi::F32);
+    }
+    wait_on(rs_done);
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
       const T* dy = static_cast<const T*>(dyv[r]);
@@ -865,16 +917,16 @@ class Layer final : public LayerBase {
         k::reduce_partials(R.partials, nch_l, h, R.repl + 0 * h, false, st_);  // bo partial
       });
     }
-    if (sp_) {
+    if (sp_)
       gather([&](int r) { return (const void*)R_[r].d_s; }, [&](int r) { return (void*)R_[r].dfull; },
              kSchedule);  // block.cpp:691
-      gather([&](int r) { return (const void*)R_[r].y1_s; }, [&](int r) { return (void*)R_[r].yfull; },
-             kRegather);  // block.cpp:692
-    }
+    // re-gather Y1 (block.cpp:692) on the comm stream, overlapped with proj and attention bwd
+    cudaEvent_t y1_ready = gather_async([&](int r) { return (const void*)R_[r].y1_s; },
+                                        [&](int r) { return (void*)R_[r].yfull; }, kRegather,
+                                        ev_regather_);
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
       const T* dao = gathered_d(r, R.d_s);
-      const T* y1 = gathered(r, R.y1_s);
       gemm(RF_, lw_, h, dao, h, Major::K, R.wo, h, Major::K, R.dproj, lw_, Epi::Store);  // 699
       gemm(lw_, h, RF_, R.api, lw_, Major::MN, dao, h, Major::MN, R.dwo, h, Epi::F32);    // 700
       k::AttnArgs a = attn_args(r);
@@ -885,13 +937,18 @@ class Layer final : public LayerBase {
         k::colsum_partial<T>(R.dqkv, RF_, 3 * lw_, 3 * lw_, R.partials, kChunkRows, st_);
         k::reduce_partials(R.partials, nch_f, 3 * lw_, R.dbqkv, false, st_);  // 703-705
       });
-      gemm(h, 3 * lw_, RF_, y1, h, Major::MN, R.dqkv, 3 * lw_, Major::MN, R.dwqkv, 3 * lw_,
-           Epi::F32);  // 706-708
       // dY1 = dQ·Wqᵀ + dK·Wkᵀ + dV·Wvᵀ as one GEMM over the fused 3h/t weight (709-711)
       gemm(RF_, h, 3 * lw_, R.dqkv, 3 * lw_, Major::K, R.wqkv, 3 * lw_, Major::K, R.part, h,
            Epi::Store);
     }
-    scatter(kSchedule);  // block.cpp:714-715
+    rs_done = scatter_async(kSchedule, ev_rs_);  // block.cpp:714-715, overlaps the QKV wgrad
+    wait_on(y1_ready);
+    for (int r = 0; r < L_; ++r) {  // QKV wgrad on the re-gathered Y1 (block.cpp:706-708)
+      Rank& R = R_[r];
+      gemm(h, 3 * lw_, RF_, gathered(r, R.y1_s), h, Major::MN, R.dqkv, 3 * lw_, Major::MN,
+           R.dwqkv, 3 * lw_, Epi::F32);
+    }
+    wait_on(rs_done);
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
       launch(K_ELEM, 2, 0, 5.0 * eb * RL_ * h, [&] {
@@ -926,6 +983,8 @@ class Layer final : public LayerBase {
   cudaStream_t st_ = nullptr;
   cudaEvent_t ev_in_ = nullptr, ev_out_ = nullptr, ev_fork_ = nullptr, ev_bits_ = nullptr;
   cudaStream_t st_rng_ = nullptr;  // side stream: data-independent dropout keep bits
+  cudaStream_t st_comm_ = nullptr;  // backward collectives overlapped with the GEMMs
+  cudaEvent_t ev_cfork_ = nullptr, ev_regather_ = nullptr, ev_rs_ = nullptr;
   cudaStream_t caller_ = 0;  // legacy default stream unless set
   std::vector<Rank> R_;
   std::vector<Alloc> allocs_;
