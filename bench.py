@@ -186,6 +186,7 @@ def main():
     ap.add_argument("--no-sp", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -211,6 +212,7 @@ def main():
     L = spl.SeqparLayer(cfg, t, args.recompute, sp, "bf16", device=local_rank,
                         check_finite=False, nccl=nccl)
     L.init_params(1234)
+    L.set_graphs(not args.no_graphs)  # forward / backward replayed as CUDA graphs
     shp = L.shard_shape()
     gen = torch.Generator(device=f"cuda:{local_rank}").manual_seed(100 + rank)
     x = [(torch.rand(shp, generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)]

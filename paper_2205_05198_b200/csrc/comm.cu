@@ -76,6 +76,12 @@ class LocalComm final : public Comm {
   void all_reduce_f32(float* const* buf, int64_t n, cudaStream_t st) override {
     all_reduce(reinterpret_cast<void* const*>(buf), n, DType::F32, st);
   }
+  void reserve(size_t bytes) override {
+    if (bytes <= scratch_bytes_) return;
+    if (scratch_) SPL_CUDA(cudaFree(scratch_));
+    SPL_CUDA(cudaMalloc(&scratch_, bytes));
+    scratch_bytes_ = bytes;
+  }
   ~LocalComm() override {
     if (scratch_) cudaFree(scratch_);
   }

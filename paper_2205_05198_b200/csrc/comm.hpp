@@ -37,6 +37,9 @@ class Comm {
   // buf[r] (n) = sum_q buf[q], in place.
   virtual void all_reduce(void* const* buf, int64_t n, DType dt, cudaStream_t st) = 0;
   virtual void all_reduce_f32(float* const* buf, int64_t n, cudaStream_t st) = 0;
+  // Pre-allocate any scratch a collective of up to `bytes` may need (so that no allocation
+  // happens while a CUDA graph is being captured).
+  virtual void reserve(size_t bytes) { (void)bytes; }
 
   void log(CommTag tag, int kind, int64_t logical_elems) {
     CommCounters& c = counters[tag];

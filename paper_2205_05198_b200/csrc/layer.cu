@@ -35,6 +35,13 @@ struct Alloc {
   int rank;
 };
 
+struct Graph {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<const void*> in;
+  std::vector<void*> out;
+  int64_t launches = 0;
+};
+
 template <typename T>
 class Layer final : public LayerBase {
  public:
@@ -71,6 +78,7 @@ class Layer final : public LayerBase {
     SPL_CUDA(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming));
     SPL_CUDA(cudaEventCreateWithFlags(&ev_out_, cudaEventDisableTiming));
     allocate();
+    comm_->reserve(std::max<size_t>((size_t)(RF_ * h_) * sizeof(T), (size_t)(6 * h_) * sizeof(float)));
     // The keep-bit RNG pass runs on the main stream by default: overlapping it with the GEMMs
     // on a side stream measured no faster (the GEMMs already hold the chip at its power cap).
     const char* e = std::getenv("SPL_KEEPBITS_SIDE");
@@ -80,6 +88,8 @@ class Layer final : public LayerBase {
   ~Layer() override {
     cudaSetDevice(dev_);
     cudaStreamSynchronize(st_);
+    for (Graph* g : {&gfwd_, &gbwd_})
+      if (g->exec) cudaGraphExecDestroy(g->exec);
     for (auto& a : allocs_) cudaFree(a.ptr);
     if (pinned_) cudaFreeHost(pinned_);
     for (auto& e : evpool_) cudaEventDestroy(e);
@@ -97,6 +107,42 @@ class Layer final : public LayerBase {
 
   int local_ranks() const override { return L_; }
   void set_caller_stream(cudaStream_t s) override { caller_ = s; }
+
+  // Run `body` (which issues work on st_, possibly forking to the side streams and joining
+  // back) either eagerly or as a CUDA graph captured on the first call with these pointers.
+  template <typename F>
+  void run_graphed(Graph& g, const std::vector<const void*>& in, const std::vector<void*>& out,
+                   F&& body) {
+    const bool use = graphs_ && !profiling_ && !d_.check_finite;
+    if (!use) {
+      body();
+      return;
+    }
+    if (g.exec == nullptr || g.in != in || g.out != out) {
+      if (g.exec) {
+        SPL_CUDA(cudaGraphExecDestroy(g.exec));
+        g.exec = nullptr;
+      }
+      const int64_t l0 = launches_;
+      cudaGraph_t graph;
+      SPL_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+      try {
+        body();
+      } catch (...) {
+        cudaStreamEndCapture(st_, &graph);
+        throw;
+      }
+      SPL_CUDA(cudaStreamEndCapture(st_, &graph));
+      SPL_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+      SPL_CUDA(cudaGraphDestroy(graph));
+      g.in = in;
+      g.out = out;
+      g.launches = launches_ - l0;
+      launches_ = l0;
+    }
+    SPL_CUDA(cudaGraphLaunch(g.exec, st_));
+    launches_ += g.launches;
+  }
 
   // fork: our stream waits for the caller's prior work; join: the caller waits for ours.
   void enter() {
@@ -199,15 +245,17 @@ class Layer final : public LayerBase {
   // ------------------------------------------------------------------ forward
   void forward(const void* const* x, void* const* y) override {
     enter();
-    for (int r = 0; r < L_; ++r) {
+    for (int r = 0; r < L_; ++r)
       require(x[r] != nullptr && y[r] != nullptr, "expected one input shard per rank");
-      SPL_CUDA(cudaMemcpyAsync(R_[r].x_s, x[r], (size_t)(RL_ * h_) * sizeof(T),
-                               cudaMemcpyDeviceToDevice, st_));
-    }
-    if (d_.check_finite) SPL_CUDA(cudaMemsetAsync(nonfinite_, 0, sizeof(int), st_));
     std::vector<T*> ys(L_);
     for (int r = 0; r < L_; ++r) ys[r] = static_cast<T*>(y[r]);
-    run_forward(ys.data(), kSchedule, d_.check_finite ? nonfinite_ : nullptr);
+    run_graphed(gfwd_, std::vector<const void*>(x, x + L_), std::vector<void*>(y, y + L_), [&] {
+      for (int r = 0; r < L_; ++r)
+        SPL_CUDA(cudaMemcpyAsync(R_[r].x_s, x[r], (size_t)(RL_ * h_) * sizeof(T),
+                                 cudaMemcpyDeviceToDevice, st_));
+      if (d_.check_finite) SPL_CUDA(cudaMemsetAsync(nonfinite_, 0, sizeof(int), st_));
+      run_forward(ys.data(), kSchedule, d_.check_finite ? nonfinite_ : nullptr);
+    });
     if (d_.check_finite) {
       int flag = 0;
       SPL_CUDA(cudaMemcpyAsync(&flag, nonfinite_, sizeof(int), cudaMemcpyDeviceToHost, st_));
@@ -225,13 +273,15 @@ class Layer final : public LayerBase {
     enter();
     if (!have_fwd_) raise(5, "missing saved forward state");
     for (int r = 0; r < L_; ++r) require(dy[r] != nullptr && dx[r] != nullptr, "expected one gradient shard per rank");
-    if (kind_ == SPL_RECOMPUTE_FULL) {
-      // Full recomputation: only x_s survived; re-run the forward (with its collectives).
-      std::vector<T*> ys(L_);
-      for (int r = 0; r < L_; ++r) ys[r] = R_[r].y_re;
-      run_forward(ys.data(), kRecompute, nullptr);
-    }
-    run_backward(dy, dx);
+    run_graphed(gbwd_, std::vector<const void*>(dy, dy + L_), std::vector<void*>(dx, dx + L_), [&] {
+      if (kind_ == SPL_RECOMPUTE_FULL) {
+        // Full recomputation: only x_s survived; re-run the forward (with its collectives).
+        std::vector<T*> ys(L_);
+        for (int r = 0; r < L_; ++r) ys[r] = R_[r].y_re;
+        run_forward(ys.data(), kRecompute, nullptr);
+      }
+      run_backward(dy, dx);
+    });
     leave();
   }
 
@@ -463,7 +513,15 @@ class Layer final : public LayerBase {
     if (reset) launches_ = 0;
     return v;
   }
-  void set_graphs(bool on) override { graphs_ = on; }
+  void set_graphs(bool on) override {
+    graphs_ = on;
+    if (!on)
+      for (Graph* g : {&gfwd_, &gbwd_})
+        if (g->exec) {
+          SPL_CUDA(cudaGraphExecDestroy(g->exec));
+          g->exec = nullptr;
+        }
+  }
 
  private:
   struct Rank {
@@ -995,6 +1053,7 @@ class Layer final : public LayerBase {
   bool bits_pending_ = false;
   bool bits_serial_ = true;  // SPL_KEEPBITS_SIDE=1: RNG pass on the side stream
   bool graphs_ = false;
+  Graph gfwd_, gbwd_;
   // profiling
   struct Pending {
     cudaEvent_t a, b;
