@@ -113,6 +113,23 @@ def max_over_ranks(value, device="cuda"):
     return float(t.item())
 
 
+def gemm_traffic_from_profile(cfg_name):
+    """DRAM bytes per GEMM launch (read + write), averaged over the tcgen05 GEMM launches of
+    one step, from the committed ncu capture (profiles/r01_ncu_dram_<cfg>_t1_selective.json;
+    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum). None when absent."""
+    path = os.path.join(ROOT, "profiles", f"r01_ncu_dram_{cfg_name}_t1_selective.json")
+    try:
+        prof = json.load(open(path))
+    except Exception:
+        return None
+    n = b = 0.0
+    for k, v in prof.items():
+        if k.startswith("gemm_tc_kernel"):
+            n += v["launches"]
+            b += v["launches"] * (v["dram_read_bytes_per_launch"] + v["dram_write_bytes_per_launch"])
+    return b / n if n else None
+
+
 def cpu_baseline_sample(cfg_name, threads=0):
     """The oracle (fp64 restatement of the reference seqpar layer, test infrastructure) timed
     on the host cores on a bounded sample of the workload: the same layer width (h, a) with
@@ -307,7 +324,10 @@ def main():
                                      "per_layer_bytes": spl.per_layer_bytes(a, h, s, b, t, args.recompute, sp)},
         "roofline": {"kernel": "tcgen05 GEMM (all layer GEMMs)", "bound": "tensor",
                      "achieved": gemm_tflops, "peak": peak, "unit": "TFLOP/s",
-                     "frac": gemm_tflops / peak if peak else None, "traffic": None,
+                     "frac": gemm_tflops / peak if peak else None,
+                     "traffic": gemm_traffic_from_profile(args.config) if t == 1 else None,
+                     "traffic_unit": "DRAM bytes per GEMM launch (ncu, profiles/)",
+                     "algorithmic_bytes_per_launch": g["bytes"] / max(g["launches"], 1),
                      "peak_kind": f"{pk_kind} bf16_tflops_sustained",
                      "share_of_step": g["ms"] / total_prof_ms if total_prof_ms else None},
         "kernel_classes": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
