@@ -219,7 +219,8 @@ def main():
     torch.cuda.set_device(local_rank)
     dist = None
     nccl = None
-    if world > 1:
+    if "WORLD_SIZE" in os.environ and "MASTER_ADDR" in os.environ:
+        # launched by torchrun (any N, including 1): one NCCL rank per GPU
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
         nccl = (rank, share_unique_id(spl.SeqparLayer.nccl_unique_id, rank))
