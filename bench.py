@@ -329,7 +329,9 @@ def main():
                      "traffic": gemm_traffic_from_profile(args.config) if t == 1 else None,
                      "traffic_unit": "DRAM bytes per GEMM launch (ncu, profiles/)",
                      "algorithmic_bytes_per_launch": g["bytes"] / max(g["launches"], 1),
-                     "peak_kind": f"{pk_kind} bf16_tflops_sustained",
+                     "peak_kind": f"{pk_kind} bf16_tflops_sustained (cuBLAS 8192^3 back to back; "
+                                  f"MEASURED_PEAKS records its clock median under load)",
+                     "frac_of_burst_peak": gemm_tflops / pk["bf16_tflops"] if pk.get("bf16_tflops") else None,
                      "share_of_step": g["ms"] / total_prof_ms if total_prof_ms else None},
         "kernel_classes": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
                                "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] and v["flops"] else None,

