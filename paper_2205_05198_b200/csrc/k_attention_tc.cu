@@ -15,6 +15,7 @@
 #include <type_traits>
 
 #include "kernels.hpp"
+#include "rng_fast.cuh"
 
 namespace spl::k {
 
@@ -74,26 +75,8 @@ __device__ __forceinline__ void load_tile(bf16* sm, const bf16* base, int64_t r0
   }
 }
 
-// ---------------------------------------------------------------- counter RNG, hot-loop form
-// keep(i) = (hash_counter(folded, i) >> 11) >= ceil(p*2^53)  (rng.cpp:31-37, block.cpp:63)
-//   hash_counter(k, i) = mix64(mix64(k) ^ mix64(i + C)),  mix64(x) = post(x + G)
-// With base = row_index*s + C + G precomputed per row, one element costs
-//   post(base + key) ^ mixed, + G, post, 64-bit compare against thresh << 11.
-constexpr uint64_t kG = 0x9e3779b97f4a7c15ULL;
-constexpr uint64_t kC = 0x632be59bd9b4e019ULL;
-// x * C mod 2^64 in three 32-bit multiplies (IMAD.WIDE + 2 IMAD)
-template <uint64_t C>
-__device__ __forceinline__ uint64_t mulc(uint64_t x) {
-  const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
-  const uint64_t w = (uint64_t)xl * (uint32_t)C;
-  const uint32_t hi = (uint32_t)(w >> 32) + xl * (uint32_t)(C >> 32) + xh * (uint32_t)C;
-  return ((uint64_t)hi << 32) | (uint32_t)w;
-}
-__device__ __forceinline__ uint64_t mix_post(uint64_t x) {
-  x = mulc<0xbf58476d1ce4e5b9ULL>(x ^ (x >> 30));
-  x = mulc<0x94d049bb133111ebULL>(x ^ (x >> 27));
-  return x ^ (x >> 31);
-}
+using namespace spl::rngk;  // kG, kC, mix_post, keep_fast (rng_fast.cuh)
+
 // 2^x, one MUFU.EX2 (flush-to-zero; the softmax operands are <= 0)
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -114,14 +97,6 @@ struct Rng {
   }
 };
 
-// 8 bits at positions 0,4,...,28 of x -> bits 0..7
-__device__ __forceinline__ uint32_t compress4(uint32_t x) {
-  x &= 0x11111111u;
-  x = (x | (x >> 3)) & 0x03030303u;
-  x = (x | (x >> 6)) & 0x000F000Fu;
-  return (x | (x >> 12)) & 0xFFu;
-}
-
 // =====================================================================================
 // softmax-dropout keep bits: bits[(hl*b + bj)*s + q][w] bit j = keep(q, 32w + j)
 // The mask depends only on (seed, layer, op, microbatch) and the global {a,b,s,s} index, not
@@ -137,56 +112,6 @@ __device__ __forceinline__ uint32_t compress4(uint32_t x) {
 // shifts leave the ALU pipe the bound; shifting three of them to IMAD saturates fmaheavy (90%)
 // instead; two in IMAD form is the balance point. The multipliers come in through the kernel
 // parameters so ptxas cannot turn the multiplies back into shifts.
-struct ShiftMuls {
-  uint32_t m30, m27, m31;  // 2^(32-k)
-  uint32_t one;            // 1: the 64-bit "+ G" as IMAD.WIDE (FMA pipe) instead of IADD3 pairs
-};
-template <uint32_t CL, uint32_t CH>
-__device__ __forceinline__ void mul_c(uint32_t& lo, uint32_t& hi) {  // (hi:lo) *= (CH:CL)
-  const uint64_t w = (uint64_t)lo * CL;
-  hi = (uint32_t)(w >> 32) + lo * CH + hi * CL;
-  lo = (uint32_t)w;
-}
-__device__ __forceinline__ void xs_alu(uint32_t& lo, uint32_t& hi, int k) {  // x ^= x >> k
-  lo ^= __funnelshift_r(lo, hi, k);
-  hi ^= hi >> k;
-}
-__device__ __forceinline__ void xs_fma(uint32_t& lo, uint32_t& hi, uint32_t m) {  // m = 2^(32-k)
-  const uint32_t a = __umulhi(lo, m), b = hi * m, c = __umulhi(hi, m);
-  lo = lo ^ a ^ b;
-  hi ^= c;
-}
-__device__ __forceinline__ bool keep_fast(uint32_t lo, uint32_t hi0, uint32_t hc,
-                                          uint32_t hi_xs, uint32_t mixed_lo, uint32_t mixed_hi,
-                                          uint32_t t_lo, uint32_t t_hi, const ShiftMuls& sm) {
-  // first mix_post; the high half (hi0) is loop-invariant: hi_xs = hi0 ^ (hi0 >> 30) and
-  // hc = hi_xs * 0x1ce4e5b9 are precomputed per 32-key word.
-  lo ^= __funnelshift_r(lo, hi0, 30);
-  uint32_t hi;
-  {
-    const uint64_t w = (uint64_t)lo * 0x1ce4e5b9u + ((uint64_t)hc << 32);
-    hi = (uint32_t)(w >> 32) + lo * 0xbf58476du;
-    lo = (uint32_t)w;
-  }
-  (void)hi_xs;
-  xs_fma(lo, hi, sm.m27);
-  mul_c<0x133111ebu, 0x94d049bbu>(lo, hi);
-  xs_fma(lo, hi, sm.m31);
-  // ^ mix64(key), + G (64-bit add as IMAD.WIDE with a 64-bit addend)
-  lo ^= mixed_lo;
-  hi ^= mixed_hi;
-  {
-    const uint64_t w = ((uint64_t)hi << 32 | lo) + 0x9e3779b97f4a7c15ULL;
-    hi = (uint32_t)(w >> 32);
-    lo = (uint32_t)w;
-  }
-  xs_alu(lo, hi, 30);
-  mul_c<0x1ce4e5b9u, 0xbf58476du>(lo, hi);
-  xs_fma(lo, hi, sm.m27);
-  mul_c<0x133111ebu, 0x94d049bbu>(lo, hi);
-  xs_alu(lo, hi, 31);
-  return (((uint64_t)hi << 32) | lo) >= (((uint64_t)t_hi << 32) | t_lo);
-}
 
 __global__ void __launch_bounds__(256) keep_bits_k(DropKey key, int64_t head_offset, int lh,
                                                    int b, int s, int W, int causal,
@@ -468,21 +393,38 @@ __global__ void __launch_bounds__(128) fa_fwd(AttnArgs a) {
 // =====================================================================================
 template <int HD>
 __global__ void fa_delta(AttnArgs a, const bf16* __restrict__ dout, float* __restrict__ delta) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t r = (int64_t)blockIdx.x * 4 + warp;  // ((hl*b)+bj)*s + i
-  if (r >= a.lh * a.b * a.s) return;
-  const int64_t i = r % a.s, t = r / a.s, bj = t % a.b, hl = t / a.b;
-  const int64_t off = (i * a.b + bj) * a.ldo + hl * HD;
+  // rowdot_i = dO_i·O_i of every (head, batch, query) row. Rows are visited in memory order
+  // (token-major, heads of one token contiguous), 4 lanes per row with interleaved 16-byte
+  // vectors, so a warp streams 8 consecutive rows = one contiguous span of dO and of O.
+  static_assert(HD % 32 == 0, "fa_delta: head_dim must be a multiple of 32");
+  constexpr int VPL = HD / 32;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = t >> 2;
+  const int sub = (int)(t & 3);
+  const int64_t nrows = a.lh * a.b * a.s;
+  const int64_t hl = r % a.lh, tok = r / a.lh;  // tok = i*b + bj
   const bf16* o = static_cast<const bf16*>(a.o);
   float acc = 0.f;
-  for (int d = lane * 2; d < HD; d += 64) {
-    const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(dout + off + d);
-    const __nv_bfloat162 y = *reinterpret_cast<const __nv_bfloat162*>(o + off + d);
-    acc += __bfloat162float(x.x) * __bfloat162float(y.x) + __bfloat162float(x.y) * __bfloat162float(y.y);
-  }
+  if (r < nrows) {
+    const int64_t off = tok * a.ldo + hl * HD;
 #pragma unroll
-  for (int k = 16; k; k >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, k);
-  if (lane == 0) delta[r] = acc;
+    for (int v = 0; v < VPL; ++v) {
+      const int c = (sub + 4 * v) * 8;
+      const uint4 x = *reinterpret_cast<const uint4*>(dout + off + c);
+      const uint4 y = *reinterpret_cast<const uint4*>(o + off + c);
+      const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        acc += __uint_as_float(xs[k] << 16) * __uint_as_float(ys[k] << 16) +
+               __uint_as_float(xs[k] & 0xffff0000u) * __uint_as_float(ys[k] & 0xffff0000u);
+    }
+  }
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  if (sub == 0 && r < nrows) {
+    const int64_t bj = tok % a.b, i = tok / a.b;
+    delta[(hl * a.b + bj) * a.s + i] = acc;
+  }
 }
 
 // =====================================================================================
@@ -819,7 +761,7 @@ template <int HD, bool CAUSAL, bool STORED>
 void launch_bwd_t(const AttnArgs& a, const bf16* dout, bf16* dqkv, float* delta, cudaStream_t st) {
   constexpr int LDS = HD + 8;
   const int64_t rows = a.lh * a.b * a.s;
-  fa_delta<HD><<<(unsigned)((rows + 3) / 4), 128, 0, st>>>(a, dout, delta);
+  fa_delta<HD><<<(unsigned)((rows * 4 + 255) / 256), 256, 0, st>>>(a, dout, delta);
   SPL_CHECK_LAUNCH();
   const int smem_kv = (2 * 64 * LDS + 4 * 32 * LDS) * 2 + 4 * 32 * 4;
   const int smem_q = (2 * 64 * LDS + 4 * 32 * LDS) * 2;
@@ -903,7 +845,7 @@ void attn_bwd_tc<bf16>(const AttnArgs& a, const void* dout, void* dqkv, float* d
   const bool stored = a.sm != nullptr;
   if (!stored && umma_bwd_on(a)) {
     const int64_t rows = a.lh * a.b * a.s;
-    SPL_HD_SWITCH(a.hd, fa_delta<HD><<<(unsigned)((rows + 3) / 4), 128, 0, st>>>(
+    SPL_HD_SWITCH(a.hd, fa_delta<HD><<<(unsigned)((rows * 4 + 255) / 256), 256, 0, st>>>(
                             a, static_cast<const bf16*>(dout), delta));
     SPL_CHECK_LAUNCH();
     attn_bwd_umma(a, dout, dqkv, delta, st);

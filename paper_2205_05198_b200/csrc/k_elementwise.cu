@@ -8,6 +8,7 @@
 #include <type_traits>
 
 #include "kernels.hpp"
+#include "rng_fast.cuh"
 
 namespace spl::k {
 
@@ -109,6 +110,15 @@ constexpr int kVPT = 8;  // vectors per thread for row-cached kernels
 template <typename T>
 constexpr int vec_width() {
   return 16 / sizeof(T);
+}
+
+// vectors per thread of the register-cached row kernels (0: too wide, generic kernel)
+inline int pick_vpt(int64_t nvec) { return nvec <= 2048 ? 4 : (nvec <= 4096 ? 8 : 0); }
+// threads for a register-cached row kernel: ceil(nvec / vpt) rounded up to whole warps
+inline int vthreads(int64_t nvec, int vpt) {
+  int64_t nt = (nvec + vpt - 1) / vpt;
+  nt = ((nt + 31) / 32) * 32;
+  return (int)std::max<int64_t>(32, nt);
 }
 
 inline int row_threads(int64_t nvec) {
@@ -249,6 +259,312 @@ __global__ void __launch_bounds__(512) bdr_k(const T* __restrict__ a, const floa
   }
 }
 
+// ================================================================ register-cached row kernels
+// One CTA per row; thread i owns the 16-byte vectors i, i+nt, ... (VPT of them, coalesced
+// across the CTA) and keeps them *packed* in registers (4 regs per 8 bf16), so a row is read
+// from HBM exactly once and the CTA stays small enough (≈40-64 regs) for full occupancy:
+// nt = nvec/VPT threads <= 512: VPT = 4 up to 2048 vectors (192 threads at h = 6144),
+// VPT = 8 up to 4096 (400 threads at h = 25600); wider rows take the generic kernels.
+template <typename T>
+constexpr int kVW = 16 / (int)sizeof(T);
+
+template <typename T>
+__device__ __forceinline__ void unpack(const uint4& r, float (&v)[kVW<T>]) {
+  if constexpr (std::is_same_v<T, float>) {
+    v[0] = __uint_as_float(r.x); v[1] = __uint_as_float(r.y);
+    v[2] = __uint_as_float(r.z); v[3] = __uint_as_float(r.w);
+  } else {
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+}
+template <typename T>
+__device__ __forceinline__ uint4 pack(const float (&v)[kVW<T>]) {
+  if constexpr (std::is_same_v<T, float>) {
+    return make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]),
+                      __float_as_uint(v[3]));
+  } else {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+__device__ __forceinline__ uint4 ld16(const void* p) {  // read-once data: no L1 allocation
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st16(void* p, const uint4& v) {
+  *reinterpret_cast<uint4*>(p) = v;
+}
+// fp32 per-column parameters (gain / bias): VW of them at column c (16-byte aligned)
+template <int VW>
+__device__ __forceinline__ void ldcols(const float* __restrict__ p, int c, float (&v)[VW]) {
+#pragma unroll
+  for (int i = 0; i < VW; i += 4) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p + c + i));
+    v[i] = t.x; v[i + 1] = t.y; v[i + 2] = t.z; v[i + 3] = t.w;
+  }
+}
+// Both sums over the CTA in one pass (one pair of barriers); `red` holds >= 64 floats.
+__device__ __forceinline__ float2 block_sum2(float a, float b, float* red) {
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int nw = blockDim.x >> 5;
+  if (nw == 1) return make_float2(a, b);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) {
+    red[w] = a;
+    red[32 + w] = b;
+  }
+  __syncthreads();
+  a = l < nw ? red[l] : 0.f;
+  b = l < nw ? red[32 + l] : 0.f;
+  return make_float2(warp_sum(a), warp_sum(b));
+}
+
+template <typename T, int VPT>
+__global__ void __launch_bounds__(512) ln_fwd_v(const T* __restrict__ x,
+                                                 const float* __restrict__ g,
+                                                 const float* __restrict__ b, T* __restrict__ y,
+                                                 float* __restrict__ mean,
+                                                 float* __restrict__ rstd, int h, float eps) {
+  constexpr int VW = kVW<T>;
+  __shared__ float red[64];
+  const int64_t row = blockIdx.x;
+  const int nvec = h / VW;
+  uint4 raw[VPT];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int vi = threadIdx.x + i * blockDim.x;
+    if (vi < nvec) raw[i] = ld16(x + row * h + (int64_t)vi * VW);
+  }
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    if (threadIdx.x + i * blockDim.x < nvec) {
+      float v[VW];
+      unpack<T>(raw[i], v);
+#pragma unroll
+      for (int j = 0; j < VW; ++j) s += v[j];
+    }
+  }
+  const float mu = block_sum(s, red) / (float)h;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    if (threadIdx.x + i * blockDim.x < nvec) {
+      float v[VW];
+      unpack<T>(raw[i], v);
+#pragma unroll
+      for (int j = 0; j < VW; ++j) q += (v[j] - mu) * (v[j] - mu);
+    }
+  }
+  const float var = block_sum(q, red) / (float)h;
+  const float rs = 1.0f / sqrtf(var + eps);
+  if (threadIdx.x == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int vi = threadIdx.x + i * blockDim.x;
+    if (vi < nvec) {
+      float v[VW], gv[VW], bv[VW], o[VW];
+      unpack<T>(raw[i], v);
+      ldcols<VW>(g, vi * VW, gv);
+      ldcols<VW>(b, vi * VW, bv);
+#pragma unroll
+      for (int j = 0; j < VW; ++j) o[j] = (v[j] - mu) * rs * gv[j] + bv[j];
+      st16(y + row * h + (int64_t)vi * VW, pack<T>(o));
+    }
+  }
+}
+
+// Bias + dropout + residual (+ LayerNorm of the result). The dropout keep bits of the VW
+// elements of a vector come from the counter RNG in its hot-loop form (rng_fast.cuh): the
+// high half of the 64-bit counter is shared by the vector unless its low half carries.
+template <typename T, int VPT, bool LN>
+__global__ void __launch_bounds__(512) bdr_v(const T* __restrict__ a, const float* __restrict__ bias,
+                                              const T* __restrict__ resid, T* __restrict__ r_out,
+                                              uint8_t* __restrict__ mask_out,
+                                              T* __restrict__ ln_out, const float* __restrict__ g,
+                                              const float* __restrict__ lb,
+                                              float* __restrict__ mean, float* __restrict__ rstd,
+                                              int h, DropKey key, uint64_t base, float eps,
+                                              int* nonfinite, rngk::ShiftMuls sm) {
+  using namespace rngk;
+  constexpr int VW = kVW<T>;
+  __shared__ float red[64];
+  const int64_t row = blockIdx.x;
+  const int nvec = h / VW;
+  const uint64_t tsh = key.thresh << 11;
+  const uint32_t mixed_lo = (uint32_t)key.mixed, mixed_hi = (uint32_t)(key.mixed >> 32);
+  const uint32_t t_lo = (uint32_t)tsh, t_hi = (uint32_t)(tsh >> 32);
+  uint4 ar[VPT], xr[VPT];
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int vi = threadIdx.x + i * blockDim.x;
+    if (vi < nvec) {
+      const int64_t off = row * h + (int64_t)vi * VW;
+      ar[i] = ld16(a + off);
+      xr[i] = ld16(resid + off);
+    }
+  }
+  float s = 0.f;
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int vi = threadIdx.x + i * blockDim.x;
+    if (vi < nvec) {
+      const int64_t off = row * h + (int64_t)vi * VW;
+      uint32_t kb = (1u << VW) - 1u;
+      if (key.thresh != 0) {
+        const uint64_t B = base + (uint64_t)off + kC + kG;
+        const uint32_t blo = (uint32_t)B, bhi = (uint32_t)(B >> 32);
+        kb = 0;
+        if (blo <= 0xffffffffu - (uint32_t)(VW - 1)) {
+          const uint32_t hx = bhi ^ (bhi >> 30);
+          const uint32_t hc = hx * 0x1ce4e5b9u;
+#pragma unroll
+          for (int j = 0; j < VW; ++j)
+            if (keep_fast(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm)) kb |= 1u << j;
+        } else {
+          for (int j = 0; j < VW; ++j)
+            if (mix_post((mix_post(B + j) ^ key.mixed) + kG) >= tsh) kb |= 1u << j;
+        }
+      }
+      float av[VW], xv[VW], bv[VW], v[VW];
+      unpack<T>(ar[i], av);
+      unpack<T>(xr[i], xv);
+      ldcols<VW>(bias, vi * VW, bv);
+      uint32_t mw[2] = {0u, 0u};
+#pragma unroll
+      for (int j = 0; j < VW; ++j) {
+        const bool keep = (kb >> j) & 1u;
+        const float t = (av[j] + bv[j]) * (keep ? 1.f : 0.f) * key.inv_keep;
+        v[j] = round_t<T>(xv[j] + t);
+        s += v[j];
+        bad |= !isfinite(v[j]);
+        mw[j >> 2] |= (keep ? 1u : 0u) << (8 * (j & 3));
+      }
+      xr[i] = pack<T>(v);  // the residual output, exact in T
+      st16(r_out + off, xr[i]);
+      if constexpr (VW == 8) *reinterpret_cast<uint2*>(mask_out + off) = make_uint2(mw[0], mw[1]);
+      else *reinterpret_cast<uint32_t*>(mask_out + off) = mw[0];
+    }
+  }
+  if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
+  if constexpr (LN) {
+    const float mu = block_sum(s, red) / (float)h;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      if (threadIdx.x + i * blockDim.x < nvec) {
+        float v[VW];
+        unpack<T>(xr[i], v);
+#pragma unroll
+        for (int j = 0; j < VW; ++j) q += (v[j] - mu) * (v[j] - mu);
+      }
+    }
+    const float var = block_sum(q, red) / (float)h;
+    const float rs = 1.0f / sqrtf(var + eps);
+    if (threadIdx.x == 0) {
+      mean[row] = mu;
+      rstd[row] = rs;
+    }
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const int vi = threadIdx.x + i * blockDim.x;
+      if (vi < nvec) {
+        float v[VW], gv[VW], bv[VW], o[VW];
+        unpack<T>(xr[i], v);
+        ldcols<VW>(g, vi * VW, gv);
+        ldcols<VW>(lb, vi * VW, bv);
+#pragma unroll
+        for (int j = 0; j < VW; ++j) o[j] = (v[j] - mu) * rs * gv[j] + bv[j];
+        st16(ln_out + row * h + (int64_t)vi * VW, pack<T>(o));
+      }
+    }
+  }
+}
+
+// LN backward, dx part: dx = resid + rs·(dŷ - mean(dŷ) - x̂·mean(dŷ·x̂)), dŷ = dy·γ; dy, x
+// and resid each read once (packed in registers), one two-value CTA reduction.
+template <typename T, int VPT>
+__global__ void __launch_bounds__(512) ln_bwd_dx_v(const T* __restrict__ dy, const T* __restrict__ x,
+                                                   const float* __restrict__ mean,
+                                                   const float* __restrict__ rstd,
+                                                   const float* __restrict__ g,
+                                                   const T* __restrict__ resid,
+                                                   T* __restrict__ dx, int h) {
+  constexpr int VW = kVW<T>;
+  __shared__ float red[64];
+  const int64_t row = blockIdx.x;
+  const int nvec = h / VW;
+  uint4 dr[VPT], xr[VPT], rr[VPT];
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int vi = threadIdx.x + i * blockDim.x;
+    if (vi < nvec) {
+      const int64_t off = row * h + (int64_t)vi * VW;
+      dr[i] = ld16(dy + off);
+      xr[i] = ld16(x + off);
+      rr[i] = ld16(resid + off);
+    }
+  }
+  const float mu = mean[row], rs = rstd[row];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int vi = threadIdx.x + i * blockDim.x;
+    if (vi < nvec) {
+      float dv[VW], xv[VW], gv[VW];
+      unpack<T>(dr[i], dv);
+      unpack<T>(xr[i], xv);
+      ldcols<VW>(g, vi * VW, gv);
+#pragma unroll
+      for (int j = 0; j < VW; ++j) {
+        const float xhat = (xv[j] - mu) * rs;
+        const float dxhat = dv[j] * gv[j];
+        s1 += dxhat;
+        s2 += dxhat * xhat;
+      }
+    }
+  }
+  const float2 ss = block_sum2(s1, s2, red);
+  const float inv_h = 1.0f / (float)h;
+  const float m1 = ss.x * inv_h, m2 = ss.y * inv_h;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int vi = threadIdx.x + i * blockDim.x;
+    if (vi < nvec) {
+      float dv[VW], xv[VW], rv[VW], gv[VW], o[VW];
+      unpack<T>(dr[i], dv);
+      unpack<T>(xr[i], xv);
+      unpack<T>(rr[i], rv);
+      ldcols<VW>(g, vi * VW, gv);
+#pragma unroll
+      for (int j = 0; j < VW; ++j) {
+        const float xhat = (xv[j] - mu) * rs;
+        o[j] = rv[j] + rs * (dv[j] * gv[j] - m1 - xhat * m2);
+      }
+      st16(dx + row * h + (int64_t)vi * VW, pack<T>(o));
+    }
+  }
+}
+
 // ---------------------------------------------------------------- LN backward, dx part
 // Row per CTA; two passes over the row (the second hits L1/L2), no column accumulation.
 template <typename T, int VW>
@@ -308,6 +624,7 @@ __global__ void ln_bwd_params_k(const T* __restrict__ dy, const T* __restrict__ 
   float ag[VW], ab[VW];
 #pragma unroll
   for (int j = 0; j < VW; ++j) ag[j] = ab[j] = 0.f;
+#pragma unroll 8
   for (int64_t r = r0; r < r1; ++r) {
     float dv[VW], xv[VW];
     load_vec<T, VW>(dy + r * h + (int64_t)vi * VW, dv);
@@ -340,6 +657,7 @@ __global__ void dropout_bwd_colsum_k(const T* __restrict__ dy, const uint8_t* __
   float acc[VW];
 #pragma unroll
   for (int j = 0; j < VW; ++j) acc[j] = 0.f;
+#pragma unroll 8
   for (int64_t r = r0; r < r1; ++r) {
     const int64_t off = r * h + (int64_t)vi * VW;
     float dv[VW], o[VW];
@@ -358,6 +676,31 @@ __global__ void dropout_bwd_colsum_k(const T* __restrict__ dy, const uint8_t* __
   for (int j = 0; j < VW; ++j) p[j] = acc[j];
 }
 
+// 16-byte column vectors (VW columns per thread), a chunk of rows per CTA row
+template <typename T>
+__global__ void colsum_partial_v(const T* __restrict__ x, int64_t rows, int64_t n, int64_t ld,
+                                 float* __restrict__ partials, int chunk) {
+  constexpr int VW = kVW<T>;
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * VW;
+  if (c >= n) return;
+  const int64_t r0 = (int64_t)blockIdx.y * chunk;
+  const int64_t r1 = min(rows, r0 + chunk);
+  float acc[VW];
+#pragma unroll
+  for (int j = 0; j < VW; ++j) acc[j] = 0.f;
+#pragma unroll 4
+  for (int64_t r = r0; r < r1; ++r) {
+    float v[VW];
+    unpack<T>(ld16(x + r * ld + c), v);
+#pragma unroll
+    for (int j = 0; j < VW; ++j) acc[j] += v[j];
+  }
+  float* p = partials + (int64_t)blockIdx.y * n + c;
+#pragma unroll
+  for (int j = 0; j < VW; j += 4)
+    *reinterpret_cast<float4*>(p + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+}
+
 template <typename T>
 __global__ void colsum_partial_k(const T* __restrict__ x, int64_t rows, int64_t n, int64_t ld,
                                  float* __restrict__ partials, int chunk) {
@@ -370,13 +713,30 @@ __global__ void colsum_partial_k(const T* __restrict__ x, int64_t rows, int64_t 
   partials[(int64_t)blockIdx.y * n + j] = acc;
 }
 
-__global__ void reduce_partials_k(const float* __restrict__ partials, int nchunks, int64_t n,
-                                  float* __restrict__ out, int accumulate) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  float acc = accumulate ? out[j] : 0.f;
-  for (int c = 0; c < nchunks; ++c) acc += partials[(int64_t)c * n + j];
-  out[j] = acc;
+// out[j] (+)= sum_c partials[c][j]. CTA = 32 columns x 8 chunk groups: every thread sums its
+// group's chunks with all loads in flight, then the 8 group sums are added in a fixed order
+// (deterministic; the chunk count is ~rows/64, so a column is far too short to stream alone).
+__global__ void __launch_bounds__(256) reduce_partials_k(const float* __restrict__ partials,
+                                                         int nchunks, int64_t n,
+                                                         float* __restrict__ out, int accumulate) {
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+  float acc = 0.f;
+  if (j < n) {
+    const int per = (nchunks + 7) / 8;
+    const int c0 = grp * per, c1 = min(nchunks, c0 + per);
+#pragma unroll 8
+    for (int c = c0; c < c1; ++c) acc += partials[(int64_t)c * n + j];
+  }
+  red[grp][lane] = acc;
+  __syncthreads();
+  if (grp == 0 && j < n) {
+    float t = red[0][lane];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) t += red[g][lane];
+    out[j] = accumulate ? out[j] + t : t;
+  }
 }
 
 // ---------------------------------------------------------------- init
@@ -465,9 +825,12 @@ void layernorm_fwd(const T* x, const float* gain, const float* bias, T* y, float
                    float* rstd, int64_t rows, int64_t h, float eps, cudaStream_t st) {
   if (rows == 0) return;
   constexpr int VW = vec_width<T>();
-  if (h % VW == 0 && h / VW <= 512 * kVPT) {
-    ln_fwd_k<T, VW><<<(unsigned)rows, row_threads(h / VW), 0, st>>>(x, gain, bias, y, mean, rstd,
-                                                                    (int)h, eps);
+  if (h % VW == 0 && pick_vpt(h / VW) == 4) {
+    ln_fwd_v<T, 4><<<(unsigned)rows, vthreads(h / VW, 4), 0, st>>>(x, gain, bias, y, mean, rstd,
+                                                                   (int)h, eps);
+  } else if (h % VW == 0 && pick_vpt(h / VW) == 8) {
+    ln_fwd_v<T, 8><<<(unsigned)rows, vthreads(h / VW, 8), 0, st>>>(x, gain, bias, y, mean, rstd,
+                                                                   (int)h, eps);
   } else {
     require(h <= 512 * kVPT, "layernorm: hidden too large for the unaligned path");
     ln_fwd_k<T, 1><<<(unsigned)rows, row_threads(h), 0, st>>>(x, gain, bias, y, mean, rstd,
@@ -483,8 +846,25 @@ void bias_dropout_residual(const T* a, const float* bias, const T* resid, T* r_o
                            uint64_t base_index, float eps, int* nonfinite, cudaStream_t st) {
   if (rows == 0) return;
   constexpr int VW = vec_width<T>();
-  const bool vec = h % VW == 0 && h / VW <= 512 * kVPT;
-  require(vec || h <= 512 * kVPT, "bias_dropout_residual: hidden too large");
+  if (h % VW == 0 && pick_vpt(h / VW) != 0) {
+    const rngk::ShiftMuls sm{4u, 32u, 2u, 1u};
+    const int vpt = pick_vpt(h / VW);
+    const unsigned nt = (unsigned)vthreads(h / VW, vpt);
+#define SPL_BDRV(VPTX, LNX)                                                                   \
+  bdr_v<T, VPTX, LNX><<<(unsigned)rows, nt, 0, st>>>(a, bias, resid, r_out, mask_out, ln_out, \
+                                                     gain, lnb, mean, rstd, (int)h, key,      \
+                                                     base_index, eps, nonfinite, sm)
+    if (vpt == 4) {
+      if (ln_out) SPL_BDRV(4, true); else SPL_BDRV(4, false);
+    } else {
+      if (ln_out) SPL_BDRV(8, true); else SPL_BDRV(8, false);
+    }
+#undef SPL_BDRV
+    SPL_CHECK_LAUNCH();
+    return;
+  }
+  const bool vec = false;
+  require(h <= 512 * kVPT, "bias_dropout_residual: hidden too large");
   const int nt = row_threads(vec ? h / VW : h);
 #define SPL_BDR(VWX, LNX)                                                                    \
   bdr_k<T, VWX, LNX><<<(unsigned)rows, nt, 0, st>>>(a, bias, resid, r_out, mask_out, ln_out, \
@@ -528,9 +908,17 @@ void layernorm_bwd(const T* dy, const T* x, const float* mean, const float* rstd
   const int nch = num_chunks(rows, chunk_rows);
   if (h % VW == 0) {
     const int64_t nvec = h / VW;
-    int nt = (int)std::min<int64_t>(512, ((nvec + 31) / 32) * 32);
-    ln_bwd_dx_k<T, VW><<<(unsigned)rows, nt, 0, st>>>(dy, x, mean, rstd, gain, resid_grad, dx,
-                                                      (int)h);
+    if (pick_vpt(nvec) == 4) {
+      ln_bwd_dx_v<T, 4><<<(unsigned)rows, vthreads(nvec, 4), 0, st>>>(dy, x, mean, rstd, gain,
+                                                                      resid_grad, dx, (int)h);
+    } else if (pick_vpt(nvec) == 8) {
+      ln_bwd_dx_v<T, 8><<<(unsigned)rows, vthreads(nvec, 8), 0, st>>>(dy, x, mean, rstd, gain,
+                                                                      resid_grad, dx, (int)h);
+    } else {
+      int nt = (int)std::min<int64_t>(512, ((nvec + 31) / 32) * 32);
+      ln_bwd_dx_k<T, VW><<<(unsigned)rows, nt, 0, st>>>(dy, x, mean, rstd, gain, resid_grad, dx,
+                                                        (int)h);
+    }
     dim3 grid((unsigned)((nvec + 127) / 128), (unsigned)nch);
     ln_bwd_params_k<T, VW><<<grid, 128, 0, st>>>(dy, x, mean, rstd, pgain, pbias, rows, (int)h,
                                                  chunk_rows);
@@ -549,16 +937,22 @@ template <typename T>
 void colsum_partial(const T* x, int64_t rows, int64_t n, int64_t ld, float* partials,
                     int chunk_rows, cudaStream_t st) {
   if (rows == 0 || n == 0) return;
-  dim3 grid((unsigned)((n + 127) / 128), (unsigned)num_chunks(rows, chunk_rows));
-  colsum_partial_k<T><<<grid, 128, 0, st>>>(x, rows, n, ld, partials, chunk_rows);
+  constexpr int VW = vec_width<T>();
+  if (n % VW == 0 && ld % VW == 0 && ((uintptr_t)x & 15) == 0) {
+    dim3 grid((unsigned)((n / VW + 127) / 128), (unsigned)num_chunks(rows, chunk_rows));
+    colsum_partial_v<T><<<grid, 128, 0, st>>>(x, rows, n, ld, partials, chunk_rows);
+  } else {
+    dim3 grid((unsigned)((n + 127) / 128), (unsigned)num_chunks(rows, chunk_rows));
+    colsum_partial_k<T><<<grid, 128, 0, st>>>(x, rows, n, ld, partials, chunk_rows);
+  }
   SPL_CHECK_LAUNCH();
 }
 
 void reduce_partials(const float* partials, int nchunks, int64_t n, float* out, bool accumulate,
                      cudaStream_t st) {
   if (n == 0) return;
-  reduce_partials_k<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(partials, nchunks, n, out,
-                                                                 accumulate ? 1 : 0);
+  reduce_partials_k<<<(unsigned)((n + 31) / 32), 256, 0, st>>>(partials, nchunks, n, out,
+                                                               accumulate ? 1 : 0);
   SPL_CHECK_LAUNCH();
 }
 
