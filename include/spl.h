@@ -148,6 +148,45 @@ int spl_per_layer_bytes_exact(int64_t a, int64_t h, int64_t s, int64_t b, int64_
                               int sequence_parallel, int64_t act_bytes, int64_t mask_bytes,
                               int64_t* num, int64_t* den);
 
+/* layer_component_breakdown (activation_memory.cpp:84-104): serial-layer bytes of the
+ * attention block, the MLP block and the two layer norms, and their total: out[4]. */
+int spl_layer_component_breakdown(int64_t a, int64_t h, int64_t s, int64_t b, int64_t act_bytes,
+                                  int64_t mask_bytes, int64_t out[4]);
+/* percent_of_baseline (activation_memory.cpp:195-200): per-layer bytes of the regime over the
+ * tensor-parallel no-recompute baseline, as an exact fraction num/den. */
+int spl_percent_of_baseline(int64_t a, int64_t h, int64_t s, int64_t b, int64_t t, int kind,
+                            int sequence_parallel, int64_t act_bytes, int64_t mask_bytes,
+                            int64_t* num, int64_t* den);
+/* total_first_stage_bytes (activation_memory.cpp:112-123): per-layer bytes x L x
+ * interleave_factor (1 + (p-1)/(p*m) for m > 1), floored once. L % (p*m) == 0. */
+int spl_total_first_stage_bytes(int64_t a, int64_t h, int64_t s, int64_t b, int64_t t, int kind,
+                                int sequence_parallel, int64_t layers, int64_t pipeline,
+                                int64_t interleave, int64_t act_bytes, int64_t mask_bytes,
+                                int64_t* bytes_out);
+
+/* Layer stack: L layers of one desc (layer l uses layer_index = d->layer_index + l, so every
+ * layer draws its own dropout masks) on t simulated ranks, sharing ONE transient workspace;
+ * each layer keeps only its own saved activations. The p = 1 stage that
+ * total_first_stage_bytes and simulate_memory (pipeline_sim.cpp:222-275) account for.
+ * spl_stack_forward runs layers 0..L-1 (x -> y), spl_stack_backward L-1..0 (dy -> dx); the
+ * inter-layer activations live in two stack-owned ping-pong buffers. Per-layer parameters,
+ * gradients, ledgers and profiles go through the borrowed handle of spl_stack_layer (do not
+ * spl_destroy it). */
+typedef struct spl_stack spl_stack;
+int spl_stack_create_local(const spl_layer_desc* d, int device, int t, int layers,
+                           spl_stack** out);
+int spl_stack_destroy(spl_stack* st);
+int spl_stack_layers(const spl_stack* st);
+int spl_stack_layer(spl_stack* st, int layer, spl_handle** out);
+int spl_stack_set_stream(spl_stack* st, void* cuda_stream);
+int spl_stack_forward(spl_stack* st, const void* const* x, void* const* y);
+int spl_stack_backward(spl_stack* st, const void* const* dy, void* const* dx);
+/* Device bytes of one local rank summed over the layers: out[0] ledger (reference
+ * convention), [1] physical saved activations, [2] saved but uncounted (LN stats / LSE),
+ * [3] shared workspace (pool + ping-pong), [4] parameters, [5] gradients, [6] per-layer
+ * workspace outside the pool (0 for a stack). */
+int spl_stack_memory(spl_stack* st, int local_rank, int64_t out[7]);
+
 /* Device timing on the handle's compute stream (CUDA events; synchronizes at stop). */
 int spl_timer_start(spl_handle* h);
 int spl_timer_stop(spl_handle* h, float* ms);

@@ -91,6 +91,9 @@ def lib():
         L.orc_percent_of_baseline.restype = i32
         L.orc_percent_of_baseline.argtypes = [i64, i64, i64, i64, i64, i32, i32, i64, i64,
                                               C.POINTER(i64), C.POINTER(i64)]
+        L.orc_total_first_stage_bytes.restype = i32
+        L.orc_total_first_stage_bytes.argtypes = [i64, i64, i64, i64, i64, i32, i32, i64, i64,
+                                                  i64, i64, i64, C.POINTER(i64)]
         L.orc_layer_comm_bytes_tp.restype = i64
         L.orc_layer_comm_bytes_tp.argtypes = [i64, i64, i64, i64, i64]
         L.orc_layer_comm_bytes_sp.restype = i64
@@ -305,6 +308,17 @@ def percent_of_baseline(a, h, s, b, t, kind, sequence_parallel, act=2, mask=1):
     if rc:
         raise ValueError("invalid configuration")
     return n.value, d.value
+
+
+def total_first_stage_bytes(a, h, s, b, t, kind, sequence_parallel, layers, pipeline=1,
+                            interleave=1, act=2, mask=1):
+    out = C.c_int64()
+    rc = lib().orc_total_first_stage_bytes(a, h, s, b, t, KIND.get(kind, kind),
+                                           int(sequence_parallel), layers, pipeline, interleave,
+                                           act, mask, C.byref(out))
+    if rc:
+        raise ValueError("invalid configuration")
+    return out.value
 
 
 def layer_comm_bytes_tp(s, b, h, t, elem=2):

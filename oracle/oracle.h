@@ -130,6 +130,10 @@ int orc_layer_component_breakdown(int64_t a, int64_t h, int64_t s, int64_t b, in
 int orc_percent_of_baseline(int64_t a, int64_t h, int64_t s, int64_t b, int64_t t, int kind,
                             int sequence_parallel, int64_t act, int64_t mask, int64_t* num,
                             int64_t* den);
+int orc_total_first_stage_bytes(int64_t a, int64_t h, int64_t s, int64_t b, int64_t t, int kind,
+                                int sequence_parallel, int64_t layers, int64_t pipeline,
+                                int64_t interleave, int64_t act, int64_t mask,
+                                int64_t* bytes_out);
 /* layer_comm_bytes_tensor_parallel / _sequence (collectives.cpp:75-87) */
 int64_t orc_layer_comm_bytes_tp(int64_t s, int64_t b, int64_t h, int64_t t, int64_t elem);
 int64_t orc_layer_comm_bytes_sp(int64_t s, int64_t b, int64_t h, int64_t t, int64_t elem);

@@ -5,6 +5,7 @@
  *   per_layer_bytes     activation_memory.cpp:54-82 (floor once, rational.hpp:32-49)
  *   breakdown           activation_memory.cpp:84-104
  *   percent_of_baseline activation_memory.cpp:195-200
+ *   total_first_stage   activation_memory.cpp:106-123 (interleave_factor, x L, floor once)
  * and validate() from config.cpp:86-133 (the shape/layout rules that apply per layer).
  * Boost rationals are replaced by __int128 num/den: every per-layer value has denominator 1
  * or t, so 128-bit arithmetic is exact for all shapes whose byte counts fit int64. */
@@ -117,6 +118,26 @@ int orc_percent_of_baseline(int64_t a, int64_t h, int64_t s, int64_t b, int64_t 
   if (!fits64(n) || !fits64(d)) return 3;
   *num = (int64_t)n;
   *den = (int64_t)d;
+  return 0;
+}
+
+int orc_total_first_stage_bytes(int64_t a, int64_t h, int64_t s, int64_t b, int64_t t, int kind,
+                                int sequence_parallel, int64_t layers, int64_t pipeline,
+                                int64_t interleave, int64_t act, int64_t mask,
+                                int64_t* bytes_out) {
+  /* config.cpp:94-117: L, p, m >= 1 and L divisible by p*m */
+  if (layers < 1 || pipeline < 1 || interleave < 1) return 1;
+  if (layers % (pipeline * interleave) != 0) return 1;
+  i128 n, d;
+  if (per_layer_rational(a, h, s, b, t, kind, sequence_parallel, act, mask, &n, &d)) return 1;
+  n *= layers;
+  if (interleave > 1) { /* 1 + (p-1)/(p*m) = (p*m + p - 1)/(p*m), activation_memory.cpp:106-110 */
+    n *= (i128)pipeline * interleave + pipeline - 1;
+    d *= (i128)pipeline * interleave;
+  }
+  i128 q = n / d;
+  if (!fits64(q)) return 3;
+  *bytes_out = (int64_t)q;
   return 0;
 }
 

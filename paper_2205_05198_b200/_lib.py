@@ -83,6 +83,18 @@ def lib():
         "spl_profile_read": (I32, [H, P(D), P(I64), P(D), P(D)]),
         "spl_launch_count": (I32, [H, P(I64), I32]),
         "spl_set_graphs": (I32, [H, I32]),
+        "spl_layer_component_breakdown": (I32, [I64, I64, I64, I64, I64, I64, P(I64)]),
+        "spl_percent_of_baseline": (I32, [I64, I64, I64, I64, I64, I32, I32, I64, I64, P(I64), P(I64)]),
+        "spl_total_first_stage_bytes": (I32, [I64, I64, I64, I64, I64, I32, I32, I64, I64, I64,
+                                              I64, I64, P(I64)]),
+        "spl_stack_create_local": (I32, [P(LayerDesc), I32, I32, I32, P(H)]),
+        "spl_stack_destroy": (I32, [H]),
+        "spl_stack_layers": (I32, [H]),
+        "spl_stack_layer": (I32, [H, I32, P(H)]),
+        "spl_stack_set_stream": (I32, [H, VP]),
+        "spl_stack_forward": (I32, [H, P(VP), P(VP)]),
+        "spl_stack_backward": (I32, [H, P(VP), P(VP)]),
+        "spl_stack_memory": (I32, [H, I32, P(I64)]),
         "spl_gemm_bf16": (I32, [I64, I64, I64, VP, I64, I32, VP, I64, I32, VP, I64, I32, VP, VP,
                                 VP, I64, VP, P(I32)]),
     }

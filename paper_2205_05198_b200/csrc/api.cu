@@ -42,12 +42,13 @@ void check_handle(const spl_handle* h) {
   if (h == nullptr || !h->layer) spl::raise(SPL_EINVAL, "null handle");
 }
 
-spl_handle* make_handle(const spl_layer_desc* d, int device, std::unique_ptr<spl::Comm> comm) {
+spl_handle* make_handle(const spl_layer_desc* d, int device, std::unique_ptr<spl::Comm> comm,
+                        std::shared_ptr<spl::WorkPool> pool = nullptr) {
   auto* h = new spl_handle();
   h->device = device;
   try {
     SPL_CUDA(cudaSetDevice(device));
-    h->layer = spl::make_layer(*d, device, std::move(comm));
+    h->layer = spl::make_layer(*d, device, std::move(comm), std::move(pool));
     SPL_CUDA(cudaEventCreate(&h->t0));
     SPL_CUDA(cudaEventCreate(&h->t1));
   } catch (...) {
@@ -55,6 +56,59 @@ spl_handle* make_handle(const spl_layer_desc* d, int device, std::unique_ptr<spl
     throw;
   }
   return h;
+}
+}  // namespace
+
+// L layers (layer_index = d.layer_index + l) sharing one workspace pool, plus two ping-pong
+// shard buffers per local rank for the activations passed between layers.
+struct spl_stack {
+  std::vector<spl_handle*> layers;
+  std::shared_ptr<spl::WorkPool> pool;
+  std::vector<void*> ping[2];
+  int64_t ping_bytes = 0;
+  int device = 0;
+  int local = 0;
+};
+
+namespace {
+void check_stack(const spl_stack* st) {
+  if (st == nullptr || st->layers.empty()) spl::raise(SPL_EINVAL, "null stack");
+}
+void destroy_stack(spl_stack* st) {
+  cudaSetDevice(st->device);
+  for (spl_handle* h : st->layers) {
+    h->layer.reset();
+    if (h->t0) cudaEventDestroy(h->t0);
+    if (h->t1) cudaEventDestroy(h->t1);
+    delete h;
+  }
+  st->layers.clear();
+  st->pool.reset();
+  for (auto& v : st->ping)
+    for (void* p : v) cudaFree(p);
+  delete st;
+}
+
+// ---- accountant helpers (activation_memory.cpp:54-123, rational.hpp:32-49)
+__int128 gcd128(__int128 x, __int128 y) {
+  if (x < 0) x = -x;
+  if (y < 0) y = -y;
+  while (y) {
+    const __int128 r = x % y;
+    x = y;
+    y = r;
+  }
+  return x;
+}
+void layer_rational(int64_t a, int64_t hh, int64_t s, int64_t b, int64_t t, int kind, int sp,
+                    int64_t act, int64_t mask, __int128* n, __int128* d) {
+  if (spl::per_layer_bytes_exact(a, hh, s, b, t, kind, sp, act, mask, n, d))
+    spl::raise(SPL_EINVAL, "invalid configuration");
+}
+int64_t fit64(__int128 v) {
+  if (v > (__int128)INT64_MAX || v < (__int128)INT64_MIN)
+    spl::raise(SPL_EINVAL, "value does not fit in 64-bit integer");
+  return (int64_t)v;
 }
 }  // namespace
 
@@ -257,6 +311,165 @@ int spl_per_layer_bytes_exact(int64_t a, int64_t hh, int64_t s, int64_t b, int64
     if (n > (__int128)INT64_MAX) spl::raise(SPL_EINVAL, "value does not fit in 64-bit integer");
     *num = (int64_t)n;
     *den = (int64_t)d;
+  });
+}
+
+int spl_layer_component_breakdown(int64_t a, int64_t hh, int64_t s, int64_t b, int64_t act,
+                                  int64_t mask, int64_t out[4]) {
+  return guard([&] {
+    __int128 n, d;
+    layer_rational(a, hh, s, b, 1, SPL_RECOMPUTE_NONE, 0, act, mask, &n, &d);  // validation
+    const __int128 sbh = (__int128)s * b * hh, interior = (__int128)a * s * s * b;
+    const __int128 attn = (__int128)5 * act * sbh + (__int128)mask * sbh + ((__int128)2 * act + mask) * interior;
+    const __int128 mlp = (__int128)9 * act * sbh + (__int128)mask * sbh;
+    const __int128 lns = (__int128)2 * act * sbh;
+    out[0] = fit64(attn);
+    out[1] = fit64(mlp);
+    out[2] = fit64(lns);
+    out[3] = fit64(attn + mlp + lns);
+  });
+}
+
+int spl_percent_of_baseline(int64_t a, int64_t hh, int64_t s, int64_t b, int64_t t, int kind,
+                            int sp, int64_t act, int64_t mask, int64_t* num, int64_t* den) {
+  return guard([&] {
+    __int128 n1, d1, n0, d0;
+    layer_rational(a, hh, s, b, t, kind, sp, act, mask, &n1, &d1);
+    layer_rational(a, hh, s, b, t, SPL_RECOMPUTE_NONE, 0, act, mask, &n0, &d0);
+    __int128 n = n1 * d0, d = d1 * n0;
+    const __int128 g = gcd128(n, d);
+    if (g > 1) {
+      n /= g;
+      d /= g;
+    }
+    *num = fit64(n);
+    *den = fit64(d);
+  });
+}
+
+int spl_total_first_stage_bytes(int64_t a, int64_t hh, int64_t s, int64_t b, int64_t t,
+                                int kind, int sp, int64_t layers, int64_t pipeline,
+                                int64_t interleave, int64_t act, int64_t mask, int64_t* out) {
+  return guard([&] {
+    spl::require(layers >= 1, "L must be >= 1");
+    spl::require(pipeline >= 1, "p must be >= 1");
+    spl::require(interleave >= 1, "m must be >= 1");
+    spl::require(layers % (pipeline * interleave) == 0, "L must be divisible by p*m");
+    __int128 n, d;
+    layer_rational(a, hh, s, b, t, kind, sp, act, mask, &n, &d);
+    n *= layers;
+    if (interleave > 1) {  // interleave_factor = 1 + (p-1)/(p*m) (activation_memory.cpp:106-110)
+      n *= (__int128)pipeline * interleave + pipeline - 1;
+      d *= (__int128)pipeline * interleave;
+    }
+    *out = fit64(n / d);  // floor once
+  });
+}
+
+int spl_stack_create_local(const spl_layer_desc* d, int device, int t, int layers,
+                           spl_stack** out) {
+  return guard([&] {
+    spl::require(d != nullptr && out != nullptr, "null argument");
+    spl::require(t >= 1, "t must be >= 1");
+    spl::require(layers >= 1, "L must be >= 1");
+    SPL_CUDA(cudaSetDevice(device));
+    auto* st = new spl_stack();
+    st->device = device;
+    try {
+      st->pool = std::make_shared<spl::WorkPool>();
+      st->pool->device = device;
+      for (int l = 0; l < layers; ++l) {
+        spl_layer_desc dl = *d;
+        dl.layer_index = d->layer_index + (uint32_t)l;
+        st->layers.push_back(make_handle(&dl, device, spl::make_local_comm(t), st->pool));
+      }
+      st->local = st->layers[0]->layer->local_ranks();
+      const int64_t rows = d->sequence_parallel ? d->seq / t : d->seq;
+      st->ping_bytes = rows * d->batch * d->hidden * (d->dtype == SPL_DTYPE_F32 ? 4 : 2);
+      for (auto& v : st->ping)
+        for (int r = 0; r < st->local; ++r) {
+          void* p = nullptr;
+          SPL_CUDA(cudaMalloc(&p, (size_t)st->ping_bytes));
+          v.push_back(p);
+        }
+    } catch (...) {
+      destroy_stack(st);
+      throw;
+    }
+    *out = st;
+  });
+}
+
+int spl_stack_destroy(spl_stack* st) {
+  return guard([&] {
+    if (st) destroy_stack(st);
+  });
+}
+
+int spl_stack_layers(const spl_stack* st) { return st ? (int)st->layers.size() : 0; }
+
+int spl_stack_layer(spl_stack* st, int l, spl_handle** out) {
+  return guard([&] {
+    check_stack(st);
+    spl::require(l >= 0 && l < (int)st->layers.size() && out != nullptr, "layer index out of range");
+    *out = st->layers[l];
+  });
+}
+
+int spl_stack_set_stream(spl_stack* st, void* stream) {
+  return guard([&] {
+    check_stack(st);
+    for (spl_handle* h : st->layers) h->layer->set_caller_stream(static_cast<cudaStream_t>(stream));
+  });
+}
+
+int spl_stack_forward(spl_stack* st, const void* const* x, void* const* y) {
+  return guard([&] {
+    check_stack(st);
+    spl::require(x != nullptr && y != nullptr, "expected one input shard per rank");
+    const int L = (int)st->layers.size();
+    std::vector<const void*> in(x, x + st->local);
+    std::vector<void*> out(st->local);
+    for (int l = 0; l < L; ++l) {
+      for (int r = 0; r < st->local; ++r) out[r] = l == L - 1 ? y[r] : st->ping[l & 1][r];
+      st->layers[l]->layer->forward(in.data(), out.data());
+      for (int r = 0; r < st->local; ++r) in[r] = out[r];
+    }
+  });
+}
+
+int spl_stack_backward(spl_stack* st, const void* const* dy, void* const* dx) {
+  return guard([&] {
+    check_stack(st);
+    spl::require(dy != nullptr && dx != nullptr, "expected one gradient shard per rank");
+    const int L = (int)st->layers.size();
+    std::vector<const void*> g(dy, dy + st->local);
+    std::vector<void*> out(st->local);
+    for (int l = L - 1; l >= 0; --l) {
+      for (int r = 0; r < st->local; ++r) out[r] = l == 0 ? dx[r] : st->ping[l & 1][r];
+      st->layers[l]->layer->backward(g.data(), out.data());
+      for (int r = 0; r < st->local; ++r) g[r] = out[r];
+    }
+  });
+}
+
+int spl_stack_memory(spl_stack* st, int local_rank, int64_t out[7]) {
+  return guard([&] {
+    check_stack(st);
+    spl::require(local_rank >= 0 && local_rank < st->local, "local rank out of range");
+    for (int i = 0; i < 7; ++i) out[i] = 0;
+    for (spl_handle* h : st->layers) {
+      int64_t lb, pb, ub, cat[5];
+      h->layer->saved_bytes(local_rank, &lb, &pb, &ub);
+      h->layer->alloc_bytes(cat);
+      out[0] += lb;
+      out[1] += pb;
+      out[2] += ub;
+      out[4] += cat[spl::kParam];
+      out[5] += cat[spl::kGrad];
+      out[6] += cat[spl::kWork];
+    }
+    out[3] = st->pool->bytes() + 2 * st->ping_bytes * st->local;
   });
 }
 

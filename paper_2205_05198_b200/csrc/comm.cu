@@ -78,26 +78,35 @@ class LocalComm final : public Comm {
   }
   void reserve(size_t bytes) override {
     if (bytes <= scratch_bytes_) return;
-    if (scratch_) SPL_CUDA(cudaFree(scratch_));
+    if (scratch_ && own_) SPL_CUDA(cudaFree(scratch_));
     SPL_CUDA(cudaMalloc(&scratch_, bytes));
     scratch_bytes_ = bytes;
+    own_ = true;
+  }
+  void use_scratch(void* p, size_t bytes) override {
+    if (scratch_ && own_) SPL_CUDA(cudaFree(scratch_));
+    scratch_ = p;
+    scratch_bytes_ = bytes;
+    own_ = false;
   }
   ~LocalComm() override {
-    if (scratch_) cudaFree(scratch_);
+    if (scratch_ && own_) cudaFree(scratch_);
   }
 
  private:
   void ensure_scratch(size_t bytes, cudaStream_t st) {
     if (bytes <= scratch_bytes_) return;
-    if (scratch_) {
+    if (scratch_ && own_) {
       SPL_CUDA(cudaStreamSynchronize(st));
       SPL_CUDA(cudaFree(scratch_));
     }
     SPL_CUDA(cudaMalloc(&scratch_, bytes));
     scratch_bytes_ = bytes;
+    own_ = true;
   }
   void* scratch_ = nullptr;
   size_t scratch_bytes_ = 0;
+  bool own_ = true;
 };
 
 #define SPL_NCCL(expr)                                                             \

@@ -40,6 +40,8 @@ class Comm {
   // Pre-allocate any scratch a collective of up to `bytes` may need (so that no allocation
   // happens while a CUDA graph is being captured).
   virtual void reserve(size_t bytes) { (void)bytes; }
+  // Use a caller-owned device buffer as that scratch (a layer's workspace, shared in a stack).
+  virtual void use_scratch(void* p, size_t bytes) { (void)p; (void)bytes; }
 
   void log(CommTag tag, int kind, int64_t logical_elems) {
     CommCounters& c = counters[tag];

@@ -45,8 +45,9 @@ struct Graph {
 template <typename T>
 class Layer final : public LayerBase {
  public:
-  Layer(const spl_layer_desc& d, int device, std::unique_ptr<Comm> comm)
-      : d_(d), dev_(device), comm_(std::move(comm)) {
+  Layer(const spl_layer_desc& d, int device, std::unique_ptr<Comm> comm,
+        std::shared_ptr<WorkPool> pool)
+      : d_(d), dev_(device), comm_(std::move(comm)), pool_(std::move(pool)) {
     t_ = comm_->t();
     L_ = comm_->local();
     rank0_ = comm_->rank0();
@@ -78,7 +79,11 @@ class Layer final : public LayerBase {
     SPL_CUDA(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming));
     SPL_CUDA(cudaEventCreateWithFlags(&ev_out_, cudaEventDisableTiming));
     allocate();
-    comm_->reserve(std::max<size_t>((size_t)(RF_ * h_) * sizeof(T), (size_t)(6 * h_) * sizeof(float)));
+    {  // collective scratch from the workspace (shared by the layers of a stack)
+      const size_t scr = std::max<size_t>((size_t)(RF_ * h_) * sizeof(T), (size_t)(6 * h_) * sizeof(float));
+      comm_->use_scratch(alloc<uint8_t>((int64_t)scr, kWork, 0), scr);
+      comm_->reserve(scr);
+    }
     // The keep-bit RNG pass runs on the main stream by default: overlapping it with the GEMMs
     // on a side stream measured no faster (the GEMMs already hold the chip at its power cap).
     const char* e = std::getenv("SPL_KEEPBITS_SIDE");
@@ -469,6 +474,11 @@ class Layer final : public LayerBase {
     return v;
   }
 
+  void alloc_bytes(int64_t out[5]) const override {
+    for (int c = 0; c < 5; ++c) out[c] = 0;
+    for (auto& a : allocs_) out[a.cat] += (int64_t)a.bytes;
+  }
+
   void saved_bytes(int r, int64_t* lb, int64_t* pb, int64_t* ub) const override {
     int64_t l = 0, p = 0;
     for (auto& e : ledger(r)) {
@@ -561,6 +571,17 @@ class Layer final : public LayerBase {
   U* alloc(int64_t n, int cat, int r) {
     void* p = nullptr;
     const size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(U);
+    if (cat == kWork && pool_) {  // stack member: the i-th workspace request is shared
+      const size_t i = work_next_++;
+      if (i < pool_->bufs.size()) {
+        require(pool_->bufs[i].second == bytes, "workspace pool: layer shapes differ");
+        return static_cast<U*>(pool_->bufs[i].first);
+      }
+      SPL_CUDA(cudaMalloc(&p, bytes));
+      SPL_CUDA(cudaMemset(p, 0, bytes));
+      pool_->bufs.push_back({p, bytes});
+      return static_cast<U*>(p);
+    }
     SPL_CUDA(cudaMalloc(&p, bytes));
     SPL_CUDA(cudaMemset(p, 0, bytes));
     allocs_.push_back({p, bytes, cat, r});
@@ -1046,6 +1067,8 @@ class Layer final : public LayerBase {
   cudaStream_t caller_ = 0;  // legacy default stream unless set
   std::vector<Rank> R_;
   std::vector<Alloc> allocs_;
+  std::shared_ptr<WorkPool> pool_;  // shared workspace of a stack (nullptr: own buffers)
+  size_t work_next_ = 0;
   std::vector<T*> stage_;
   void* pinned_ = nullptr;
   int* nonfinite_ = nullptr;
@@ -1071,9 +1094,11 @@ class Layer final : public LayerBase {
 }  // namespace
 
 std::unique_ptr<LayerBase> make_layer(const spl_layer_desc& d, int device,
-                                      std::unique_ptr<Comm> comm) {
-  if (d.dtype == SPL_DTYPE_F32) return std::make_unique<Layer<float>>(d, device, std::move(comm));
-  if (d.dtype == SPL_DTYPE_BF16) return std::make_unique<Layer<bf16>>(d, device, std::move(comm));
+                                      std::unique_ptr<Comm> comm, std::shared_ptr<WorkPool> pool) {
+  if (d.dtype == SPL_DTYPE_F32)
+    return std::make_unique<Layer<float>>(d, device, std::move(comm), std::move(pool));
+  if (d.dtype == SPL_DTYPE_BF16)
+    return std::make_unique<Layer<bf16>>(d, device, std::move(comm), std::move(pool));
   raise(1, "unknown dtype");
 }
 

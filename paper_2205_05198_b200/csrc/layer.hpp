@@ -52,10 +52,32 @@ class LayerBase {
   virtual void set_graphs(bool on) = 0;
   virtual int local_ranks() const = 0;
   virtual void set_caller_stream(cudaStream_t s) = 0;
+  // Device bytes this layer allocated per BufCat (kWork: only buffers it owns, not a pool's).
+  virtual void alloc_bytes(int64_t out[5]) const = 0;
+};
+
+// Transient device buffers shared by the layers of a stack. Layers of one stack have identical
+// shapes and run one after another on the caller stream, so the i-th workspace request of every
+// layer maps to the same buffer: an L-layer stack holds L sets of saved activations but one
+// workspace (the unit total_first_stage_bytes / simulate_memory count, activation_memory.cpp
+// :112-123, pipeline_sim.cpp:222-275).
+struct WorkPool {
+  int device = 0;
+  std::vector<std::pair<void*, size_t>> bufs;
+  int64_t bytes() const {
+    int64_t n = 0;
+    for (auto& b : bufs) n += (int64_t)b.second;
+    return n;
+  }
+  ~WorkPool() {
+    cudaSetDevice(device);
+    for (auto& b : bufs) cudaFree(b.first);
+  }
 };
 
 std::unique_ptr<LayerBase> make_layer(const spl_layer_desc& d, int device,
-                                      std::unique_ptr<Comm> comm);
+                                      std::unique_ptr<Comm> comm,
+                                      std::shared_ptr<WorkPool> pool = nullptr);
 
 // Accountant (activation_memory.cpp:54-82) — exact, floor once.
 int per_layer_bytes_exact(int64_t a, int64_t h, int64_t s, int64_t b, int64_t t, int kind,

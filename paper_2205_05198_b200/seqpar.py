@@ -57,25 +57,38 @@ def _tdtype(dtype: str):
     return torch.float32 if _lib.DTYPE[dtype] == 0 else torch.bfloat16
 
 
+def _desc(cfg: BlockConfig, recompute: str, sequence_parallel: bool, dtype: str,
+          check_finite: bool) -> "_lib.LayerDesc":
+    d = _lib.LayerDesc()
+    lib().spl_desc_default(C.byref(d))
+    d.heads, d.hidden, d.seq, d.batch = cfg.heads, cfg.hidden, cfg.seq, cfg.batch
+    d.dropout_p, d.causal, d.seed = cfg.dropout_p, int(cfg.causal), cfg.seed
+    d.layer_index, d.microbatch, d.ln_eps = cfg.layer_index, cfg.microbatch, cfg.layer_norm_eps
+    d.recompute = _lib.RECOMPUTE[recompute]
+    d.sequence_parallel = int(sequence_parallel)
+    d.dtype = _lib.DTYPE[dtype]
+    d.check_finite = int(check_finite)
+    d.act_bytes, d.mask_bytes = cfg.act_bytes, cfg.mask_bytes
+    return d
+
+
 class SeqparLayer:
     """One layer handle: t simulated ranks on one GPU (nccl=None), or one rank of an NCCL
     group (nccl=(rank, unique_id_bytes))."""
 
     def __init__(self, cfg: BlockConfig, t: int, recompute: str = "none",
                  sequence_parallel: bool = True, dtype: str = "bf16", device: int = 0,
-                 check_finite: bool = True, nccl: tuple[int, bytes] | None = None):
+                 check_finite: bool = True, nccl: tuple[int, bytes] | None = None,
+                 _borrow=None):
         self.cfg, self.t, self.recompute, self.sp, self.dtype = cfg, t, recompute, sequence_parallel, dtype
         self.device = device
-        d = _lib.LayerDesc()
-        lib().spl_desc_default(C.byref(d))
-        d.heads, d.hidden, d.seq, d.batch = cfg.heads, cfg.hidden, cfg.seq, cfg.batch
-        d.dropout_p, d.causal, d.seed = cfg.dropout_p, int(cfg.causal), cfg.seed
-        d.layer_index, d.microbatch, d.ln_eps = cfg.layer_index, cfg.microbatch, cfg.layer_norm_eps
-        d.recompute = _lib.RECOMPUTE[recompute]
-        d.sequence_parallel = int(sequence_parallel)
-        d.dtype = _lib.DTYPE[dtype]
-        d.check_finite = int(check_finite)
-        d.act_bytes, d.mask_bytes = cfg.act_bytes, cfg.mask_bytes
+        self._owned = True
+        if _borrow is not None:  # a layer of a SeqparStack: the stack owns the handle
+            self._h, self._owned = _borrow, False
+            self.local = lib().spl_local_ranks(self._h)
+            self.rank0 = 0
+            return
+        d = _desc(cfg, recompute, sequence_parallel, dtype, check_finite)
         self._h = C.c_void_p()
         if nccl is None:
             check(lib().spl_create_local(C.byref(d), device, t, C.byref(self._h)))
@@ -87,9 +100,9 @@ class SeqparLayer:
 
     # ---- lifecycle
     def close(self):
-        if self._h:
+        if self._h and self._owned:
             lib().spl_destroy(self._h)
-            self._h = C.c_void_p()
+        self._h = C.c_void_p()
 
     def __del__(self):
         try:
@@ -315,3 +328,98 @@ def per_layer_bytes_exact(a, h, s, b, t, kind, sequence_parallel, act=2, mask=1)
     check(lib().spl_per_layer_bytes_exact(a, h, s, b, t, _lib.RECOMPUTE[kind], int(sequence_parallel),
                                           act, mask, C.byref(n), C.byref(d)))
     return n.value, d.value
+
+
+def layer_component_breakdown(a: int, h: int, s: int, b: int, act: int = 2, mask: int = 1) -> dict:
+    """layer_component_breakdown (activation_memory.cpp:84-104) through the C ABI."""
+    out = (C.c_int64 * 4)()
+    check(lib().spl_layer_component_breakdown(a, h, s, b, act, mask, out))
+    return dict(attention=out[0], mlp=out[1], layer_norms=out[2], total=out[3])
+
+
+def percent_of_baseline(a, h, s, b, t, kind, sequence_parallel, act=2, mask=1):
+    """percent_of_baseline (activation_memory.cpp:195-200): exact (num, den)."""
+    n, d = C.c_int64(), C.c_int64()
+    check(lib().spl_percent_of_baseline(a, h, s, b, t, _lib.RECOMPUTE[kind], int(sequence_parallel),
+                                        act, mask, C.byref(n), C.byref(d)))
+    return n.value, d.value
+
+
+def total_first_stage_bytes(a, h, s, b, t, kind, sequence_parallel, layers, pipeline=1,
+                            interleave=1, act=2, mask=1) -> int:
+    """total_first_stage_bytes (activation_memory.cpp:112-123) through the C ABI."""
+    out = C.c_int64()
+    check(lib().spl_total_first_stage_bytes(a, h, s, b, t, _lib.RECOMPUTE[kind],
+                                            int(sequence_parallel), layers, pipeline, interleave,
+                                            act, mask, C.byref(out)))
+    return out.value
+
+
+class SeqparStack:
+    """L layers (layer_index = cfg.layer_index + l) on t simulated ranks sharing one workspace
+    (spl_stack_*): the p = 1 stage of total_first_stage_bytes / simulate_memory."""
+
+    def __init__(self, cfg: BlockConfig, t: int, layers: int, recompute: str = "selective",
+                 sequence_parallel: bool = True, dtype: str = "bf16", device: int = 0,
+                 check_finite: bool = True):
+        self.cfg, self.t, self.recompute, self.sp, self.dtype = cfg, t, recompute, sequence_parallel, dtype
+        self.device = device
+        d = _desc(cfg, recompute, sequence_parallel, dtype, check_finite)
+        self._s = C.c_void_p()
+        check(lib().spl_stack_create_local(C.byref(d), device, t, layers, C.byref(self._s)))
+        self.layers = []
+        for l in range(layers):
+            h = C.c_void_p()
+            check(lib().spl_stack_layer(self._s, l, C.byref(h)))
+            cl = BlockConfig(**{**cfg.__dict__, "layer_index": cfg.layer_index + l})
+            self.layers.append(SeqparLayer(cl, t, recompute, sequence_parallel, dtype, device,
+                                           check_finite, _borrow=h))
+        self.local = self.layers[0].local
+
+    def close(self):
+        for L in getattr(self, "layers", []):
+            L.close()
+        if getattr(self, "_s", None):
+            lib().spl_stack_destroy(self._s)
+            self._s = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def shard_shape(self):
+        return self.layers[0].shard_shape()
+
+    def _bind_stream(self):
+        torch = _torch()
+        check(lib().spl_stack_set_stream(self._s, C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+
+    def _run(self, fn, a: list, out: list | None) -> list:
+        torch = _torch()
+        self._bind_stream()
+        if len(a) != self.local:
+            raise ValueError("expected one shard per rank")
+        for ai in a:
+            if tuple(ai.shape) != self.shard_shape() or ai.dtype != _tdtype(self.dtype):
+                raise ValueError(f"shard must be {self.shard_shape()} {self.dtype}")
+        if out is None:
+            out = [torch.empty_like(ai) for ai in a]
+        ap = (C.c_void_p * self.local)(*[ai.data_ptr() for ai in a])
+        op = (C.c_void_p * self.local)(*[oi.data_ptr() for oi in out])
+        check(fn(self._s, ap, op))
+        return out
+
+    def forward(self, x: list, y: list | None = None) -> list:
+        return self._run(lib().spl_stack_forward, x, y)
+
+    def backward(self, dy: list, dx: list | None = None) -> list:
+        return self._run(lib().spl_stack_backward, dy, dx)
+
+    def memory(self, r: int = 0) -> dict:
+        out = (C.c_int64 * 7)()
+        check(lib().spl_stack_memory(self._s, r, out))
+        keys = ["ledger", "physical_saved", "uncounted_saved", "workspace", "params", "grads",
+                "layer_workspace"]
+        return dict(zip(keys, list(out)))

@@ -49,3 +49,37 @@ def test_accountant_pins():
     assert spl.per_layer_bytes(128, 20480, 2048, 1, 8, "selective", True) == 178_257_920
     with pytest.raises(ValueError):
         spl.per_layer_bytes(4, 100, 2048, 1, 8, "none", False)
+
+
+def test_accountant_extras_match_oracle(orc):
+    """layer_component_breakdown, percent_of_baseline and total_first_stage_bytes of the product
+    library (host code behind the C ABI) equal the oracle restatement and the reference pins."""
+    import random
+    assert spl.layer_component_breakdown(2, 8, 4, 1) == dict(attention=512, mlp=608, layer_norms=128, total=1248)
+    assert spl.percent_of_baseline(128, 20480, 2048, 1, 8, "selective", True) == (17, 84)
+    assert spl.percent_of_baseline(128, 20480, 2048, 1, 8, "full", False) == (2, 21)
+    assert spl.total_first_stage_bytes(128, 20480, 2048, 1, 8, "selective", True, 105, 35, 3) == 24_777_850_880
+    rng = random.Random(7)
+    for _ in range(500):
+        a = rng.randint(1, 16)
+        h = a * rng.randint(1, 32)
+        t = rng.choice([1, 2, 4, 8])
+        if a % t or h % t:
+            continue
+        s = t * rng.randint(1, 64)
+        b = rng.randint(1, 8)
+        act, mask = rng.choice([(2, 1), (4, 1), (2, 2)])
+        kind = rng.choice(["none", "selective", "full"])
+        sp = rng.random() < 0.5
+        L = rng.choice([1, 2, 6, 12])
+        p = rng.choice([1, 2, 3])
+        m = rng.choice([1, 2])
+        assert spl.layer_component_breakdown(a, h, s, b, act, mask) == orc.layer_component_breakdown(a, h, s, b, act, mask)
+        assert spl.percent_of_baseline(a, h, s, b, t, kind, sp, act, mask) == \
+            orc.percent_of_baseline(a, h, s, b, t, kind, sp, act, mask)
+        if L % (p * m):
+            with pytest.raises(ValueError):
+                spl.total_first_stage_bytes(a, h, s, b, t, kind, sp, L, p, m, act, mask)
+        else:
+            assert spl.total_first_stage_bytes(a, h, s, b, t, kind, sp, L, p, m, act, mask) == \
+                orc.total_first_stage_bytes(a, h, s, b, t, kind, sp, L, p, m, act, mask)

@@ -138,3 +138,17 @@ def test_baseline_table(orc, key):
 def test_comm_models(orc):  # collectives.cpp:75-87; verify.cpp:285-321
     for t in (2, 4, 8):
         assert orc.layer_comm_bytes_sp(2048, 4, 6144, t) == orc.layer_comm_bytes_tp(2048, 4, 6144, t)
+
+
+def test_total_first_stage(orc):  # test_activation_memory.cpp:76-99
+    a, h, s = S22
+    assert orc.total_first_stage_bytes(a, h, s, 4, 8, "none", False, 48) == \
+        orc.per_layer_bytes(a, h, s, 4, 8, "none", False) * 48
+    a, h, s = S530  # ParallelLayout{t=8, p=35, m=3, d=1, b=1, n_mb=280}
+    assert orc.total_first_stage_bytes(a, h, s, 1, 8, "selective", True, 105, 35, 3) == 24_777_850_880
+    # interleave factors 31/24 (175B, p=8 m=3) and 139/105 (530B, p=35 m=3): 96 L -> 124 L
+    a, h, s = S175
+    one = orc.per_layer_bytes(a, h, s, 1, 8, "selective", True)
+    assert orc.total_first_stage_bytes(a, h, s, 1, 8, "selective", True, 96, 8, 3) == one * 124
+    with pytest.raises(ValueError):  # L % (p*m) != 0 (config.cpp:114-117)
+        orc.total_first_stage_bytes(a, h, s, 1, 8, "selective", True, 96, 7, 3)
