@@ -55,7 +55,11 @@ struct FwdCfg {
   static constexpr int O_COL = 256;  // O accumulator columns [256, 256 + HD)
 };
 
-template <int HD, bool CAUSAL>
+// MAT (no-recompute regime): pass 2 also writes the interior the reference stores —
+// softmax_out P, the softmax-dropout mask (the raw keep bit at every position, block.cpp:
+// 392-394) and softmax_dropout_out P·mask/(1-p) — as {lh, b, s, s} rows (bf16, u8, bf16);
+// every key tile is visited (causal-masked tiles still carry mask bits).
+template <int HD, bool CAUSAL, bool MAT>
 __global__ void __launch_bounds__(320, 1)
     fa_fwd_umma(const __grid_constant__ CUtensorMap map_qkv, AttnArgs a) {
   using Cfg = FwdCfg<HD>;
@@ -79,7 +83,7 @@ __global__ void __launch_bounds__(320, 1)
   const int q0 = blockIdx.x * 128;
   const int hl = blockIdx.y / (int)a.b, bj = blockIdx.y % (int)a.b;
   const int S = (int)a.s;
-  const int kv_end = CAUSAL ? min(S, q0 + 128) : S;
+  const int kv_end = (CAUSAL && !MAT) ? min(S, q0 + 128) : S;
   const int nkv = (kv_end + 127) / 128;
   const int qcol = (int)(a.qoff + (int64_t)hl * HD), kcol = (int)(a.koff + (int64_t)hl * HD),
             vcol = (int)(a.voff + (int64_t)hl * HD);
@@ -249,6 +253,7 @@ __global__ void __launch_bounds__(320, 1)
     }
     asm volatile("bar.sync 1, 256;" ::: "memory");  // stats read before P overwrites them
     const float scale_p = a.drop.inv_keep / l;  // 1/l and the dropout rescale folded
+    const float inv_l = 1.0f / l;
     const float mm = m == -INFINITY ? 0.f : m;
     // pass 2: probabilities -> P̃ (bf16, K-major SW128 in smem)
     const int kw0 = half * 2;  // this half's first 32-key word within a tile
@@ -280,20 +285,53 @@ __global__ void __launch_bounds__(320, 1)
       const bool full = tile_full(j);
       const int k0 = j * 128 + half * 64;
       uint32_t pk[32];
+      uint32_t pm[MAT ? 32 : 1];  // MAT: softmax_out pairs
 #pragma unroll
       for (int i = 0; i < 64; i += 2) {
-        float p2[2];
+        float p2[2], pn[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int e = i + u;
           const float sv = __uint_as_float(e < 32 ? r0[e] : r1[e - 32]);
           const uint32_t word = e < 32 ? wcur.x : wcur.y;
           const bool keep = (word >> (e & 31)) & 1u;
-          float p = ex2(sv * sl2 - mm) * scale_p;
-          if (!full && (k0 + e >= S || (CAUSAL && k0 + e > qr))) p = 0.f;
+          float p;
+          if constexpr (MAT) {
+            pn[u] = ex2(sv * sl2 - mm) * inv_l;
+            if (!full && (k0 + e >= S || (CAUSAL && k0 + e > qr))) pn[u] = 0.f;
+            p = pn[u] * a.drop.inv_keep;
+          } else {
+            p = ex2(sv * sl2 - mm) * scale_p;
+            if (!full && (k0 + e >= S || (CAUSAL && k0 + e > qr))) p = 0.f;
+          }
           p2[u] = keep ? p : 0.f;
         }
         pk[i >> 1] = pack_bf16(p2[0], p2[1]);
+        if constexpr (MAT) pm[i >> 1] = pack_bf16(pn[0], pn[1]);
+      }
+      if constexpr (MAT) {  // S % 64 == 0 (dispatcher): a half-tile is all in or all out
+        if (qr < S && k0 < S) {
+          const int64_t mi = (brow + qr) * (int64_t)S + k0;
+          uint4* smo = reinterpret_cast<uint4*>(static_cast<bf16*>(a.sm) + mi);
+          uint4* sdo = reinterpret_cast<uint4*>(static_cast<bf16*>(a.sd) + mi);
+          uint4* mko = reinterpret_cast<uint4*>(a.mask + mi);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            smo[u] = make_uint4(pm[4 * u], pm[4 * u + 1], pm[4 * u + 2], pm[4 * u + 3]);
+            sdo[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          }
+          const uint32_t wb[2] = {wcur.x, wcur.y};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {  // 16 keys -> 16 mask bytes
+            uint32_t q4[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const uint32_t bits = (wb[u >> 1] >> (16 * (u & 1) + 4 * v)) & 0xFu;
+              q4[v] = (bits & 1u) | ((bits & 2u) << 7) | ((bits & 4u) << 14) | ((bits & 8u) << 21);
+            }
+            mko[u] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
+          }
+        }
       }
       uint8_t* prow = Ps + pb * Cfg::P_BYTES + row * 128;
       // this half's keys = logical 16 B chunks 8*half .. 8*half+7 = atom `half`, swizzled by row
@@ -380,35 +418,48 @@ CUtensorMap attn_seq_map(const void* ptr, int64_t width, int64_t b, int64_t s, i
 
 namespace {
 
-template <int HD, bool CAUSAL>
+template <int HD, bool CAUSAL, bool MAT>
 void launch_fwd_umma(const AttnArgs& a, cudaStream_t st) {
   using Cfg = FwdCfg<HD>;
   static bool once = [] {
-    SPL_CUDA(cudaFuncSetAttribute(fa_fwd_umma<HD, CAUSAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SPL_CUDA(cudaFuncSetAttribute(fa_fwd_umma<HD, CAUSAL, MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   Cfg::SMEM));
     return true;
   }();
   (void)once;
   const CUtensorMap mq = attn_seq_map(a.qkv, a.ld, a.b, a.s, a.ld, 128);
   dim3 grid((unsigned)((a.s + 127) / 128), (unsigned)(a.lh * a.b));
-  fa_fwd_umma<HD, CAUSAL><<<grid, 320, Cfg::SMEM, st>>>(mq, a);
+  fa_fwd_umma<HD, CAUSAL, MAT><<<grid, 320, Cfg::SMEM, st>>>(mq, a);
   SPL_CHECK_LAUNCH();
+}
+template <int HD>
+void launch_fwd_umma_hd(const AttnArgs& a, cudaStream_t st) {
+  if (a.sm != nullptr) {
+    if (a.causal) launch_fwd_umma<HD, true, true>(a, st); else launch_fwd_umma<HD, false, true>(a, st);
+  } else {
+    if (a.causal) launch_fwd_umma<HD, true, false>(a, st); else launch_fwd_umma<HD, false, false>(a, st);
+  }
 }
 
 }  // namespace
 
 bool attn_fwd_umma_supported(const AttnArgs& a) {
   const bool hd_ok = a.hd == 64 || a.hd == 96 || a.hd == 128;
-  return hd_ok && a.sm == nullptr && a.lse != nullptr && a.ld % 8 == 0 && a.ldo % 8 == 0 &&
+  const bool regime_ok = a.sm == nullptr
+                             ? a.lse != nullptr
+                             : (a.mask != nullptr && a.sd != nullptr && a.s % 64 == 0 &&
+                                ((uintptr_t)a.sm & 15) == 0 && ((uintptr_t)a.sd & 15) == 0 &&
+                                ((uintptr_t)a.mask & 15) == 0);
+  return hd_ok && regime_ok && a.ld % 8 == 0 && a.ldo % 8 == 0 &&
          ((uintptr_t)a.qkv & 15) == 0 && ((uintptr_t)a.o & 15) == 0 &&
          (a.keepbits != nullptr || a.drop.thresh == 0) && a.s < (1 << 30);
 }
 
 void attn_fwd_umma(const AttnArgs& a, cudaStream_t st) {
   switch (a.hd) {
-    case 64: return a.causal ? launch_fwd_umma<64, true>(a, st) : launch_fwd_umma<64, false>(a, st);
-    case 96: return a.causal ? launch_fwd_umma<96, true>(a, st) : launch_fwd_umma<96, false>(a, st);
-    case 128: return a.causal ? launch_fwd_umma<128, true>(a, st) : launch_fwd_umma<128, false>(a, st);
+    case 64: return launch_fwd_umma_hd<64>(a, st);
+    case 96: return launch_fwd_umma_hd<96>(a, st);
+    case 128: return launch_fwd_umma_hd<128>(a, st);
     default: raise(3, "attn_fwd_umma: unsupported head_dim");
   }
 }

@@ -20,6 +20,20 @@
 namespace spl::k {
 
 CUtensorMap attn_seq_map(const void* ptr, int64_t width, int64_t b, int64_t s, int64_t ld, int rows);
+using EncodeFnB = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeFnB encode_fn_bwd() {
+  static EncodeFnB fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SPL_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (p == nullptr || q != cudaDriverEntryPointSuccess) raise(3, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<EncodeFnB>(p);
+  }();
+  return fn;
+}
 
 namespace {
 
@@ -50,19 +64,44 @@ struct BwdCfg {
 // =====================================================================================
 // dK, dV (+ keep bits)
 // =====================================================================================
-template <int HD, bool CAUSAL>
+// STORED (no-recompute regime): Sᵀ is not recomputed; P = softmax_out and the dropout mask
+// of each [64 queries x 128 keys] block come from the stored interior by TMA (2 stages), and
+// P̃ = P·mask/(1-p) — the stored softmax_dropout_out by its definition (block.cpp:144-147) —
+// is formed in registers, so the backward reads 3 of the 5 stored bytes per element.
+template <int HD>
+struct DkdvLayout {
+  using C = BwdCfg<HD>;
+  static constexpr int SMT = 64 * 128 * 2, MKT = 64 * 128;  // stored P / mask tiles
+  template <bool STORED>
+  struct L {
+    static constexpr int K_OFF = 0;
+    static constexpr int V_OFF = STORED ? 0 : C::T128;
+    static constexpr int QD_OFF = V_OFF + C::T128;
+    static constexpr int W_OFF = QD_OFF + 4 * C::T64;
+    static constexpr int SMM_OFF = W_OFF + 4 * C::W_BYTES;
+    static constexpr int LD_OFF = SMM_OFF + (STORED ? 2 * (SMT + MKT) : 0);
+    static constexpr int BAR_OFF = LD_OFF + 2 * 2 * 64 * 4;
+    static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  };
+};
+
+template <int HD, bool CAUSAL, bool STORED>
 __global__ void __launch_bounds__(320, 1)
     fa_bwd_dkdv_umma(const __grid_constant__ CUtensorMap map_kv,  // qkv, 128-row boxes
                      const __grid_constant__ CUtensorMap map_q,   // qkv, 64-row boxes
                      const __grid_constant__ CUtensorMap map_do,  // dO, 64-row boxes
+                     const __grid_constant__ CUtensorMap map_sm,  // STORED: P, box {128 k, 64 q}
+                     const __grid_constant__ CUtensorMap map_mk,  // STORED: mask, same box
                      AttnArgs a,
                      bf16* __restrict__ dqkv, const float* __restrict__ delta) {
   using C = BwdCfg<HD>;
-  // smem: K, V (128 rows) | 2 x (Q, dO) (64 rows) | 2 x (P̃ᵀ, dSᵀ) (128 x 64) | lse/delta | bars
-  constexpr int K_OFF = 0, V_OFF = C::T128, QD_OFF = 2 * C::T128;
-  constexpr int W_OFF = QD_OFF + 4 * C::T64;
-  constexpr int LD_OFF = W_OFF + 4 * C::W_BYTES;  // [2 stages][2][64] floats
-  constexpr int BAR_OFF = LD_OFF + 2 * 2 * 64 * 4;
+  using Lay = typename DkdvLayout<HD>::template L<STORED>;
+  constexpr int SMT = DkdvLayout<HD>::SMT, MKT = DkdvLayout<HD>::MKT;
+  // smem: K, V (128 rows) | 2 x (Q, dO) (64 rows) | 2 x (P̃ᵀ, dSᵀ) (128 x 64) | [2 x (P, mask)]
+  //       | lse/delta | bars        (STORED: no K)
+  constexpr int K_OFF = Lay::K_OFF, V_OFF = Lay::V_OFF, QD_OFF = Lay::QD_OFF;
+  constexpr int W_OFF = Lay::W_OFF, SMM_OFF = Lay::SMM_OFF;
+  constexpr int BAR_OFF = Lay::BAR_OFF;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
@@ -109,10 +148,10 @@ __global__ void __launch_bounds__(320, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(kv_full, 2 * C::T128);
+      mbar_expect_tx(kv_full, (STORED ? 1 : 2) * C::T128);
 #pragma unroll
       for (int at = 0; at < C::ATOMS; ++at) {
-        tma_load_3d(smem + K_OFF + at * C::A128, &map_kv, kv_full, kcol + 64 * at, bj, k0);
+        if (!STORED) tma_load_3d(smem + K_OFF + at * C::A128, &map_kv, kv_full, kcol + 64 * at, bj, k0);
         tma_load_3d(smem + V_OFF + at * C::A128, &map_kv, kv_full, vcol + 64 * at, bj, k0);
       }
       for (int it = 0; it < nq; ++it) {
@@ -121,11 +160,16 @@ __global__ void __launch_bounds__(320, 1)
         uint8_t* Qt = smem + QD_OFF + st * 2 * C::T64;
         uint8_t* Dt = Qt + C::T64;
         const int qb = q_start + it * 64;
-        mbar_expect_tx(&qd_full[st], 2 * C::T64);
+        mbar_expect_tx(&qd_full[st], 2 * C::T64 + (STORED ? SMT + MKT : 0));
 #pragma unroll
         for (int at = 0; at < C::ATOMS; ++at) {
           tma_load_3d(Qt + at * C::A64, &map_q, &qd_full[st], qcol + 64 * at, bj, qb);
           tma_load_3d(Dt + at * C::A64, &map_do, &qd_full[st], dcol + 64 * at, bj, qb);
+        }
+        if (STORED) {
+          uint8_t* St = smem + SMM_OFF + st * (SMT + MKT);
+          tma_load_3d(St, &map_sm, &qd_full[st], k0, qb, (int)blockIdx.y);
+          tma_load_3d(St + SMT, &map_mk, &qd_full[st], k0, qb, (int)blockIdx.y);
         }
       }
     }
@@ -145,8 +189,9 @@ __global__ void __launch_bounds__(320, 1)
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t oa = (kk >> 2) * C::A128 + (kk & 3) * 32;
           const uint32_t ob = (kk >> 2) * C::A64 + (kk & 3) * 32;
-          umma_bf16(tmem + st * 64, smem_desc(ka + oa, 16, 1024), smem_desc(qb + ob, 16, 1024),
-                    idesc_sd, kk > 0 ? 1u : 0u);
+          if (!STORED)
+            umma_bf16(tmem + st * 64, smem_desc(ka + oa, 16, 1024), smem_desc(qb + ob, 16, 1024),
+                      idesc_sd, kk > 0 ? 1u : 0u);
           umma_bf16(tmem + 128 + st * 64, smem_desc(va + oa, 16, 1024),
                     smem_desc(db + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
         }
@@ -190,19 +235,22 @@ __global__ void __launch_bounds__(320, 1)
       const int qb = q_start + it * 64;
       // lse (log2 domain), rowdot and the keep-bit word (q, this warp's 32 keys) of this half's
       // 32 queries: lane e holds query q0h + e
-      float lse_l, dl_l;
-      uint32_t kw_l;
+      float lse_l = 0.f, dl_l;
+      uint32_t kw_l = 0u;
       {
         const int q = qb + 32 * half + lane;
-        lse_l = q < S ? a.lse[brow + q] * kLog2e : INFINITY;
         dl_l = q < S ? delta[brow + q] : 0.f;
-        kw_l = !drop_on ? 0xffffffffu
-               : (q < S && (k0 >> 5) + qd < W) ? kbits[(brow + q) * W + (k0 >> 5) + qd] : 0u;
+        if (!STORED) {
+          lse_l = q < S ? a.lse[brow + q] * kLog2e : INFINITY;
+          kw_l = !drop_on ? 0xffffffffu
+                 : (q < S && (k0 >> 5) + qd < W) ? kbits[(brow + q) * W + (k0 >> 5) + qd] : 0u;
+        }
       }
+      if (STORED) mbar_wait(&qd_full[st], (it >> 1) & 1);  // stored P / mask tiles landed
       mbar_wait(&sd_full[st], (it >> 1) & 1);
       tc_fence_after();
       uint32_t rs[32], rp[32];
-      tmem_ld32_nw(tl + st * 64 + half * 32, rs);
+      if (!STORED) tmem_ld32_nw(tl + st * 64 + half * 32, rs);
       tmem_ld32_nw(tl + 128 + st * 64 + half * 32, rp);
       tmem_wait();
       tc_fence_before();
@@ -219,10 +267,20 @@ __global__ void __launch_bounds__(320, 1)
           const int e = i + u;
           const int q = q0h + e;
           const bool valid = q < S && key < S && !(CAUSAL && key > q);
-          bool keep = (__shfl_sync(0xffffffffu, kw_l, e) >> lane) & 1u;
-          const float lqe = __shfl_sync(0xffffffffu, lse_l, e);
           const float dqe = __shfl_sync(0xffffffffu, dl_l, e);
-          const float p = valid ? ex2(__uint_as_float(rs[e]) * sl2 - lqe) : 0.f;
+          bool keep;
+          float p;
+          if constexpr (STORED) {
+            // [64 q][128 k] tiles: this warp's 32 keys of query row 32*half + e
+            const uint8_t* St = smem + SMM_OFF + st * (SMT + MKT);
+            const int qi = 32 * half + e;
+            p = valid ? __bfloat162float(reinterpret_cast<const bf16*>(St)[qi * 128 + row]) : 0.f;
+            keep = St[SMT + qi * 128 + row] != 0;
+          } else {
+            keep = (__shfl_sync(0xffffffffu, kw_l, e) >> lane) & 1u;
+            const float lqe = __shfl_sync(0xffffffffu, lse_l, e);
+            p = valid ? ex2(__uint_as_float(rs[e]) * sl2 - lqe) : 0.f;
+          }
           keep = keep && valid;
           pv[u] = keep ? p * inv_keep : 0.f;
           const float dpk = keep ? __uint_as_float(rp[e]) * inv_keep : 0.f;
@@ -279,18 +337,38 @@ __global__ void __launch_bounds__(320, 1)
 // =====================================================================================
 // dQ
 // =====================================================================================
-template <int HD, bool CAUSAL>
+// STORED: S is not recomputed; P and the mask of each [128 queries x 64 keys] block come from
+// the stored interior by TMA (P with the 128-byte swizzle, read conflict-free by row).
+template <int HD>
+struct DqLayout {
+  using C = BwdCfg<HD>;
+  static constexpr int SMT = 128 * 64 * 2, MKT = 128 * 64;
+  template <bool STORED>
+  struct L {
+    static constexpr int Q_OFF = 0, D_OFF = C::T128, KV_OFF = 2 * C::T128;
+    static constexpr int W_OFF = KV_OFF + 4 * C::T64;
+    static constexpr int SMM_OFF = W_OFF + 2 * C::W_BYTES;
+    static constexpr int BAR_OFF = SMM_OFF + (STORED ? 2 * (SMT + MKT) : 0);
+    static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  };
+};
+
+template <int HD, bool CAUSAL, bool STORED>
 __global__ void __launch_bounds__(320, 1)
     fa_bwd_dq_umma(const __grid_constant__ CUtensorMap map_q,   // qkv, 128-row boxes
                    const __grid_constant__ CUtensorMap map_do,  // dO, 128-row boxes
                    const __grid_constant__ CUtensorMap map_kv,  // qkv, 64-row boxes
+                   const __grid_constant__ CUtensorMap map_sm,  // STORED: P, box {64 k, 128 q}, SW128
+                   const __grid_constant__ CUtensorMap map_mk,  // STORED: mask, same box
                    AttnArgs a,
                    bf16* __restrict__ dqkv, const float* __restrict__ delta) {
   using C = BwdCfg<HD>;
-  // smem: Q, dO (128 rows) | 2 x (K, V) (64 rows) | 2 x dS (128 x 64) | bars
-  constexpr int Q_OFF = 0, D_OFF = C::T128, KV_OFF = 2 * C::T128;
-  constexpr int W_OFF = KV_OFF + 4 * C::T64;
-  constexpr int BAR_OFF = W_OFF + 2 * C::W_BYTES;
+  using Lay = typename DqLayout<HD>::template L<STORED>;
+  constexpr int SMT = DqLayout<HD>::SMT, MKT = DqLayout<HD>::MKT;
+  // smem: Q, dO (128 rows) | 2 x (K, V) (64 rows) | 2 x dS (128 x 64) | [2 x (P, mask)] | bars
+  constexpr int Q_OFF = Lay::Q_OFF, D_OFF = Lay::D_OFF, KV_OFF = Lay::KV_OFF;
+  constexpr int W_OFF = Lay::W_OFF, SMM_OFF = Lay::SMM_OFF;
+  constexpr int BAR_OFF = Lay::BAR_OFF;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
@@ -336,10 +414,10 @@ __global__ void __launch_bounds__(320, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(q_full, 2 * C::T128);
+      mbar_expect_tx(q_full, (STORED ? 1 : 2) * C::T128);
 #pragma unroll
       for (int at = 0; at < C::ATOMS; ++at) {
-        tma_load_3d(smem + Q_OFF + at * C::A128, &map_q, q_full, qcol + 64 * at, bj, q0);
+        if (!STORED) tma_load_3d(smem + Q_OFF + at * C::A128, &map_q, q_full, qcol + 64 * at, bj, q0);
         tma_load_3d(smem + D_OFF + at * C::A128, &map_do, q_full, dcol + 64 * at, bj, q0);
       }
       for (int it = 0; it < nkv; ++it) {
@@ -347,11 +425,16 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(&kv_empty[st], ((it >> 1) & 1) ^ 1);
         uint8_t* Kt = smem + KV_OFF + st * 2 * C::T64;
         uint8_t* Vt = Kt + C::T64;
-        mbar_expect_tx(&kv_full[st], 2 * C::T64);
+        mbar_expect_tx(&kv_full[st], 2 * C::T64 + (STORED ? SMT + MKT : 0));
 #pragma unroll
         for (int at = 0; at < C::ATOMS; ++at) {
           tma_load_3d(Kt + at * C::A64, &map_kv, &kv_full[st], kcol + 64 * at, bj, it * 64);
           tma_load_3d(Vt + at * C::A64, &map_kv, &kv_full[st], vcol + 64 * at, bj, it * 64);
+        }
+        if (STORED) {
+          uint8_t* St = smem + SMM_OFF + st * (SMT + MKT);
+          tma_load_3d(St, &map_sm, &kv_full[st], it * 64, q0, (int)blockIdx.y);
+          tma_load_3d(St + SMT, &map_mk, &kv_full[st], it * 64, q0, (int)blockIdx.y);
         }
       }
     }
@@ -371,8 +454,9 @@ __global__ void __launch_bounds__(320, 1)
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t oa = (kk >> 2) * C::A128 + (kk & 3) * 32;
           const uint32_t ob = (kk >> 2) * C::A64 + (kk & 3) * 32;
-          umma_bf16(tmem + st * 64, smem_desc(qa + oa, 16, 1024), smem_desc(kb + ob, 16, 1024),
-                    idesc_sd, kk > 0 ? 1u : 0u);
+          if (!STORED)
+            umma_bf16(tmem + st * 64, smem_desc(qa + oa, 16, 1024), smem_desc(kb + ob, 16, 1024),
+                      idesc_sd, kk > 0 ? 1u : 0u);
           umma_bf16(tmem + 128 + st * 64, smem_desc(da + oa, 16, 1024),
                     smem_desc(vb + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
         }
@@ -405,17 +489,35 @@ __global__ void __launch_bounds__(320, 1)
     const float inv_keep = a.drop.inv_keep;
     const bool drop_on = a.drop.thresh != 0;
     const int W = (S + 31) / 32;
-    const float lse2 = qr < S ? a.lse[brow + qr] * kLog2e : INFINITY;
+    const float lse2 = (!STORED && qr < S) ? a.lse[brow + qr] * kLog2e : INFINITY;
     const float dl = qr < S ? delta[brow + qr] : 0.f;
-    const uint32_t* kb = a.keepbits + (brow + (qr < S ? qr : 0)) * W;
+    const uint32_t* kb = STORED ? nullptr : a.keepbits + (brow + (qr < S ? qr : 0)) * W;
     for (int it = 0; it < nkv; ++it) {
       const int st = it & 1;
       const int kc0 = it * 64 + 32 * half;
-      const uint32_t word = !drop_on ? 0xffffffffu : (qr < S && kc0 < S) ? kb[kc0 >> 5] : 0u;
+      uint32_t word = 0xffffffffu;
+      uint32_t pst[16];  // STORED: this half's 32 stored probabilities (bf16 pairs)
+      if constexpr (STORED) {
+        mbar_wait(&kv_full[st], (it >> 1) & 1);  // stored P / mask tiles landed
+        const uint8_t* St = smem + SMM_OFF + st * (SMT + MKT);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint4 v = *reinterpret_cast<const uint4*>(St + row * 128 + (((4 * half + u) ^ (row & 7)) * 16));
+          pst[4 * u] = v.x; pst[4 * u + 1] = v.y; pst[4 * u + 2] = v.z; pst[4 * u + 3] = v.w;
+        }
+        const uint4 m0 = *reinterpret_cast<const uint4*>(St + SMT + row * 64 + 32 * half);
+        const uint4 m1 = *reinterpret_cast<const uint4*>(St + SMT + row * 64 + 32 * half + 16);
+        const uint32_t mw[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+        word = 0u;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) word |= ((mw[e >> 2] >> (8 * (e & 3))) & 1u) << e;
+      } else {
+        word = !drop_on ? 0xffffffffu : (qr < S && kc0 < S) ? kb[kc0 >> 5] : 0u;
+      }
       mbar_wait(&sd_full[st], (it >> 1) & 1);
       tc_fence_after();
       uint32_t rs[32], rp[32];
-      tmem_ld32_nw(tl + st * 64 + half * 32, rs);
+      if (!STORED) tmem_ld32_nw(tl + st * 64 + half * 32, rs);
       tmem_ld32_nw(tl + 128 + st * 64 + half * 32, rp);
       tmem_wait();
       tc_fence_before();
@@ -431,7 +533,11 @@ __global__ void __launch_bounds__(320, 1)
         for (int u = 0; u < 2; ++u) {
           const int e = i + u;
           const bool keep = (word >> e) & 1u;
-          float p = ex2(__uint_as_float(rs[e]) * sl2 - lse2);
+          float p;
+          if constexpr (STORED)
+            p = __uint_as_float((e & 1) ? (pst[e >> 1] & 0xffff0000u) : (pst[e >> 1] << 16));
+          else
+            p = ex2(__uint_as_float(rs[e]) * sl2 - lse2);
           if (!full && (kc0 + e >= S || qr >= S || (CAUSAL && kc0 + e > qr))) p = 0.f;
           const float dpk = keep ? __uint_as_float(rp[e]) * inv_keep : 0.f;
           dv[u] = p * (dpk - dl);
@@ -473,15 +579,35 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
-template <int HD, bool CAUSAL>
+// 3-D map over a stored interior {nblk = lh*b, s, s} (row = query, contiguous keys):
+// dims {s (key), s (query), nblk}; box {box_k, box_q, 1}.
+CUtensorMap interior_map(const void* ptr, bool u8, int64_t s, int64_t nblk, int box_k, int box_q,
+                         bool sw128) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof m);
+  const int64_t es = u8 ? 1 : 2;
+  const cuuint64_t dims[3] = {(cuuint64_t)s, (cuuint64_t)s, (cuuint64_t)nblk};
+  const cuuint64_t strides[2] = {(cuuint64_t)(s * es), (cuuint64_t)(s * s * es)};
+  const cuuint32_t box[3] = {(cuuint32_t)box_k, (cuuint32_t)box_q, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn_bwd()(&m, u8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                               3, const_cast<void*>(ptr), dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(3, "cuTensorMapEncodeTiled (interior) failed: " + std::to_string((int)r));
+  return m;
+}
+
+template <int HD, bool CAUSAL, bool STORED>
 void launch_bwd_umma(const AttnArgs& a, const bf16* dout, bf16* dqkv, const float* delta,
                      cudaStream_t st) {
-  using C = BwdCfg<HD>;
-  constexpr int smem_kv = 2 * C::T128 + 4 * C::T64 + 4 * C::W_BYTES + 2 * 2 * 64 * 4 + 256 + 1024;
-  constexpr int smem_q = 2 * C::T128 + 4 * C::T64 + 2 * C::W_BYTES + 256 + 1024;
+  constexpr int smem_kv = DkdvLayout<HD>::template L<STORED>::SMEM;
+  constexpr int smem_q = DqLayout<HD>::template L<STORED>::SMEM;
+  static_assert(smem_kv <= 232448 && smem_q <= 232448, "attention backward: smem over the limit");
   static bool once = [] {
-    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_dkdv_umma<HD, CAUSAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv));
-    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_dq_umma<HD, CAUSAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q));
+    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_dkdv_umma<HD, CAUSAL, STORED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv));
+    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_dq_umma<HD, CAUSAL, STORED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q));
     return true;
   }();
   (void)once;
@@ -489,11 +615,19 @@ void launch_bwd_umma(const AttnArgs& a, const bf16* dout, bf16* dqkv, const floa
   const CUtensorMap m64 = attn_seq_map(a.qkv, a.ld, a.b, a.s, a.ld, 64);
   const CUtensorMap d64 = attn_seq_map(dout, a.ldo, a.b, a.s, a.ldo, 64);
   const CUtensorMap d128 = attn_seq_map(dout, a.ldo, a.b, a.s, a.ldo, 128);
+  CUtensorMap skv = m128, mkv = m128, sq = m128, mq = m128;  // unused unless STORED
+  if (STORED) {
+    const int64_t nblk = a.lh * a.b;
+    skv = interior_map(a.sm, false, a.s, nblk, 128, 64, false);
+    mkv = interior_map(a.mask, true, a.s, nblk, 128, 64, false);
+    sq = interior_map(a.sm, false, a.s, nblk, 64, 128, true);
+    mq = interior_map(a.mask, true, a.s, nblk, 64, 128, false);
+  }
   dim3 grid((unsigned)((a.s + 127) / 128), (unsigned)(a.lh * a.b));
   // dK/dV: K,V 128-row boxes + Q 64-row boxes from the same map family
-  fa_bwd_dkdv_umma<HD, CAUSAL><<<grid, 320, smem_kv, st>>>(m128, m64, d64, a, dqkv, delta);
+  fa_bwd_dkdv_umma<HD, CAUSAL, STORED><<<grid, 320, smem_kv, st>>>(m128, m64, d64, skv, mkv, a, dqkv, delta);
   SPL_CHECK_LAUNCH();
-  fa_bwd_dq_umma<HD, CAUSAL><<<grid, 320, smem_q, st>>>(m128, d128, m64, a, dqkv, delta);
+  fa_bwd_dq_umma<HD, CAUSAL, STORED><<<grid, 320, smem_q, st>>>(m128, d128, m64, sq, mq, a, dqkv, delta);
   SPL_CHECK_LAUNCH();
 }
 
@@ -501,21 +635,32 @@ void launch_bwd_umma(const AttnArgs& a, const bf16* dout, bf16* dqkv, const floa
 
 bool attn_bwd_umma_supported(const AttnArgs& a) {
   const bool hd_ok = a.hd == 64 || a.hd == 96 || a.hd == 128;
-  return hd_ok && a.sm == nullptr && a.lse != nullptr && a.ld % 8 == 0 && a.ldo % 8 == 0 &&
-         ((uintptr_t)a.qkv & 15) == 0 && ((uintptr_t)a.o & 15) == 0 &&
-         (a.keepbits != nullptr || a.drop.thresh == 0) && a.s < (1 << 30);
+  const bool regime_ok =
+      a.sm == nullptr ? (a.lse != nullptr && (a.keepbits != nullptr || a.drop.thresh == 0))
+                      : (a.mask != nullptr && a.s % 64 == 0 && ((uintptr_t)a.sm & 15) == 0 &&
+                         ((uintptr_t)a.mask & 15) == 0);
+  return hd_ok && regime_ok && a.ld % 8 == 0 && a.ldo % 8 == 0 && ((uintptr_t)a.qkv & 15) == 0 &&
+         ((uintptr_t)a.o & 15) == 0 && a.s < (1 << 30);
 }
 
 void attn_bwd_umma(const AttnArgs& a, const void* dout, void* dqkv, const float* delta,
                    cudaStream_t st) {
   const bf16* d = static_cast<const bf16*>(dout);
   bf16* g = static_cast<bf16*>(dqkv);
+#define SPL_BWD_CASE(HDX)                                                                        \
+  case HDX:                                                                                      \
+    if (a.sm != nullptr)                                                                         \
+      return a.causal ? launch_bwd_umma<HDX, true, true>(a, d, g, delta, st)                     \
+                      : launch_bwd_umma<HDX, false, true>(a, d, g, delta, st);                   \
+    return a.causal ? launch_bwd_umma<HDX, true, false>(a, d, g, delta, st)                      \
+                    : launch_bwd_umma<HDX, false, false>(a, d, g, delta, st);
   switch (a.hd) {
-    case 64: return a.causal ? launch_bwd_umma<64, true>(a, d, g, delta, st) : launch_bwd_umma<64, false>(a, d, g, delta, st);
-    case 96: return a.causal ? launch_bwd_umma<96, true>(a, d, g, delta, st) : launch_bwd_umma<96, false>(a, d, g, delta, st);
-    case 128: return a.causal ? launch_bwd_umma<128, true>(a, d, g, delta, st) : launch_bwd_umma<128, false>(a, d, g, delta, st);
+    SPL_BWD_CASE(64)
+    SPL_BWD_CASE(96)
+    SPL_BWD_CASE(128)
     default: raise(3, "attn_bwd_umma: unsupported head_dim");
   }
+#undef SPL_BWD_CASE
 }
 
 }  // namespace spl::k
