@@ -107,11 +107,10 @@ struct Rng {
 // high half of (row_base + key) and of the first xor-shift are loop-invariant (the carry out of
 // the low half is checked once per word), so a key costs ~40 integer instructions.
 // The hash is integer work split between the ALU pipe (LOP3/SHF/ISETP/IADD3) and the FMA-heavy
-// pipe (IMAD*). A 64-bit xor-shift is either 4 ALU ops (funnel shifts) or 2 ALU + 3 IMAD ops
-// (shifts as multiplies by 2^(32-k): IMAD.HI for >>, IMAD for <<). Measured (ncu): all-ALU
-// shifts leave the ALU pipe the bound; shifting three of them to IMAD saturates fmaheavy (90%)
-// instead; two in IMAD form is the balance point. The multipliers come in through the kernel
-// parameters so ptxas cannot turn the multiplies back into shifts.
+// pipe (IMAD*: the 64-bit constant multiplies). A 64-bit xor-shift can be 4 ALU ops (funnel
+// shifts) or 2 ALU + 3 IMAD ops (multiplies by 2^(32-k)); with three shifts in IMAD form
+// fmaheavy ran at 89% (ncu) and the all-funnel-shift form is 7% faster (tools/micro/
+// bench_rng2.cu), so keep_fast uses funnel shifts throughout.
 
 __global__ void __launch_bounds__(256) keep_bits_k(DropKey key, int64_t head_offset, int lh,
                                                    int b, int s, int W, int causal,

@@ -6,10 +6,14 @@
 //   warp 1      TMEM allocator + single-thread MMA issuer
 //   warps 2..9  softmax: query row = TMEM lane (warp w reads lanes 32*(w%4)..); warps 2-5 take
 //               keys 0-63 of each tile, warps 6-9 keys 64-127 (row statistics merged via smem)
-// Two passes over the keys (no O rescaling, everything in TMEM stays exact):
-//   pass 1: S = Q·Kᵀ -> row max m and sum l (online, log2 domain)
-//   pass 2: S = Q·Kᵀ -> P̃ = exp2(S·c - m)/l · keep/(1-p) (keep bits from attn_keep_bits)
-//           written as bf16 to smem in the UMMA K-major SW128 layout -> O += P̃·V in TMEM
+// Selective / full regimes: ONE pass over the keys with a lazily rescaled O (online softmax):
+//   S = Q·Kᵀ -> row max over both column halves (exchanged through smem per tile); the
+//   reference point m_used moves only when the max grows by more than 2^8, and then O (TMEM)
+//   and l are rescaled once PV of the previous tile has completed (rare after the first tile);
+//   P̃ = exp2(S·c - m_used)·keep (≤ 2^8, bf16) -> smem (UMMA K-major SW128) -> O += P̃·V;
+//   epilogue O · (1/(1-p))/l, LSE = m_used + log2 l.
+// No-recompute regime (MAT): two passes (pass 1 row max/sum, pass 2 normalised P), because the
+//   stored softmax_out must be normalised when it is written.
 // TMEM: S double-buffered (2 × 128 fp32 columns) + O (HD columns). MMAs of tile j+1 overlap
 // the softmax of tile j. SMEM: Q 32 KB, 2 × (K, V) 128 KB, 2 × P 64 KB.
 #include <cstring>
@@ -51,7 +55,8 @@ struct FwdCfg {
   // [2 halves][128 rows] (m, l) exchanged between pass 1 and pass 2, when the P buffers are
   // not in use yet (smem is at the 227 KB limit for HD = 96/128)
   static constexpr int STAT_OFF = P_OFF;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int XCH_OFF = BAR_OFF + 256;  // [2 halves][128 rows] floats (single pass)
+  static constexpr int SMEM = XCH_OFF + 1024 + 1024;
   static constexpr int O_COL = 256;  // O accumulator columns [256, 256 + HD)
 };
 
@@ -78,6 +83,7 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* p_free = bar + 11;   // [2]
   uint64_t* o_full = bar + 13;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t* o_done = bar + 15;   // one phase per P̃·V MMA (single pass: gates O rescaling)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q0 = blockIdx.x * 128;
@@ -99,6 +105,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&p_free[i], 1);
     }
     mbar_init(o_full, 1);
+    mbar_init(o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_qkv) : "memory");
   }
@@ -116,17 +123,19 @@ __global__ void __launch_bounds__(320, 1)
       for (int at = 0; at < Cfg::ATOMS; ++at)
         tma_load_3d(Qs + at * kAtomBytes, &map_qkv, q_full, qcol + 64 * at, bj, q0);
       int it = 0;
-      for (int pass = 0; pass < 2; ++pass) {
+      constexpr int PASSES = MAT ? 2 : 1;
+      for (int pass = 0; pass < PASSES; ++pass) {
+        const bool with_v = pass == PASSES - 1;
         for (int j = 0; j < nkv; ++j, ++it) {
           const int st = it & 1;
           mbar_wait(&kv_empty[st], ((it >> 1) & 1) ^ 1);
           uint8_t* Kt = KVs + st * 2 * Cfg::TILE;
           uint8_t* Vt = Kt + Cfg::TILE;
-          mbar_expect_tx(&kv_full[st], (pass + 1) * Cfg::TILE);
+          mbar_expect_tx(&kv_full[st], (with_v ? 2 : 1) * Cfg::TILE);
 #pragma unroll
           for (int at = 0; at < Cfg::ATOMS; ++at)
             tma_load_3d(Kt + at * kAtomBytes, &map_qkv, &kv_full[st], kcol + 64 * at, bj, j * 128);
-          if (pass == 1) {
+          if (with_v) {
 #pragma unroll
             for (int at = 0; at < Cfg::ATOMS; ++at)
               tma_load_3d(Vt + at * kAtomBytes, &map_qkv, &kv_full[st], vcol + 64 * at, bj, j * 128);
@@ -158,10 +167,11 @@ __global__ void __launch_bounds__(320, 1)
         umma_commit(&s_full[sb]);
         ++sc;
       };
-      // pass 1
-      for (int j = 0; j < nkv; ++j, ++it) {
-        issue_s(it);
-        umma_commit(&kv_empty[it & 1]);
+      if constexpr (MAT) {  // pass 1 (statistics only)
+        for (int j = 0; j < nkv; ++j, ++it) {
+          issue_s(it);
+          umma_commit(&kv_empty[it & 1]);
+        }
       }
       // pass 2: S_{j+1} is issued before PV_j so the softmax of j+1 can start early
       const int base = it;
@@ -182,6 +192,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         umma_commit(&p_free[pb]);
         umma_commit(&kv_empty[st]);
+        umma_commit(o_done);
       }
       umma_commit(o_full);
     }
@@ -197,155 +208,276 @@ __global__ void __launch_bounds__(320, 1)
     const int W = (S + 31) / 32;
     const int64_t brow = ((int64_t)hl * a.b + bj) * a.s;
     const uint32_t* kbits = a.keepbits + (brow + (qr < S ? qr : 0)) * W;
-    float2* stat = reinterpret_cast<float2*>(smem + Cfg::STAT_OFF);
-    float m = -INFINITY, l = 0.f;
-    int sc = 0;
-    // a tile needs per-element masking only at the sequence tail or on the causal diagonal
-    auto tile_full = [&](int j) {
-      return j * 128 + 128 <= S && !(CAUSAL && j * 128 + 127 > q0);
-    };
-    // pass 1: statistics of this half's 64 columns
-    for (int j = 0; j < nkv; ++j, ++sc) {
-      const int sb = sc & 1;
-      mbar_wait(&s_full[sb], (sc >> 1) & 1);
-      tc_fence_after();
-      uint32_t r0[32], r1[32];
-      tmem_ld32_nw(tl + sb * 128 + half * 64, r0);
-      tmem_ld32_nw(tl + sb * 128 + half * 64 + 32, r1);
-      tmem_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[sb]);  // S buffer may be overwritten now
-      float v[64];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        v[i] = __uint_as_float(r0[i]) * sl2;
-        v[32 + i] = __uint_as_float(r1[i]) * sl2;
+    float m, l;
+    float oscale = 1.f;
+    if constexpr (MAT) {
+      float2* stat = reinterpret_cast<float2*>(smem + Cfg::STAT_OFF);
+      m = -INFINITY;
+      l = 0.f;
+      int sc = 0;
+      // a tile needs per-element masking only at the sequence tail or on the causal diagonal
+      auto tile_full = [&](int j) {
+        return j * 128 + 128 <= S && !(CAUSAL && j * 128 + 127 > q0);
+      };
+      // pass 1: statistics of this half's 64 columns
+      for (int j = 0; j < nkv; ++j, ++sc) {
+        const int sb = sc & 1;
+        mbar_wait(&s_full[sb], (sc >> 1) & 1);
+        tc_fence_after();
+        uint32_t r0[32], r1[32];
+        tmem_ld32_nw(tl + sb * 128 + half * 64, r0);
+        tmem_ld32_nw(tl + sb * 128 + half * 64 + 32, r1);
+        tmem_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[sb]);  // S buffer may be overwritten now
+        float v[64];
+  #pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          v[i] = __uint_as_float(r0[i]) * sl2;
+          v[32 + i] = __uint_as_float(r1[i]) * sl2;
+        }
+        if (!tile_full(j)) {
+          const int k0 = j * 128 + half * 64;
+  #pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (k0 + i >= S || (CAUSAL && k0 + i > qr)) v[i] = -INFINITY;
+        }
+        float cm = v[0];
+  #pragma unroll
+        for (int i = 1; i < 64; ++i) cm = fmaxf(cm, v[i]);
+        const float mn = fmaxf(m, cm);
+        if (mn != -INFINITY) {
+          float sum = 0.f;
+  #pragma unroll
+          for (int i = 0; i < 64; ++i) sum += ex2(v[i] - mn);
+          l = l * ex2(m - mn) + sum;
+          m = mn;
+        }
       }
-      if (!tile_full(j)) {
+      // merge the two halves' (m, l) of each row
+      stat[half * 128 + row] = make_float2(m, l);
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 softmax warps only
+      {
+        const float2 o = stat[(half ^ 1) * 128 + row];
+        const float mn = fmaxf(m, o.x);
+        if (mn != -INFINITY) {
+          l = (m == -INFINITY ? 0.f : l * ex2(m - mn)) + (o.x == -INFINITY ? 0.f : o.y * ex2(o.x - mn));
+          m = mn;
+        }
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // stats read before P overwrites them
+      const float scale_p = a.drop.inv_keep / l;  // 1/l and the dropout rescale folded
+      const float inv_l = 1.0f / l;
+      const float mm = m == -INFINITY ? 0.f : m;
+      // pass 2: probabilities -> P̃ (bf16, K-major SW128 in smem)
+      const int kw0 = half * 2;  // this half's first 32-key word within a tile
+      uint2 wnext = make_uint2(0xffffffffu, 0xffffffffu);
+      auto load_words = [&](int j) {
+        uint2 w = make_uint2(0xffffffffu, 0xffffffffu);
+        if (drop_on) {
+          const int wd = j * 4 + kw0;
+          w.x = (qr < S && wd < W) ? kbits[wd] : 0u;
+          w.y = (qr < S && wd + 1 < W) ? kbits[wd + 1] : 0u;
+        }
+        return w;
+      };
+      if (nkv > 0) wnext = load_words(0);
+      for (int j = 0; j < nkv; ++j, ++sc) {
+        const int sb = sc & 1, pb = j & 1;
+        const uint2 wcur = wnext;
+        if (j + 1 < nkv) wnext = load_words(j + 1);  // prefetch the next tile's keep bits
+        mbar_wait(&s_full[sb], (sc >> 1) & 1);
+        tc_fence_after();
+        uint32_t r0[32], r1[32];
+        tmem_ld32_nw(tl + sb * 128 + half * 64, r0);
+        tmem_ld32_nw(tl + sb * 128 + half * 64 + 32, r1);
+        tmem_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[sb]);
+        mbar_wait(&p_free[pb], ((j >> 1) & 1) ^ 1);
+        const bool full = tile_full(j);
         const int k0 = j * 128 + half * 64;
-#pragma unroll
-        for (int i = 0; i < 64; ++i)
-          if (k0 + i >= S || (CAUSAL && k0 + i > qr)) v[i] = -INFINITY;
-      }
-      float cm = v[0];
-#pragma unroll
-      for (int i = 1; i < 64; ++i) cm = fmaxf(cm, v[i]);
-      const float mn = fmaxf(m, cm);
-      if (mn != -INFINITY) {
-        float sum = 0.f;
-#pragma unroll
-        for (int i = 0; i < 64; ++i) sum += ex2(v[i] - mn);
-        l = l * ex2(m - mn) + sum;
-        m = mn;
-      }
-    }
-    // merge the two halves' (m, l) of each row
-    stat[half * 128 + row] = make_float2(m, l);
-    asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 softmax warps only
-    {
-      const float2 o = stat[(half ^ 1) * 128 + row];
-      const float mn = fmaxf(m, o.x);
-      if (mn != -INFINITY) {
-        l = (m == -INFINITY ? 0.f : l * ex2(m - mn)) + (o.x == -INFINITY ? 0.f : o.y * ex2(o.x - mn));
-        m = mn;
-      }
-    }
-    asm volatile("bar.sync 1, 256;" ::: "memory");  // stats read before P overwrites them
-    const float scale_p = a.drop.inv_keep / l;  // 1/l and the dropout rescale folded
-    const float inv_l = 1.0f / l;
-    const float mm = m == -INFINITY ? 0.f : m;
-    // pass 2: probabilities -> P̃ (bf16, K-major SW128 in smem)
-    const int kw0 = half * 2;  // this half's first 32-key word within a tile
-    uint2 wnext = make_uint2(0xffffffffu, 0xffffffffu);
-    auto load_words = [&](int j) {
-      uint2 w = make_uint2(0xffffffffu, 0xffffffffu);
-      if (drop_on) {
-        const int wd = j * 4 + kw0;
-        w.x = (qr < S && wd < W) ? kbits[wd] : 0u;
-        w.y = (qr < S && wd + 1 < W) ? kbits[wd + 1] : 0u;
-      }
-      return w;
-    };
-    if (nkv > 0) wnext = load_words(0);
-    for (int j = 0; j < nkv; ++j, ++sc) {
-      const int sb = sc & 1, pb = j & 1;
-      const uint2 wcur = wnext;
-      if (j + 1 < nkv) wnext = load_words(j + 1);  // prefetch the next tile's keep bits
-      mbar_wait(&s_full[sb], (sc >> 1) & 1);
-      tc_fence_after();
-      uint32_t r0[32], r1[32];
-      tmem_ld32_nw(tl + sb * 128 + half * 64, r0);
-      tmem_ld32_nw(tl + sb * 128 + half * 64 + 32, r1);
-      tmem_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[sb]);
-      mbar_wait(&p_free[pb], ((j >> 1) & 1) ^ 1);
-      const bool full = tile_full(j);
-      const int k0 = j * 128 + half * 64;
-      uint32_t pk[32];
-      uint32_t pm[MAT ? 32 : 1];  // MAT: softmax_out pairs
-#pragma unroll
-      for (int i = 0; i < 64; i += 2) {
-        float p2[2], pn[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int e = i + u;
-          const float sv = __uint_as_float(e < 32 ? r0[e] : r1[e - 32]);
-          const uint32_t word = e < 32 ? wcur.x : wcur.y;
-          const bool keep = (word >> (e & 31)) & 1u;
-          float p;
-          if constexpr (MAT) {
-            pn[u] = ex2(sv * sl2 - mm) * inv_l;
-            if (!full && (k0 + e >= S || (CAUSAL && k0 + e > qr))) pn[u] = 0.f;
-            p = pn[u] * a.drop.inv_keep;
-          } else {
-            p = ex2(sv * sl2 - mm) * scale_p;
-            if (!full && (k0 + e >= S || (CAUSAL && k0 + e > qr))) p = 0.f;
-          }
-          p2[u] = keep ? p : 0.f;
-        }
-        pk[i >> 1] = pack_bf16(p2[0], p2[1]);
-        if constexpr (MAT) pm[i >> 1] = pack_bf16(pn[0], pn[1]);
-      }
-      if constexpr (MAT) {  // S % 64 == 0 (dispatcher): a half-tile is all in or all out
-        if (qr < S && k0 < S) {
-          const int64_t mi = (brow + qr) * (int64_t)S + k0;
-          uint4* smo = reinterpret_cast<uint4*>(static_cast<bf16*>(a.sm) + mi);
-          uint4* sdo = reinterpret_cast<uint4*>(static_cast<bf16*>(a.sd) + mi);
-          uint4* mko = reinterpret_cast<uint4*>(a.mask + mi);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            smo[u] = make_uint4(pm[4 * u], pm[4 * u + 1], pm[4 * u + 2], pm[4 * u + 3]);
-            sdo[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-          }
-          const uint32_t wb[2] = {wcur.x, wcur.y};
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {  // 16 keys -> 16 mask bytes
-            uint32_t q4[4];
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const uint32_t bits = (wb[u >> 1] >> (16 * (u & 1) + 4 * v)) & 0xFu;
-              q4[v] = (bits & 1u) | ((bits & 2u) << 7) | ((bits & 4u) << 14) | ((bits & 8u) << 21);
+        uint32_t pk[32];
+        uint32_t pm[MAT ? 32 : 1];  // MAT: softmax_out pairs
+  #pragma unroll
+        for (int i = 0; i < 64; i += 2) {
+          float p2[2], pn[2];
+  #pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int e = i + u;
+            const float sv = __uint_as_float(e < 32 ? r0[e] : r1[e - 32]);
+            const uint32_t word = e < 32 ? wcur.x : wcur.y;
+            const bool keep = (word >> (e & 31)) & 1u;
+            float p;
+            if constexpr (MAT) {
+              pn[u] = ex2(sv * sl2 - mm) * inv_l;
+              if (!full && (k0 + e >= S || (CAUSAL && k0 + e > qr))) pn[u] = 0.f;
+              p = pn[u] * a.drop.inv_keep;
+            } else {
+              p = ex2(sv * sl2 - mm) * scale_p;
+              if (!full && (k0 + e >= S || (CAUSAL && k0 + e > qr))) p = 0.f;
             }
-            mko[u] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
+            p2[u] = keep ? p : 0.f;
+          }
+          pk[i >> 1] = pack_bf16(p2[0], p2[1]);
+          if constexpr (MAT) pm[i >> 1] = pack_bf16(pn[0], pn[1]);
+        }
+        if constexpr (MAT) {  // S % 64 == 0 (dispatcher): a half-tile is all in or all out
+          if (qr < S && k0 < S) {
+            const int64_t mi = (brow + qr) * (int64_t)S + k0;
+            uint4* smo = reinterpret_cast<uint4*>(static_cast<bf16*>(a.sm) + mi);
+            uint4* sdo = reinterpret_cast<uint4*>(static_cast<bf16*>(a.sd) + mi);
+            uint4* mko = reinterpret_cast<uint4*>(a.mask + mi);
+  #pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              smo[u] = make_uint4(pm[4 * u], pm[4 * u + 1], pm[4 * u + 2], pm[4 * u + 3]);
+              sdo[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+            }
+            const uint32_t wb[2] = {wcur.x, wcur.y};
+  #pragma unroll
+            for (int u = 0; u < 4; ++u) {  // 16 keys -> 16 mask bytes
+              uint32_t q4[4];
+  #pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                const uint32_t bits = (wb[u >> 1] >> (16 * (u & 1) + 4 * v)) & 0xFu;
+                q4[v] = (bits & 1u) | ((bits & 2u) << 7) | ((bits & 4u) << 14) | ((bits & 8u) << 21);
+              }
+              mko[u] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
+            }
           }
         }
+        uint8_t* prow = Ps + pb * Cfg::P_BYTES + row * 128;
+        // this half's keys = logical 16 B chunks 8*half .. 8*half+7 = atom `half`, swizzled by row
+  #pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int phys = u ^ (row & 7);
+          *reinterpret_cast<uint4*>(prow + half * kAtomBytes + phys * 16) =
+              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[pb]);
       }
-      uint8_t* prow = Ps + pb * Cfg::P_BYTES + row * 128;
-      // this half's keys = logical 16 B chunks 8*half .. 8*half+7 = atom `half`, swizzled by row
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int phys = u ^ (row & 7);
-        *reinterpret_cast<uint4*>(prow + half * kAtomBytes + phys * 16) =
-            make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+
+    } else {
+      float m_used = -INFINITY;
+      l = 0.f;
+      int sc = 0;
+      auto tile_full = [&](int j) {
+        return j * 128 + 128 <= S && !(CAUSAL && j * 128 + 127 > q0);
+      };
+      float* xch = reinterpret_cast<float*>(smem + Cfg::XCH_OFF);  // [half][row]
+      const int kw0 = half * 2;  // this half's first 32-key word within a tile
+      auto load_words = [&](int j) {
+        uint2 w = make_uint2(0xffffffffu, 0xffffffffu);
+        if (drop_on) {
+          const int wd = j * 4 + kw0;
+          w.x = (qr < S && wd < W) ? kbits[wd] : 0u;
+          w.y = (qr < S && wd + 1 < W) ? kbits[wd + 1] : 0u;
+        }
+        return w;
+      };
+      auto pair_sync = [&] { asm volatile("bar.sync %0, 64;" ::"r"(2 + qd) : "memory"); };
+      uint2 wnext = nkv > 0 ? load_words(0) : make_uint2(0u, 0u);
+      for (int j = 0; j < nkv; ++j, ++sc) {
+        const int sb = sc & 1, pb = j & 1;
+        const uint2 wcur = wnext;
+        if (j + 1 < nkv) wnext = load_words(j + 1);
+        mbar_wait(&s_full[sb], (sc >> 1) & 1);
+        tc_fence_after();
+        uint32_t r0[32], r1[32];
+        tmem_ld32_nw(tl + sb * 128 + half * 64, r0);
+        tmem_ld32_nw(tl + sb * 128 + half * 64 + 32, r1);
+        tmem_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[sb]);
+        const bool full = tile_full(j);
+        const int k0 = j * 128 + half * 64;
+        float v[64];
+  #pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          v[i] = __uint_as_float(r0[i]) * sl2;
+          v[32 + i] = __uint_as_float(r1[i]) * sl2;
+        }
+        if (!full) {
+  #pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (k0 + i >= S || (CAUSAL && k0 + i > qr)) v[i] = -INFINITY;
+        }
+        float cm = v[0];
+  #pragma unroll
+        for (int i = 1; i < 64; ++i) cm = fmaxf(cm, v[i]);
+        // row max of the whole tile: exchange with the partner warp (same rows, other half)
+        xch[half * 128 + row] = cm;
+        pair_sync();
+        const float mt = fmaxf(cm, xch[(half ^ 1) * 128 + row]);
+        pair_sync();  // both read before the next tile's write
+        bool rescale = false;
+        float f = 1.f;
+        if (m_used == -INFINITY) {
+          m_used = mt;  // O and l are still zero: nothing to rescale
+        } else if (mt > m_used + 8.f) {
+          f = ex2(m_used - mt);
+          m_used = mt;
+          l *= f;
+          rescale = true;
+        }
+        const float mm = m_used == -INFINITY ? 0.f : m_used;
+        mbar_wait(&p_free[pb], ((j >> 1) & 1) ^ 1);
+        if (__any_sync(0xffffffffu, rescale)) {
+          // O += P̃·V of tile j-1 must have landed before O is rescaled in TMEM
+          mbar_wait(o_done, (j - 1) & 1);
+          tc_fence_after();
+  #pragma unroll 1
+          for (int c = half; c < HD / 32; c += 2) {
+            float o[32];
+            tmem_ld32(tl + Cfg::O_COL + c * 32, o);
+  #pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= f;
+            tmem_st32(tl + Cfg::O_COL + c * 32, o);
+          }
+        }
+        uint32_t pk[32];
+        float ls = 0.f;
+  #pragma unroll
+        for (int i = 0; i < 64; i += 2) {
+          float p2[2];
+  #pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int e = i + u;
+            const uint32_t word = e < 32 ? wcur.x : wcur.y;
+            const bool keep = (word >> (e & 31)) & 1u;
+            const float p = ex2(v[e] - mm);
+            ls += p;
+            p2[u] = keep ? p : 0.f;
+          }
+          pk[i >> 1] = pack_bf16(p2[0], p2[1]);
+        }
+        l += ls;
+        uint8_t* prow = Ps + pb * Cfg::P_BYTES + row * 128;
+  #pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int phys = u ^ (row & 7);
+          *reinterpret_cast<uint4*>(prow + half * kAtomBytes + phys * 16) =
+              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+        fence_proxy_async();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[pb]);
       }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[pb]);
+      // l of the whole row: both halves share m_used
+      xch[half * 128 + row] = l;
+      pair_sync();
+      l += xch[(half ^ 1) * 128 + row];
+      m = m_used;
+      oscale = a.drop.inv_keep / l;
+
     }
-    // epilogue: O (already normalised) -> bf16; the halves take alternate 32-column chunks
+    // epilogue: O · oscale -> bf16; the halves take alternate 32-column chunks
     mbar_wait(o_full, 0);
     tc_fence_after();
     bf16* out = static_cast<bf16*>(a.o) + ((int64_t)(qr < S ? qr : 0) * a.b + bj) * a.ldo +
@@ -358,8 +490,10 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int i = 0; i < 32; i += 8)
           *reinterpret_cast<uint4*>(out + c * 32 + i) =
-              make_uint4(pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]),
-                         pack_bf16(v[i + 4], v[i + 5]), pack_bf16(v[i + 6], v[i + 7]));
+              make_uint4(pack_bf16(v[i] * oscale, v[i + 1] * oscale),
+                         pack_bf16(v[i + 2] * oscale, v[i + 3] * oscale),
+                         pack_bf16(v[i + 4] * oscale, v[i + 5] * oscale),
+                         pack_bf16(v[i + 6] * oscale, v[i + 7] * oscale));
       }
     }
     if (half == 0 && qr < S && a.lse) a.lse[brow + qr] = (m + log2f(l)) * kLn2;

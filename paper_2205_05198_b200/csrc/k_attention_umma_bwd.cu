@@ -74,13 +74,16 @@ struct DkdvLayout {
   static constexpr int SMT = 64 * 128 * 2, MKT = 64 * 128;  // stored P / mask tiles
   template <bool STORED>
   struct L {
+    // (Q, dO) ring depth: 3 stages keep the TMA of tile it+2 in flight while tile it's dV/dK
+    // MMAs run (2 stages exposed the TMA latency between them); the stored variant needs its
+    // smem for the P / mask tiles.
+    static constexpr int NS = STORED ? 2 : 3;
     static constexpr int K_OFF = 0;
     static constexpr int V_OFF = STORED ? 0 : C::T128;
     static constexpr int QD_OFF = V_OFF + C::T128;
-    static constexpr int W_OFF = QD_OFF + 4 * C::T64;
+    static constexpr int W_OFF = QD_OFF + NS * 2 * C::T64;
     static constexpr int SMM_OFF = W_OFF + 4 * C::W_BYTES;
-    static constexpr int LD_OFF = SMM_OFF + (STORED ? 2 * (SMT + MKT) : 0);
-    static constexpr int BAR_OFF = LD_OFF + 2 * 2 * 64 * 4;
+    static constexpr int BAR_OFF = SMM_OFF + (STORED ? NS * (SMT + MKT) : 0);
     static constexpr int SMEM = BAR_OFF + 256 + 1024;
   };
 };
@@ -105,15 +108,16 @@ __global__ void __launch_bounds__(320, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
+  constexpr int NS = Lay::NS;
   uint64_t* kv_full = bar + 0;
-  uint64_t* qd_full = bar + 1;   // [2]
-  uint64_t* qd_empty = bar + 3;  // [2]
-  uint64_t* sd_full = bar + 5;   // [2] Sᵀ, dPᵀ ready in TMEM
-  uint64_t* sd_free = bar + 7;   // [2] read by the warps
-  uint64_t* w_full = bar + 9;    // [2] P̃ᵀ, dSᵀ written to smem
-  uint64_t* w_free = bar + 11;   // [2] consumed by the dV/dK MMAs
-  uint64_t* acc_full = bar + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t* qd_full = bar + 1;          // [NS]
+  uint64_t* qd_empty = bar + 1 + NS;    // [NS]
+  uint64_t* sd_full = bar + 1 + 2 * NS; // [2] Sᵀ, dPᵀ ready in TMEM
+  uint64_t* sd_free = sd_full + 2;      // [2] read by the warps
+  uint64_t* w_full = sd_full + 4;       // [2] P̃ᵀ, dSᵀ written to smem
+  uint64_t* w_free = sd_full + 6;       // [2] consumed by the dV/dK MMAs
+  uint64_t* acc_full = sd_full + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sd_full + 9);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k0 = blockIdx.x * 128;
@@ -129,9 +133,11 @@ __global__ void __launch_bounds__(320, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(&qd_full[i], 1);
       mbar_init(&qd_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&sd_full[i], 1);
       mbar_init(&sd_free[i], 8);
       mbar_init(&w_full[i], 8);
@@ -155,8 +161,8 @@ __global__ void __launch_bounds__(320, 1)
         tma_load_3d(smem + V_OFF + at * C::A128, &map_kv, kv_full, vcol + 64 * at, bj, k0);
       }
       for (int it = 0; it < nq; ++it) {
-        const int st = it & 1;
-        mbar_wait(&qd_empty[st], ((it >> 1) & 1) ^ 1);
+        const int st = it % NS;
+        mbar_wait(&qd_empty[st], ((it / NS) & 1) ^ 1);
         uint8_t* Qt = smem + QD_OFF + st * 2 * C::T64;
         uint8_t* Dt = Qt + C::T64;
         const int qb = q_start + it * 64;
@@ -180,11 +186,11 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t ka = smem_u32(smem + K_OFF), va = smem_u32(smem + V_OFF);
       mbar_wait(kv_full, 0);
       auto issue_sd = [&](int it) {
-        const int st = it & 1;
-        mbar_wait(&qd_full[st], (it >> 1) & 1);
+        const int st = it & 1, qs = it % NS;
+        mbar_wait(&qd_full[qs], (it / NS) & 1);
         mbar_wait(&sd_free[st], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t qb = smem_u32(smem + QD_OFF + st * 2 * C::T64), db = qb + C::T64;
+        const uint32_t qb = smem_u32(smem + QD_OFF + qs * 2 * C::T64), db = qb + C::T64;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t oa = (kk >> 2) * C::A128 + (kk & 3) * 32;
@@ -200,11 +206,11 @@ __global__ void __launch_bounds__(320, 1)
       if (nq > 0) issue_sd(0);
       for (int it = 0; it < nq; ++it) {
         if (it + 1 < nq) issue_sd(it + 1);
-        const int st = it & 1;
+        const int st = it & 1, qs = it % NS;
         mbar_wait(&w_full[st], (it >> 1) & 1);
         tc_fence_after();
         const uint32_t pw = smem_u32(smem + W_OFF + st * 2 * C::W_BYTES), dw = pw + C::W_BYTES;
-        const uint32_t qb = smem_u32(smem + QD_OFF + st * 2 * C::T64), db = qb + C::T64;
+        const uint32_t qb = smem_u32(smem + QD_OFF + qs * 2 * C::T64), db = qb + C::T64;
 #pragma unroll
         for (int kk = 0; kk < 64 / 16; ++kk) {
           // dV += P̃ᵀ·dO ; dK += dSᵀ·Q  (B = dO / Q tiles read MN-major)
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(320, 1)
                     smem_desc(qb + kk * 2048, C::A64, 1024), idesc_acc, (it | kk) != 0 ? 1u : 0u);
         }
         umma_commit(&w_free[st]);
-        umma_commit(&qd_empty[st]);
+        umma_commit(&qd_empty[qs]);
       }
       umma_commit(acc_full);
     }
@@ -246,7 +252,7 @@ __global__ void __launch_bounds__(320, 1)
                  : (q < S && (k0 >> 5) + qd < W) ? kbits[(brow + q) * W + (k0 >> 5) + qd] : 0u;
         }
       }
-      if (STORED) mbar_wait(&qd_full[st], (it >> 1) & 1);  // stored P / mask tiles landed
+      if (STORED) mbar_wait(&qd_full[it % NS], (it / NS) & 1);  // stored P / mask tiles landed
       mbar_wait(&sd_full[st], (it >> 1) & 1);
       tc_fence_after();
       uint32_t rs[32], rp[32];
@@ -272,7 +278,7 @@ __global__ void __launch_bounds__(320, 1)
           float p;
           if constexpr (STORED) {
             // [64 q][128 k] tiles: this warp's 32 keys of query row 32*half + e
-            const uint8_t* St = smem + SMM_OFF + st * (SMT + MKT);
+            const uint8_t* St = smem + SMM_OFF + (it % NS) * (SMT + MKT);
             const int qi = 32 * half + e;
             p = valid ? __bfloat162float(reinterpret_cast<const bf16*>(St)[qi * 128 + row]) : 0.f;
             keep = St[SMT + qi * 128 + row] != 0;
@@ -345,10 +351,11 @@ struct DqLayout {
   static constexpr int SMT = 128 * 64 * 2, MKT = 128 * 64;
   template <bool STORED>
   struct L {
+    static constexpr int NS = STORED ? 2 : 4;  // (K, V [, P, mask]) ring depth
     static constexpr int Q_OFF = 0, D_OFF = C::T128, KV_OFF = 2 * C::T128;
-    static constexpr int W_OFF = KV_OFF + 4 * C::T64;
+    static constexpr int W_OFF = KV_OFF + NS * 2 * C::T64;
     static constexpr int SMM_OFF = W_OFF + 2 * C::W_BYTES;
-    static constexpr int BAR_OFF = SMM_OFF + (STORED ? 2 * (SMT + MKT) : 0);
+    static constexpr int BAR_OFF = SMM_OFF + (STORED ? NS * (SMT + MKT) : 0);
     static constexpr int SMEM = BAR_OFF + 256 + 1024;
   };
 };
@@ -372,15 +379,16 @@ __global__ void __launch_bounds__(320, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
+  constexpr int NS = Lay::NS;
   uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* sd_full = bar + 5;   // [2]
-  uint64_t* sd_free = bar + 7;   // [2]
-  uint64_t* w_full = bar + 9;    // [2]
-  uint64_t* w_free = bar + 11;   // [2]
-  uint64_t* acc_full = bar + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t* kv_full = bar + 1;          // [NS]
+  uint64_t* kv_empty = bar + 1 + NS;    // [NS]
+  uint64_t* sd_full = bar + 1 + 2 * NS; // [2]
+  uint64_t* sd_free = sd_full + 2;      // [2]
+  uint64_t* w_full = sd_full + 4;       // [2]
+  uint64_t* w_free = sd_full + 6;       // [2]
+  uint64_t* acc_full = sd_full + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sd_full + 9);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q0 = blockIdx.x * 128;
@@ -395,9 +403,11 @@ __global__ void __launch_bounds__(320, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&sd_full[i], 1);
       mbar_init(&sd_free[i], 8);
       mbar_init(&w_full[i], 8);
@@ -421,8 +431,8 @@ __global__ void __launch_bounds__(320, 1)
         tma_load_3d(smem + D_OFF + at * C::A128, &map_do, q_full, dcol + 64 * at, bj, q0);
       }
       for (int it = 0; it < nkv; ++it) {
-        const int st = it & 1;
-        mbar_wait(&kv_empty[st], ((it >> 1) & 1) ^ 1);
+        const int st = it % NS;
+        mbar_wait(&kv_empty[st], ((it / NS) & 1) ^ 1);
         uint8_t* Kt = smem + KV_OFF + st * 2 * C::T64;
         uint8_t* Vt = Kt + C::T64;
         mbar_expect_tx(&kv_full[st], 2 * C::T64 + (STORED ? SMT + MKT : 0));
@@ -432,7 +442,7 @@ __global__ void __launch_bounds__(320, 1)
           tma_load_3d(Vt + at * C::A64, &map_kv, &kv_full[st], vcol + 64 * at, bj, it * 64);
         }
         if (STORED) {
-          uint8_t* St = smem + SMM_OFF + st * (SMT + MKT);
+          uint8_t* St = smem + SMM_OFF + st * (SMT + MKT);  // st = it % NS here
           tma_load_3d(St, &map_sm, &kv_full[st], it * 64, q0, (int)blockIdx.y);
           tma_load_3d(St + SMT, &map_mk, &kv_full[st], it * 64, q0, (int)blockIdx.y);
         }
@@ -445,11 +455,11 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t qa = smem_u32(smem + Q_OFF), da = smem_u32(smem + D_OFF);
       mbar_wait(q_full, 0);
       auto issue_sd = [&](int it) {
-        const int st = it & 1;
-        mbar_wait(&kv_full[st], (it >> 1) & 1);
+        const int st = it & 1, ks = it % NS;
+        mbar_wait(&kv_full[ks], (it / NS) & 1);
         mbar_wait(&sd_free[st], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t kb = smem_u32(smem + KV_OFF + st * 2 * C::T64), vb = kb + C::T64;
+        const uint32_t kb = smem_u32(smem + KV_OFF + ks * 2 * C::T64), vb = kb + C::T64;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t oa = (kk >> 2) * C::A128 + (kk & 3) * 32;
@@ -465,17 +475,17 @@ __global__ void __launch_bounds__(320, 1)
       if (nkv > 0) issue_sd(0);
       for (int it = 0; it < nkv; ++it) {
         if (it + 1 < nkv) issue_sd(it + 1);
-        const int st = it & 1;
+        const int st = it & 1, ks = it % NS;
         mbar_wait(&w_full[st], (it >> 1) & 1);
         tc_fence_after();
         const uint32_t dsw = smem_u32(smem + W_OFF + st * C::W_BYTES);
-        const uint32_t kb = smem_u32(smem + KV_OFF + st * 2 * C::T64);
+        const uint32_t kb = smem_u32(smem + KV_OFF + ks * 2 * C::T64);
 #pragma unroll
         for (int kk = 0; kk < 64 / 16; ++kk)
           umma_bf16(tmem + DQ_COL, smem_desc(dsw + kk * 32, 16, 1024),
                     smem_desc(kb + kk * 2048, C::A64, 1024), idesc_acc, (it | kk) != 0 ? 1u : 0u);
         umma_commit(&w_free[st]);
-        umma_commit(&kv_empty[st]);
+        umma_commit(&kv_empty[ks]);
       }
       umma_commit(acc_full);
     }
@@ -498,8 +508,8 @@ __global__ void __launch_bounds__(320, 1)
       uint32_t word = 0xffffffffu;
       uint32_t pst[16];  // STORED: this half's 32 stored probabilities (bf16 pairs)
       if constexpr (STORED) {
-        mbar_wait(&kv_full[st], (it >> 1) & 1);  // stored P / mask tiles landed
-        const uint8_t* St = smem + SMM_OFF + st * (SMT + MKT);
+        mbar_wait(&kv_full[it % NS], (it / NS) & 1);  // stored P / mask tiles landed
+        const uint8_t* St = smem + SMM_OFF + (it % NS) * (SMT + MKT);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint4 v = *reinterpret_cast<const uint4*>(St + row * 128 + (((4 * half + u) ^ (row & 7)) * 16));

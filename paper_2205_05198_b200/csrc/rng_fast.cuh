@@ -61,9 +61,12 @@ __device__ __forceinline__ bool keep_fast(uint32_t lo, uint32_t hi0, uint32_t hc
     lo = (uint32_t)w;
   }
   (void)hi_xs;
-  xs_fma(lo, hi, sm.m27);
+  (void)sm;
+  // Every xor-shift in funnel-shift (ALU) form: measured fastest on B200 (tools/micro/
+  // bench_rng2.cu: 1.97 ms vs 2.12 ms for three in IMAD.HI form, 1.07e9 keys).
+  xs_alu(lo, hi, 27);
   mul_c<0x133111ebu, 0x94d049bbu>(lo, hi);
-  xs_fma(lo, hi, sm.m31);
+  xs_alu(lo, hi, 31);
   // ^ mix64(key), + G (64-bit add as IMAD.WIDE with a 64-bit addend)
   lo ^= mixed_lo;
   hi ^= mixed_hi;
@@ -74,7 +77,7 @@ __device__ __forceinline__ bool keep_fast(uint32_t lo, uint32_t hi0, uint32_t hc
   }
   xs_alu(lo, hi, 30);
   mul_c<0x1ce4e5b9u, 0xbf58476du>(lo, hi);
-  xs_fma(lo, hi, sm.m27);
+  xs_alu(lo, hi, 27);
   mul_c<0x133111ebu, 0x94d049bbu>(lo, hi);
   xs_alu(lo, hi, 31);
   return (((uint64_t)hi << 32) | lo) >= (((uint64_t)t_hi << 32) | t_lo);
