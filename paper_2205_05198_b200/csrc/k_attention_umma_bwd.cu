@@ -236,22 +236,28 @@ __global__ void __launch_bounds__(320, 1)
     const bool drop_on = a.drop.thresh != 0;
     const int W = (S + 31) / 32;
     const uint32_t* kbits = a.keepbits;
+    // lse (log2 domain), rowdot and the keep-bit word (q, this warp's 32 keys) of this half's
+    // 32 queries of tile `it`: lane e holds query qb + 32*half + e. Loaded one tile ahead.
+    auto row_stats = [&](int it, float& lse_o, float& dl_o, uint32_t& kw_o) {
+      const int q = q_start + it * 64 + 32 * half + lane;
+      lse_o = 0.f;
+      kw_o = 0u;
+      dl_o = (it < nq && q < S) ? delta[brow + q] : 0.f;
+      if (!STORED && it < nq) {
+        lse_o = q < S ? a.lse[brow + q] * kLog2e : INFINITY;
+        kw_o = !drop_on ? 0xffffffffu
+               : (q < S && (k0 >> 5) + qd < W) ? kbits[(brow + q) * W + (k0 >> 5) + qd] : 0u;
+      }
+    };
+    float lse_n, dl_n;
+    uint32_t kw_n;
+    row_stats(0, lse_n, dl_n, kw_n);
     for (int it = 0; it < nq; ++it) {
       const int st = it & 1;
       const int qb = q_start + it * 64;
-      // lse (log2 domain), rowdot and the keep-bit word (q, this warp's 32 keys) of this half's
-      // 32 queries: lane e holds query q0h + e
-      float lse_l = 0.f, dl_l;
-      uint32_t kw_l = 0u;
-      {
-        const int q = qb + 32 * half + lane;
-        dl_l = q < S ? delta[brow + q] : 0.f;
-        if (!STORED) {
-          lse_l = q < S ? a.lse[brow + q] * kLog2e : INFINITY;
-          kw_l = !drop_on ? 0xffffffffu
-                 : (q < S && (k0 >> 5) + qd < W) ? kbits[(brow + q) * W + (k0 >> 5) + qd] : 0u;
-        }
-      }
+      const float lse_l = lse_n, dl_l = dl_n;
+      const uint32_t kw_l = kw_n;
+      row_stats(it + 1, lse_n, dl_n, kw_n);
       if (STORED) mbar_wait(&qd_full[it % NS], (it / NS) & 1);  // stored P / mask tiles landed
       mbar_wait(&sd_full[st], (it >> 1) & 1);
       tc_fence_after();
@@ -502,10 +508,16 @@ __global__ void __launch_bounds__(320, 1)
     const float lse2 = (!STORED && qr < S) ? a.lse[brow + qr] * kLog2e : INFINITY;
     const float dl = qr < S ? delta[brow + qr] : 0.f;
     const uint32_t* kb = STORED ? nullptr : a.keepbits + (brow + (qr < S ? qr : 0)) * W;
+    auto key_word = [&](int it) {  // keep bits of (this row, keys it*64 + 32*half ..)
+      const int kc = it * 64 + 32 * half;
+      return (STORED || !drop_on) ? 0xffffffffu : (it < nkv && qr < S && kc < S) ? kb[kc >> 5] : 0u;
+    };
+    uint32_t word_n = key_word(0);
     for (int it = 0; it < nkv; ++it) {
       const int st = it & 1;
       const int kc0 = it * 64 + 32 * half;
-      uint32_t word = 0xffffffffu;
+      uint32_t word = word_n;
+      word_n = key_word(it + 1);
       uint32_t pst[16];  // STORED: this half's 32 stored probabilities (bf16 pairs)
       if constexpr (STORED) {
         mbar_wait(&kv_full[it % NS], (it / NS) & 1);  // stored P / mask tiles landed
@@ -521,8 +533,6 @@ __global__ void __launch_bounds__(320, 1)
         word = 0u;
 #pragma unroll
         for (int e = 0; e < 32; ++e) word |= ((mw[e >> 2] >> (8 * (e & 3))) & 1u) << e;
-      } else {
-        word = !drop_on ? 0xffffffffu : (qr < S && kc0 < S) ? kb[kc0 >> 5] : 0u;
       }
       mbar_wait(&sd_full[st], (it >> 1) & 1);
       tc_fence_after();
