@@ -166,12 +166,14 @@ def run_reference(args):
     p = orc.params_random(h, 7)
     x = orc.random_uniform(1, (s_sample, b_sample, h), -1, 1)
     dy = orc.random_uniform(2, (s_sample, b_sample, h), -1, 1)
-    budget = 150.0  # seconds for the whole run
+    budget = 150.0  # seconds for the whole run (warm-up included)
     t0 = time.perf_counter()
-    orc.seqpar_layer(cfg, 1, p, x, dy)
+    orc.seqpar_layer(cfg, 1, p, x, dy)  # first warm-up step, also sizes the run
     one = time.perf_counter() - t0
-    steps = max(1, min(args.steps, int(budget / max(one, 1e-3)) - min(args.warmup, 1)))
-    for _ in range(max(0, min(args.warmup, 1) - 1)):
+    fit = max(2, int(budget / max(one, 1e-3)))
+    warmup = max(1, min(args.warmup, fit // 2))
+    steps = max(1, min(args.steps, fit - warmup))
+    for _ in range(warmup - 1):
         orc.seqpar_layer(cfg, 1, p, x, dy)
     t0 = time.perf_counter()
     for _ in range(steps):
@@ -181,7 +183,7 @@ def run_reference(args):
     sample = (f"oracle fp64 seqpar fwd+bwd (reference algorithm; reference build needs Eigen3/"
               f"Boost, absent), h={h} a={a} s={s_sample} b={b_sample} t=1, {steps} steps")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s",
-            "n_gpus": args.gpus, "steps": steps, "warmup": min(args.warmup, 1),
+            "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
             "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config} layer fwd+bwd (sampled)", "heads": a, "hidden": h,
