@@ -124,7 +124,7 @@ def gemm_traffic_from_profile(cfg_name):
         return None
     n = b = 0.0
     for k, v in prof.items():
-        if k.startswith("gemm_tc_kernel"):
+        if k.startswith("gemm_tc"):
             n += v["launches"]
             b += v["launches"] * (v["dram_read_bytes_per_launch"] + v["dram_write_bytes_per_launch"])
     return b / n if n else None

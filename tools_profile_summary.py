@@ -18,7 +18,7 @@ for r in rows:
         recs[d["ID"]][d["Metric Name"]] = float(d["Metric Value"])
 fam = defaultdict(lambda: dict(n=0, ns=0.0, rd=0.0, wr=0.0))
 for v in recs.values():
-    m = re.search(r"(fa_\w+|gemm_tc_kernel<[^>]*>|keep_bits_k|ln_\w+|bdr_k<[^>]*>|dropout\w+|colsum\w+|reduce\w+|rs_local_k|\w+_k)", v["name"])
+    m = re.search(r"(fa_\w+|gemm_tc\w*<[^>]*>|keep_bits_k|ln_\w+|bdr_\w+<[^>]*>|dropout\w+|colsum\w+|reduce\w+|rs_local_k|\w+_k)", v["name"])
     key = m.group(1) if m else v["name"][:60]
     f = fam[key]
     f["n"] += 1
