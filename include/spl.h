@@ -102,6 +102,14 @@ int spl_backward(spl_handle* h, const void* const* dy, void* const* dx);
  * order, in the desc dtype; pinned host memory is used directly, pageable is staged. */
 int spl_step_host(spl_handle* h, const void* x_host, const void* dy_host, void* y_host,
                   void* dx_host);
+/* The same step issued asynchronously (a training loop's overlapped data path): uploads run
+ * on an upload stream, downloads on a download stream, and the device staging is double
+ * buffered, so step k+1's H2D and step k's D2H overlap the compute. The host buffers of a step
+ * must stay valid and untouched until spl_step_host_wait() returns (it waits for every step
+ * issued so far); use pinned memory for the copies to be asynchronous. */
+int spl_step_host_async(spl_handle* h, const void* x_host, const void* dy_host, void* y_host,
+                        void* dx_host);
+int spl_step_host_wait(spl_handle* h);
 
 /* Gradients assembled into the full fp64 layout (block.cpp:730-746). For an NCCL rank, only
  * the rank's own shard of column/row-sharded tensors is filled (others left zero) and the

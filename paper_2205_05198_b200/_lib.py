@@ -66,6 +66,8 @@ def lib():
         "spl_forward": (I32, [H, P(VP), P(VP)]),
         "spl_backward": (I32, [H, P(VP), P(VP)]),
         "spl_step_host": (I32, [H, VP, VP, VP, VP]),
+        "spl_step_host_async": (I32, [H, VP, VP, VP, VP]),
+        "spl_step_host_wait": (I32, [H]),
         "spl_get_grads": (I32, [H, P(D)]),
         "spl_get_w1_grad_shard": (I32, [H, I32, P(D)]),
         "spl_get_saved": (I32, [H, I32, C.c_char_p, P(D), I64]),

@@ -213,6 +213,21 @@ int spl_step_host(spl_handle* h, const void* x, const void* dy, void* y, void* d
   });
 }
 
+int spl_step_host_async(spl_handle* h, const void* x, const void* dy, void* y, void* dx) {
+  return guard([&] {
+    check_handle(h);
+    spl::require(x && dy && y && dx, "null host buffer");
+    h->layer->step_host_async(x, dy, y, dx);
+  });
+}
+
+int spl_step_host_wait(spl_handle* h) {
+  return guard([&] {
+    check_handle(h);
+    h->layer->step_host_wait();
+  });
+}
+
 int spl_get_grads(spl_handle* h, double* out) {
   return guard([&] {
     check_handle(h);

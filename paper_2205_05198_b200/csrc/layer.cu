@@ -93,8 +93,9 @@ class Layer final : public LayerBase {
   ~Layer() override {
     cudaSetDevice(dev_);
     cudaStreamSynchronize(st_);
-    for (Graph* g : {&gfwd_, &gbwd_})
-      if (g->exec) cudaGraphExecDestroy(g->exec);
+    for (auto* set : {&gfwd_, &gbwd_})
+      for (Graph& g : *set)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     for (auto& a : allocs_) cudaFree(a.ptr);
     if (pinned_) cudaFreeHost(pinned_);
     for (auto& e : evpool_) cudaEventDestroy(e);
@@ -102,6 +103,14 @@ class Layer final : public LayerBase {
     cudaEventDestroy(ev_out_);
     cudaEventDestroy(ev_fork_);
     cudaEventDestroy(ev_bits_);
+    if (st_up_) {
+      cudaStreamSynchronize(st_up_);
+      cudaStreamSynchronize(st_down_);
+      cudaStreamDestroy(st_up_);
+      cudaStreamDestroy(st_down_);
+      for (int i = 0; i < 2; ++i)
+        for (auto e : {ev_x_[i], ev_dy_[i], ev_f_[i], ev_b_[i], ev_free_[i]}) cudaEventDestroy(e);
+    }
     cudaStreamSynchronize(st_rng_);
     cudaStreamDestroy(st_rng_);
     cudaStreamSynchronize(st_comm_);
@@ -115,19 +124,30 @@ class Layer final : public LayerBase {
 
   // Run `body` (which issues work on st_, possibly forking to the side streams and joining
   // back) either eagerly or as a CUDA graph captured on the first call with these pointers.
+  // One executable graph per (input, output) pointer set, up to kMaxGraphs per direction
+  // (double-buffered callers alternate between two sets).
+  static constexpr size_t kMaxGraphs = 4;
   template <typename F>
-  void run_graphed(Graph& g, const std::vector<const void*>& in, const std::vector<void*>& out,
-                   F&& body) {
+  void run_graphed(std::vector<Graph>& set, const std::vector<const void*>& in,
+                   const std::vector<void*>& out, F&& body) {
     const bool use = graphs_ && !profiling_ && !d_.check_finite;
     if (!use) {
       body();
       return;
     }
-    if (g.exec == nullptr || g.in != in || g.out != out) {
-      if (g.exec) {
-        SPL_CUDA(cudaGraphExecDestroy(g.exec));
-        g.exec = nullptr;
+    Graph* gp = nullptr;
+    for (Graph& c : set)
+      if (c.exec != nullptr && c.in == in && c.out == out) gp = &c;
+    if (gp == nullptr) {
+      if (set.size() >= kMaxGraphs) {
+        SPL_CUDA(cudaGraphExecDestroy(set.front().exec));
+        set.erase(set.begin());
       }
+      set.emplace_back();
+      gp = &set.back();
+    }
+    Graph& g = *gp;
+    if (g.exec == nullptr) {
       const int64_t l0 = launches_;
       cudaGraph_t graph;
       SPL_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
@@ -290,31 +310,70 @@ class Layer final : public LayerBase {
     leave();
   }
 
-  void step_host(const void* x, const void* dy, void* y, void* dx) override {
+  // One training step through host buffers, issued asynchronously: H2D of x and dy on the
+  // upload stream, forward / backward on the compute stream, D2H of y and dx on the download
+  // stream, each side waiting only for what it needs (x before the forward, dy before the
+  // backward, y after the forward, dx after the backward). The device staging buffers are
+  // double-buffered, so step k+1's uploads overlap step k's compute and step k's downloads
+  // overlap step k+1's compute. step_host_wait() returns when the last issued step's results
+  // are in host memory; the host buffers must stay untouched until then.
+  void step_host_async(const void* x, const void* dy, void* y, void* dx) override {
     SPL_CUDA(cudaSetDevice(dev_));
     const size_t shard = (size_t)(RL_ * h_) * sizeof(T);
     ensure_staging();
+    if (st_up_ == nullptr) {
+      SPL_CUDA(cudaStreamCreateWithFlags(&st_up_, cudaStreamNonBlocking));
+      SPL_CUDA(cudaStreamCreateWithFlags(&st_down_, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i)
+        for (auto* e : {&ev_x_[i], &ev_dy_[i], &ev_f_[i], &ev_b_[i], &ev_free_[i]}) {
+          SPL_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+          SPL_CUDA(cudaEventRecord(*e, st_));  // recorded once so that the first waits pass
+        }
+    }
+    const int sl = (int)(host_steps_++ & 1);
     std::vector<const void*> xs(L_), dys(L_);
     std::vector<void*> ysv(L_), dxs(L_);
     for (int r = 0; r < L_; ++r) {
-      SPL_CUDA(cudaMemcpyAsync(stage_[4 * r + 0], static_cast<const char*>(x) + r * shard, shard,
-                               cudaMemcpyHostToDevice, st_));
-      SPL_CUDA(cudaMemcpyAsync(stage_[4 * r + 1], static_cast<const char*>(dy) + r * shard, shard,
-                               cudaMemcpyHostToDevice, st_));
-      xs[r] = stage_[4 * r + 0];
-      dys[r] = stage_[4 * r + 1];
-      ysv[r] = stage_[4 * r + 2];
-      dxs[r] = stage_[4 * r + 3];
+      T* const* b = &stage_[(size_t)(8 * r + 4 * sl)];
+      xs[r] = b[0];
+      dys[r] = b[1];
+      ysv[r] = b[2];
+      dxs[r] = b[3];
     }
+    // uploads into this slot once its previous user (two steps ago) has been downloaded
+    SPL_CUDA(cudaStreamWaitEvent(st_up_, ev_free_[sl], 0));
+    for (int r = 0; r < L_; ++r)
+      SPL_CUDA(cudaMemcpyAsync(const_cast<void*>(xs[r]), static_cast<const char*>(x) + r * shard,
+                               shard, cudaMemcpyHostToDevice, st_up_));
+    SPL_CUDA(cudaEventRecord(ev_x_[sl], st_up_));
+    for (int r = 0; r < L_; ++r)
+      SPL_CUDA(cudaMemcpyAsync(const_cast<void*>(dys[r]), static_cast<const char*>(dy) + r * shard,
+                               shard, cudaMemcpyHostToDevice, st_up_));
+    SPL_CUDA(cudaEventRecord(ev_dy_[sl], st_up_));
+    SPL_CUDA(cudaStreamWaitEvent(st_, ev_x_[sl], 0));
     forward(xs.data(), ysv.data());
+    SPL_CUDA(cudaEventRecord(ev_f_[sl], st_));
+    SPL_CUDA(cudaStreamWaitEvent(st_, ev_dy_[sl], 0));
     backward(dys.data(), dxs.data());
-    for (int r = 0; r < L_; ++r) {
+    SPL_CUDA(cudaEventRecord(ev_b_[sl], st_));
+    SPL_CUDA(cudaStreamWaitEvent(st_down_, ev_f_[sl], 0));
+    for (int r = 0; r < L_; ++r)
       SPL_CUDA(cudaMemcpyAsync(static_cast<char*>(y) + r * shard, ysv[r], shard,
-                               cudaMemcpyDeviceToHost, st_));
+                               cudaMemcpyDeviceToHost, st_down_));
+    SPL_CUDA(cudaStreamWaitEvent(st_down_, ev_b_[sl], 0));
+    for (int r = 0; r < L_; ++r)
       SPL_CUDA(cudaMemcpyAsync(static_cast<char*>(dx) + r * shard, dxs[r], shard,
-                               cudaMemcpyDeviceToHost, st_));
-    }
+                               cudaMemcpyDeviceToHost, st_down_));
+    SPL_CUDA(cudaEventRecord(ev_free_[sl], st_down_));
+  }
+  void step_host_wait() override {
+    SPL_CUDA(cudaSetDevice(dev_));
+    if (st_down_) SPL_CUDA(cudaStreamSynchronize(st_down_));
     SPL_CUDA(cudaStreamSynchronize(st_));
+  }
+  void step_host(const void* x, const void* dy, void* y, void* dx) override {
+    step_host_async(x, dy, y, dx);
+    step_host_wait();
   }
 
   // ------------------------------------------------------------------ read-back
@@ -526,11 +585,11 @@ class Layer final : public LayerBase {
   void set_graphs(bool on) override {
     graphs_ = on;
     if (!on)
-      for (Graph* g : {&gfwd_, &gbwd_})
-        if (g->exec) {
-          SPL_CUDA(cudaGraphExecDestroy(g->exec));
-          g->exec = nullptr;
-        }
+      for (auto* set : {&gfwd_, &gbwd_}) {
+        for (Graph& g : *set)
+          if (g.exec) SPL_CUDA(cudaGraphExecDestroy(g.exec));
+        set->clear();
+      }
   }
 
  private:
@@ -681,10 +740,10 @@ class Layer final : public LayerBase {
     nonfinite_ = alloc<int>(1, kWork, 0);
   }
 
-  void ensure_staging() {
+  void ensure_staging() {  // [rank][slot][x, dy, y, dx]
     if (!stage_.empty()) return;
     for (int r = 0; r < L_; ++r)
-      for (int i = 0; i < 4; ++i) stage_.push_back(alloc<T>(RL_ * h_, kWork, r));
+      for (int i = 0; i < 8; ++i) stage_.push_back(alloc<T>(RL_ * h_, kWork, r));
   }
 
   // ---- launch bookkeeping
@@ -1061,7 +1120,10 @@ class Layer final : public LayerBase {
   DropKey k_soft_{}, k_attn_{}, k_mlp_{};
   cudaStream_t st_ = nullptr;
   cudaEvent_t ev_in_ = nullptr, ev_out_ = nullptr, ev_fork_ = nullptr, ev_bits_ = nullptr;
-  cudaStream_t st_rng_ = nullptr;  // side stream: data-independent dropout keep bits
+  cudaStream_t st_rng_ = nullptr;
+  cudaStream_t st_up_ = nullptr, st_down_ = nullptr;  // host-step H2D / D2H copies
+  cudaEvent_t ev_x_[2] = {}, ev_dy_[2] = {}, ev_f_[2] = {}, ev_b_[2] = {}, ev_free_[2] = {};
+  uint64_t host_steps_ = 0;  // side stream: data-independent dropout keep bits
   cudaStream_t st_comm_ = nullptr;  // backward collectives overlapped with the GEMMs
   cudaEvent_t ev_cfork_ = nullptr, ev_regather_ = nullptr, ev_rs_ = nullptr;
   cudaStream_t caller_ = 0;  // legacy default stream unless set
@@ -1076,7 +1138,7 @@ class Layer final : public LayerBase {
   bool bits_pending_ = false;
   bool bits_serial_ = true;  // SPL_KEEPBITS_SIDE=1: RNG pass on the side stream
   bool graphs_ = false;
-  Graph gfwd_, gbwd_;
+  std::vector<Graph> gfwd_, gbwd_;
   // profiling
   struct Pending {
     cudaEvent_t a, b;

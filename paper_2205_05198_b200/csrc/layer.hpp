@@ -37,6 +37,8 @@ class LayerBase {
   virtual void forward(const void* const* x, void* const* y) = 0;
   virtual void backward(const void* const* dy, void* const* dx) = 0;
   virtual void step_host(const void* x, const void* dy, void* y, void* dx) = 0;
+  virtual void step_host_async(const void* x, const void* dy, void* y, void* dx) = 0;
+  virtual void step_host_wait() = 0;
   virtual void get_grads(double* packed) = 0;
   virtual void get_w1_grad_shard(int r, double* out) = 0;
   virtual void get_saved(int r, const std::string& name, double* out, int64_t n) = 0;

@@ -173,6 +173,15 @@ class SeqparLayer:
         check(lib().spl_step_host(self._h, x_host.data_ptr(), dy_host.data_ptr(),
                                   y_host.data_ptr(), dx_host.data_ptr()))
 
+    def step_host_async(self, x_host, dy_host, y_host, dx_host):
+        """Issue one host-buffer step (spl_step_host_async); buffers stay in use until
+        step_host_wait()."""
+        check(lib().spl_step_host_async(self._h, x_host.data_ptr(), dy_host.data_ptr(),
+                                        y_host.data_ptr(), dx_host.data_ptr()))
+
+    def step_host_wait(self):
+        check(lib().spl_step_host_wait(self._h))
+
     # ---- read-back
     def grads(self) -> np.ndarray:
         out = np.empty(param_count(self.cfg.hidden), np.float64)

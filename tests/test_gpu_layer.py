@@ -336,3 +336,57 @@ def test_cuda_graphs_bit_identical(spl, orc, t, recompute):
     assert all(torch.equal(a, b) for a, b in zip(de, dg))
     assert np.array_equal(ge, gg)
     assert le == lg  # graph replays are counted like the eager launches
+
+
+@pytest.mark.parametrize("t,pinned", [(1, True), (2, True), (1, False)])
+def test_step_host_matches_device_step(spl, orc, t, pinned):
+    """spl_step_host (the end-to-end path bench.py's e2e uses: H2D x/dy, fwd, bwd, D2H y/dx,
+    copies overlapped with compute on a copy stream) equals the device-buffer calls bit-for-bit,
+    for pinned and pageable host buffers, over repeated steps."""
+    import torch
+    cfg, x, dy, p = make_case(orc, dict(heads=8, hidden=512, seq=256, batch=2), key=11)
+    c = to_spl_cfg(spl, cfg)
+    A = spl.SeqparLayer(c, t, "selective", True, "bf16", check_finite=False)
+    B = spl.SeqparLayer(c, t, "selective", True, "bf16", check_finite=False)
+    A.load_params(p)
+    B.load_params(p)
+    xs = [torch.from_numpy(s.copy()).to("cuda", torch.bfloat16) for s in np.split(x, t, 0)]
+    ds = [torch.from_numpy(s.copy()).to("cuda", torch.bfloat16) for s in np.split(dy, t, 0)]
+    hx, hdy = torch.cat(xs).cpu(), torch.cat(ds).cpu()
+    hy, hdx = torch.empty_like(hx), torch.empty_like(hx)
+    if pinned:
+        hx, hdy, hy, hdx = hx.pin_memory(), hdy.pin_memory(), hy.pin_memory(), hdx.pin_memory()
+    for _ in range(3):
+        y = A.forward(xs)
+        dx = A.backward(ds)
+        B.step_host(hx, hdy, hy, hdx)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(y).cpu(), hy)
+    assert torch.equal(torch.cat(dx).cpu(), hdx)
+    assert np.array_equal(A.grads(), B.grads())
+
+
+def test_step_host_async_pipelined(spl, orc):
+    """Several spl_step_host_async calls in flight over two host buffer sets (the bench's e2e
+    loop) give every step the same results as synchronous device calls."""
+    import torch
+    cfg, x, dy, p = make_case(orc, dict(heads=8, hidden=512, seq=256, batch=2), key=12)
+    c = to_spl_cfg(spl, cfg)
+    A = spl.SeqparLayer(c, 1, "selective", True, "bf16", check_finite=False)
+    B = spl.SeqparLayer(c, 1, "selective", True, "bf16", check_finite=False)
+    A.load_params(p)
+    B.load_params(p)
+    xs = [torch.from_numpy(x).to("cuda", torch.bfloat16)]
+    ds = [torch.from_numpy(dy).to("cuda", torch.bfloat16)]
+    y = A.forward(xs)[0].cpu()
+    dx = A.backward(ds)[0].cpu()
+    hx = [xs[0].cpu().pin_memory() for _ in range(2)]
+    hdy = [ds[0].cpu().pin_memory() for _ in range(2)]
+    hy = [torch.full_like(hx[0], float("nan")).pin_memory() for _ in range(2)]
+    hdx = [torch.full_like(hx[0], float("nan")).pin_memory() for _ in range(2)]
+    for i in range(5):
+        B.step_host_async(hx[i & 1], hdy[i & 1], hy[i & 1], hdx[i & 1])
+    B.step_host_wait()
+    for j in range(2):
+        assert torch.equal(hy[j], y) and torch.equal(hdx[j], dx)
+    assert np.array_equal(A.grads(), B.grads())
