@@ -47,9 +47,11 @@ template <int HD>
 struct FwdCfg {
   static constexpr int ATOMS = (HD + 63) / 64;
   static constexpr int TILE = ATOMS * kAtomBytes;  // one 128-row tile of Q, K or V
+  // K/V ring depth: 2 stages up to head_dim 128; head_dim 160 (3 atoms, 48 KB tiles) fits one
+  static constexpr int KVS = HD > 128 ? 1 : 2;
   static constexpr int Q_OFF = 0;
-  static constexpr int KV_OFF = TILE;             // [2 stages][K tile, V tile]
-  static constexpr int P_OFF = KV_OFF + 4 * TILE; // [2][128 x 128 bf16]
+  static constexpr int KV_OFF = TILE;                   // [KVS stages][K tile, V tile]
+  static constexpr int P_OFF = KV_OFF + KVS * 2 * TILE; // [2][128 x 128 bf16]
   static constexpr int P_BYTES = 2 * kAtomBytes;
   static constexpr int BAR_OFF = P_OFF + 2 * P_BYTES;
   // [2 halves][128 rows] (m, l) exchanged between pass 1 and pass 2, when the P buffers are
@@ -127,8 +129,8 @@ __global__ void __launch_bounds__(320, 1)
       for (int pass = 0; pass < PASSES; ++pass) {
         const bool with_v = pass == PASSES - 1;
         for (int j = 0; j < nkv; ++j, ++it) {
-          const int st = it & 1;
-          mbar_wait(&kv_empty[st], ((it >> 1) & 1) ^ 1);
+          const int st = it % Cfg::KVS;
+          mbar_wait(&kv_empty[st], ((it / Cfg::KVS) & 1) ^ 1);
           uint8_t* Kt = KVs + st * 2 * Cfg::TILE;
           uint8_t* Vt = Kt + Cfg::TILE;
           mbar_expect_tx(&kv_full[st], (with_v ? 2 : 1) * Cfg::TILE);
@@ -152,8 +154,8 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(q_full, 0);
       int it = 0, sc = 0;
       auto issue_s = [&](int stage_it) {  // S[sc%2] = Q · K(stage)ᵀ
-        const int st = stage_it & 1;
-        mbar_wait(&kv_full[st], (stage_it >> 1) & 1);
+        const int st = stage_it % Cfg::KVS;
+        mbar_wait(&kv_full[st], (stage_it / Cfg::KVS) & 1);
         const int sb = sc & 1;
         mbar_wait(&s_free[sb], ((sc >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -170,18 +172,21 @@ __global__ void __launch_bounds__(320, 1)
       if constexpr (MAT) {  // pass 1 (statistics only)
         for (int j = 0; j < nkv; ++j, ++it) {
           issue_s(it);
-          umma_commit(&kv_empty[it & 1]);
+          umma_commit(&kv_empty[it % Cfg::KVS]);
         }
       }
-      // pass 2: S_{j+1} is issued before PV_j so the softmax of j+1 can start early
+      // pass 2: S_{j+1} is issued before PV_j so the softmax of j+1 can start early — unless
+      // the K/V ring has one stage (head_dim 160), where K_{j+1} can only arrive after PV_j
+      // has released the stage
+      constexpr bool kAhead = Cfg::KVS > 1;
       const int base = it;
       issue_s(base);
       for (int j = 0; j < nkv; ++j) {
-        if (j + 1 < nkv) issue_s(base + j + 1);
+        if (kAhead && j + 1 < nkv) issue_s(base + j + 1);
         const int pb = j & 1;
         mbar_wait(&p_full[pb], (j >> 1) & 1);
         tc_fence_after();
-        const int st = (base + j) & 1;
+        const int st = (base + j) % Cfg::KVS;
         const uint32_t pa = smem_u32(Ps + pb * Cfg::P_BYTES);
         const uint32_t vb = smem_u32(KVs + st * 2 * Cfg::TILE + Cfg::TILE);
 #pragma unroll
@@ -193,6 +198,7 @@ __global__ void __launch_bounds__(320, 1)
         umma_commit(&p_free[pb]);
         umma_commit(&kv_empty[st]);
         umma_commit(o_done);
+        if (!kAhead && j + 1 < nkv) issue_s(base + j + 1);
       }
       umma_commit(o_full);
     }
@@ -555,6 +561,7 @@ namespace {
 template <int HD, bool CAUSAL, bool MAT>
 void launch_fwd_umma(const AttnArgs& a, cudaStream_t st) {
   using Cfg = FwdCfg<HD>;
+  static_assert(Cfg::SMEM <= 232448, "attention forward: smem over the limit");
   static bool once = [] {
     SPL_CUDA(cudaFuncSetAttribute(fa_fwd_umma<HD, CAUSAL, MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   Cfg::SMEM));
@@ -578,7 +585,7 @@ void launch_fwd_umma_hd(const AttnArgs& a, cudaStream_t st) {
 }  // namespace
 
 bool attn_fwd_umma_supported(const AttnArgs& a) {
-  const bool hd_ok = a.hd == 64 || a.hd == 96 || a.hd == 128;
+  const bool hd_ok = a.hd == 64 || a.hd == 96 || a.hd == 128 || a.hd == 160;
   const bool regime_ok = a.sm == nullptr
                              ? a.lse != nullptr
                              : (a.mask != nullptr && a.sd != nullptr && a.s % 64 == 0 &&
@@ -594,6 +601,7 @@ void attn_fwd_umma(const AttnArgs& a, cudaStream_t st) {
     case 64: return launch_fwd_umma_hd<64>(a, st);
     case 96: return launch_fwd_umma_hd<96>(a, st);
     case 128: return launch_fwd_umma_hd<128>(a, st);
+    case 160: return launch_fwd_umma_hd<160>(a, st);
     default: raise(3, "attn_fwd_umma: unsupported head_dim");
   }
 }

@@ -77,7 +77,7 @@ struct DkdvLayout {
     // (Q, dO) ring depth: 3 stages keep the TMA of tile it+2 in flight while tile it's dV/dK
     // MMAs run (2 stages exposed the TMA latency between them); the stored variant needs its
     // smem for the P / mask tiles.
-    static constexpr int NS = STORED ? 2 : 3;
+    static constexpr int NS = HD > 128 ? 1 : (STORED ? 2 : 3);
     static constexpr int K_OFF = 0;
     static constexpr int V_OFF = STORED ? 0 : C::T128;
     static constexpr int QD_OFF = V_OFF + C::T128;
@@ -129,7 +129,11 @@ __global__ void __launch_bounds__(320, 1)
             qcol = (int)(a.qoff + (int64_t)hl * HD), dcol = hl * HD;
   const int64_t brow = ((int64_t)hl * a.b + bj) * a.s;
   // TMEM columns: Sᵀ [0,64) [64,128), dPᵀ [128,192) [192,256), dV [256,+HD), dK [384,+HD)
-  constexpr uint32_t DV_COL = 256, DK_COL = 384;
+  // TMEM: Sᵀ and dPᵀ in SB buffers of 64 columns each, then dV and dK (HD columns each).
+  // head_dim 160 single-buffers Sᵀ/dPᵀ to fit 64 + 64 + 160 + 160 <= 512 columns.
+  constexpr int SB = HD > 128 ? 1 : 2;
+  constexpr uint32_t S_COL = 0, DP_COL = SB * 64, DV_COL = 2 * SB * 64;
+  constexpr uint32_t DK_COL = DV_COL + (HD > 128 ? HD : 128);
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
@@ -186,9 +190,9 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t ka = smem_u32(smem + K_OFF), va = smem_u32(smem + V_OFF);
       mbar_wait(kv_full, 0);
       auto issue_sd = [&](int it) {
-        const int st = it & 1, qs = it % NS;
+        const int sb = it % SB, qs = it % NS;
         mbar_wait(&qd_full[qs], (it / NS) & 1);
-        mbar_wait(&sd_free[st], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&sd_free[sb], ((it / SB) & 1) ^ 1);
         tc_fence_after();
         const uint32_t qb = smem_u32(smem + QD_OFF + qs * 2 * C::T64), db = qb + C::T64;
 #pragma unroll
@@ -196,16 +200,19 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t oa = (kk >> 2) * C::A128 + (kk & 3) * 32;
           const uint32_t ob = (kk >> 2) * C::A64 + (kk & 3) * 32;
           if (!STORED)
-            umma_bf16(tmem + st * 64, smem_desc(ka + oa, 16, 1024), smem_desc(qb + ob, 16, 1024),
+            umma_bf16(tmem + S_COL + sb * 64, smem_desc(ka + oa, 16, 1024), smem_desc(qb + ob, 16, 1024),
                       idesc_sd, kk > 0 ? 1u : 0u);
-          umma_bf16(tmem + 128 + st * 64, smem_desc(va + oa, 16, 1024),
+          umma_bf16(tmem + DP_COL + sb * 64, smem_desc(va + oa, 16, 1024),
                     smem_desc(db + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
         }
-        umma_commit(&sd_full[st]);
+        umma_commit(&sd_full[sb]);
       };
+      // look ahead one tile (Sᵀ/dPᵀ of it+1 before dV/dK of it) unless the (Q, dO) ring has a
+      // single stage, where tile it+1 can only load after tile it's MMAs released it
+      constexpr bool kAhead = NS > 1;
       if (nq > 0) issue_sd(0);
       for (int it = 0; it < nq; ++it) {
-        if (it + 1 < nq) issue_sd(it + 1);
+        if (kAhead && it + 1 < nq) issue_sd(it + 1);
         const int st = it & 1, qs = it % NS;
         mbar_wait(&w_full[st], (it >> 1) & 1);
         tc_fence_after();
@@ -221,6 +228,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         umma_commit(&w_free[st]);
         umma_commit(&qd_empty[qs]);
+        if (!kAhead && it + 1 < nq) issue_sd(it + 1);
       }
       umma_commit(acc_full);
     }
@@ -259,15 +267,16 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t kw_l = kw_n;
       row_stats(it + 1, lse_n, dl_n, kw_n);
       if (STORED) mbar_wait(&qd_full[it % NS], (it / NS) & 1);  // stored P / mask tiles landed
-      mbar_wait(&sd_full[st], (it >> 1) & 1);
+      const int sb = it % SB;
+      mbar_wait(&sd_full[sb], (it / SB) & 1);
       tc_fence_after();
       uint32_t rs[32], rp[32];
-      if (!STORED) tmem_ld32_nw(tl + st * 64 + half * 32, rs);
-      tmem_ld32_nw(tl + 128 + st * 64 + half * 32, rp);
+      if (!STORED) tmem_ld32_nw(tl + S_COL + sb * 64 + half * 32, rs);
+      tmem_ld32_nw(tl + DP_COL + sb * 64 + half * 32, rp);
       tmem_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sd_free[st]);
+      if (lane == 0) mbar_arrive(&sd_free[sb]);
       mbar_wait(&w_free[st], ((it >> 1) & 1) ^ 1);
       const int q0h = qb + 32 * half;
       uint32_t pw[16], dw[16];
@@ -357,7 +366,8 @@ struct DqLayout {
   static constexpr int SMT = 128 * 64 * 2, MKT = 128 * 64;
   template <bool STORED>
   struct L {
-    static constexpr int NS = STORED ? 2 : 4;  // (K, V [, P, mask]) ring depth
+    // (K, V [, P, mask]) ring depth (head_dim 160: 48 KB K/V tiles leave room for fewer)
+    static constexpr int NS = HD > 128 ? (STORED ? 1 : 2) : (STORED ? 2 : 4);
     static constexpr int Q_OFF = 0, D_OFF = C::T128, KV_OFF = 2 * C::T128;
     static constexpr int W_OFF = KV_OFF + NS * 2 * C::T64;
     static constexpr int SMM_OFF = W_OFF + 2 * C::W_BYTES;
@@ -478,9 +488,10 @@ __global__ void __launch_bounds__(320, 1)
         }
         umma_commit(&sd_full[st]);
       };
+      constexpr bool kAhead = NS > 1;  // see the dK/dV kernel
       if (nkv > 0) issue_sd(0);
       for (int it = 0; it < nkv; ++it) {
-        if (it + 1 < nkv) issue_sd(it + 1);
+        if (kAhead && it + 1 < nkv) issue_sd(it + 1);
         const int st = it & 1, ks = it % NS;
         mbar_wait(&w_full[st], (it >> 1) & 1);
         tc_fence_after();
@@ -492,6 +503,7 @@ __global__ void __launch_bounds__(320, 1)
                     smem_desc(kb + kk * 2048, C::A64, 1024), idesc_acc, (it | kk) != 0 ? 1u : 0u);
         umma_commit(&w_free[st]);
         umma_commit(&kv_empty[ks]);
+        if (!kAhead && it + 1 < nkv) issue_sd(it + 1);
       }
       umma_commit(acc_full);
     }
@@ -654,7 +666,7 @@ void launch_bwd_umma(const AttnArgs& a, const bf16* dout, bf16* dqkv, const floa
 }  // namespace
 
 bool attn_bwd_umma_supported(const AttnArgs& a) {
-  const bool hd_ok = a.hd == 64 || a.hd == 96 || a.hd == 128;
+  const bool hd_ok = a.hd == 64 || a.hd == 96 || a.hd == 128 || a.hd == 160;
   const bool regime_ok =
       a.sm == nullptr ? (a.lse != nullptr && (a.keepbits != nullptr || a.drop.thresh == 0))
                       : (a.mask != nullptr && a.s % 64 == 0 && ((uintptr_t)a.sm & 15) == 0 &&
@@ -678,6 +690,7 @@ void attn_bwd_umma(const AttnArgs& a, const void* dout, void* dqkv, const float*
     SPL_BWD_CASE(64)
     SPL_BWD_CASE(96)
     SPL_BWD_CASE(128)
+    SPL_BWD_CASE(160)
     default: raise(3, "attn_bwd_umma: unsupported head_dim");
   }
 #undef SPL_BWD_CASE
