@@ -16,6 +16,7 @@
 //   stored softmax_out must be normalised when it is written.
 // TMEM: S double-buffered (2 × 128 fp32 columns) + O (HD columns). MMAs of tile j+1 overlap
 // the softmax of tile j. SMEM: Q 32 KB, 2 × (K, V) 128 KB, 2 × P 64 KB.
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -43,17 +44,18 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int HD>
+template <int HD, bool PT>
 struct FwdCfg {
   static constexpr int ATOMS = (HD + 63) / 64;
   static constexpr int TILE = ATOMS * kAtomBytes;  // one 128-row tile of Q, K or V
-  // K/V ring depth: 2 stages up to head_dim 128; head_dim 160 (3 atoms, 48 KB tiles) fits one
-  static constexpr int KVS = HD > 128 ? 1 : 2;
+  // K/V ring depth: head_dim <= 128 takes 2 stages, or 3 when P̃ lives in TMEM (PT) and its
+  // 64 KB of smem are free; head_dim 160 (3 atoms, 48 KB tiles) fits one.
+  static constexpr int KVS = HD > 128 ? 1 : (PT ? 3 : 2);
   static constexpr int Q_OFF = 0;
   static constexpr int KV_OFF = TILE;                   // [KVS stages][K tile, V tile]
-  static constexpr int P_OFF = KV_OFF + KVS * 2 * TILE; // [2][128 x 128 bf16]
+  static constexpr int P_OFF = KV_OFF + KVS * 2 * TILE; // [2][128 x 128 bf16] (!PT)
   static constexpr int P_BYTES = 2 * kAtomBytes;
-  static constexpr int BAR_OFF = P_OFF + 2 * P_BYTES;
+  static constexpr int BAR_OFF = P_OFF + (PT ? 0 : 2 * P_BYTES);
   // [2 halves][128 rows] (m, l) exchanged between pass 1 and pass 2, when the P buffers are
   // not in use yet (smem is at the 227 KB limit for HD = 96/128)
   static constexpr int STAT_OFF = P_OFF;
@@ -66,10 +68,12 @@ struct FwdCfg {
 // softmax_out P, the softmax-dropout mask (the raw keep bit at every position, block.cpp:
 // 392-394) and softmax_dropout_out P·mask/(1-p) — as {lh, b, s, s} rows (bf16, u8, bf16);
 // every key tile is visited (causal-masked tiles still carry mask bits).
-template <int HD, bool CAUSAL, bool MAT>
+// PT (single pass only): P̃ goes to TMEM (over the consumed half of its S buffer) and the
+// P̃·V MMA reads A from TMEM, instead of a swizzled smem tile + proxy fence.
+template <int HD, bool CAUSAL, bool MAT, bool PT>
 __global__ void __launch_bounds__(320, 1)
     fa_fwd_umma(const __grid_constant__ CUtensorMap map_qkv, AttnArgs a) {
-  using Cfg = FwdCfg<HD>;
+  using Cfg = FwdCfg<HD, PT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* Qs = smem + Cfg::Q_OFF;
@@ -77,15 +81,15 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* Ps = smem + Cfg::P_OFF;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
   uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;    // [2]
-  uint64_t* s_free = bar + 7;    // [2]
-  uint64_t* p_full = bar + 9;    // [2]
-  uint64_t* p_free = bar + 11;   // [2]
-  uint64_t* o_full = bar + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
-  uint64_t* o_done = bar + 15;   // one phase per P̃·V MMA (single pass: gates O rescaling)
+  uint64_t* kv_full = bar + 1;   // [3] (KVS used)
+  uint64_t* kv_empty = bar + 4;  // [3]
+  uint64_t* s_full = bar + 7;    // [2]
+  uint64_t* s_free = bar + 9;    // [2]
+  uint64_t* p_full = bar + 11;   // [2]
+  uint64_t* p_free = bar + 13;   // [2]
+  uint64_t* o_full = bar + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t* o_done = bar + 17;   // one phase per P̃·V MMA (single pass: gates O rescaling)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q0 = blockIdx.x * 128;
@@ -98,9 +102,11 @@ __global__ void __launch_bounds__(320, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < Cfg::KVS; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], 8);
       mbar_init(&p_full[i], 8);
@@ -191,9 +197,14 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t vb = smem_u32(KVs + st * 2 * Cfg::TILE + Cfg::TILE);
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk) {
-          const uint64_t ad = smem_desc(pa + (kk >> 2) * kAtomBytes + (kk & 3) * 32, 16, 1024);
           const uint64_t bd = smem_desc(vb + kk * 2048, kAtomBytes, 1024);
-          umma_bf16(tmem + Cfg::O_COL, ad, bd, idesc_o, (j | kk) != 0 ? 1u : 0u);
+          if constexpr (PT) {  // P̃ of tile j over the first 64 columns of its S buffer
+            const uint32_t ta = tmem + (uint32_t)(((base + j) & 1) * 128 + kk * 8);
+            umma_bf16_ts(tmem + Cfg::O_COL, ta, bd, idesc_o, (j | kk) != 0 ? 1u : 0u);
+          } else {
+            const uint64_t ad = smem_desc(pa + (kk >> 2) * kAtomBytes + (kk & 3) * 32, 16, 1024);
+            umma_bf16(tmem + Cfg::O_COL, ad, bd, idesc_o, (j | kk) != 0 ? 1u : 0u);
+          }
         }
         umma_commit(&p_free[pb]);
         umma_commit(&kv_empty[st]);
@@ -463,14 +474,18 @@ __global__ void __launch_bounds__(320, 1)
           pk[i >> 1] = pack_bf16(p2[0], p2[1]);
         }
         l += ls;
-        uint8_t* prow = Ps + pb * Cfg::P_BYTES + row * 128;
-  #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int phys = u ^ (row & 7);
-          *reinterpret_cast<uint4*>(prow + half * kAtomBytes + phys * 16) =
-              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        if constexpr (PT) {
+          tmem_st32u(tl + sb * 128 + half * 32, pk);  // keys 64*half.. as bf16 pairs
+        } else {
+          uint8_t* prow = Ps + pb * Cfg::P_BYTES + row * 128;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int phys = u ^ (row & 7);
+            *reinterpret_cast<uint4*>(prow + half * kAtomBytes + phys * 16) =
+                make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          }
+          fence_proxy_async();
         }
-        fence_proxy_async();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[pb]);
@@ -558,27 +573,39 @@ CUtensorMap attn_seq_map(const void* ptr, int64_t width, int64_t b, int64_t s, i
 
 namespace {
 
-template <int HD, bool CAUSAL, bool MAT>
+template <int HD, bool CAUSAL, bool MAT, bool PT>
 void launch_fwd_umma(const AttnArgs& a, cudaStream_t st) {
-  using Cfg = FwdCfg<HD>;
+  using Cfg = FwdCfg<HD, PT>;
   static_assert(Cfg::SMEM <= 232448, "attention forward: smem over the limit");
   static bool once = [] {
-    SPL_CUDA(cudaFuncSetAttribute(fa_fwd_umma<HD, CAUSAL, MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  Cfg::SMEM));
+    SPL_CUDA(cudaFuncSetAttribute(fa_fwd_umma<HD, CAUSAL, MAT, PT>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     return true;
   }();
   (void)once;
   const CUtensorMap mq = attn_seq_map(a.qkv, a.ld, a.b, a.s, a.ld, 128);
   dim3 grid((unsigned)((a.s + 127) / 128), (unsigned)(a.lh * a.b));
-  fa_fwd_umma<HD, CAUSAL, MAT><<<grid, 320, Cfg::SMEM, st>>>(mq, a);
+  fa_fwd_umma<HD, CAUSAL, MAT, PT><<<grid, 320, Cfg::SMEM, st>>>(mq, a);
   SPL_CHECK_LAUNCH();
+}
+bool fwd_p_tmem() {
+  static const bool on = [] {
+    const char* e = std::getenv("SPL_ATTN_P_TMEM");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
 }
 template <int HD>
 void launch_fwd_umma_hd(const AttnArgs& a, cudaStream_t st) {
   if (a.sm != nullptr) {
-    if (a.causal) launch_fwd_umma<HD, true, true>(a, st); else launch_fwd_umma<HD, false, true>(a, st);
+    if (a.causal) launch_fwd_umma<HD, true, true, false>(a, st);
+    else launch_fwd_umma<HD, false, true, false>(a, st);
+  } else if (fwd_p_tmem()) {
+    if (a.causal) launch_fwd_umma<HD, true, false, true>(a, st);
+    else launch_fwd_umma<HD, false, false, true>(a, st);
   } else {
-    if (a.causal) launch_fwd_umma<HD, true, false>(a, st); else launch_fwd_umma<HD, false, false>(a, st);
+    if (a.causal) launch_fwd_umma<HD, true, false, false>(a, st);
+    else launch_fwd_umma<HD, false, false, false>(a, st);
   }
 }
 
