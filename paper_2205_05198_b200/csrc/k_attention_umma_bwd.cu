@@ -77,12 +77,14 @@ struct DkdvLayout {
     // (Q, dO) ring depth: 3 stages keep the TMA of tile it+2 in flight while tile it's dV/dK
     // MMAs run (2 stages exposed the TMA latency between them); the stored variant needs its
     // smem for the P / mask tiles.
-    static constexpr int NS = HD > 128 ? 1 : (STORED ? 2 : 3);
+    // Recompute regimes keep P̃ᵀ and dSᵀ in TMEM (TS-form MMA), which frees the 64 KB of smem
+    // the stored variant still uses for them; the (Q, dO) ring takes it.
+    static constexpr int NS = HD > 128 ? (STORED ? 1 : 2) : (STORED ? 2 : 4);
     static constexpr int K_OFF = 0;
     static constexpr int V_OFF = STORED ? 0 : C::T128;
     static constexpr int QD_OFF = V_OFF + C::T128;
     static constexpr int W_OFF = QD_OFF + NS * 2 * C::T64;
-    static constexpr int SMM_OFF = W_OFF + 4 * C::W_BYTES;
+    static constexpr int SMM_OFF = W_OFF + (STORED ? 4 * C::W_BYTES : 0);
     static constexpr int BAR_OFF = SMM_OFF + (STORED ? NS * (SMT + MKT) : 0);
     static constexpr int SMEM = BAR_OFF + 256 + 1024;
   };
@@ -209,7 +211,7 @@ __global__ void __launch_bounds__(320, 1)
       };
       // look ahead one tile (Sᵀ/dPᵀ of it+1 before dV/dK of it) unless the (Q, dO) ring has a
       // single stage, where tile it+1 can only load after tile it's MMAs released it
-      constexpr bool kAhead = NS > 1;
+      constexpr bool kAhead = NS > 1 && SB > 1;  // (single S/dP buffer: P̃ᵀ/dSᵀ live in it)
       if (nq > 0) issue_sd(0);
       for (int it = 0; it < nq; ++it) {
         if (kAhead && it + 1 < nq) issue_sd(it + 1);
@@ -218,13 +220,22 @@ __global__ void __launch_bounds__(320, 1)
         tc_fence_after();
         const uint32_t pw = smem_u32(smem + W_OFF + st * 2 * C::W_BYTES), dw = pw + C::W_BYTES;
         const uint32_t qb = smem_u32(smem + QD_OFF + qs * 2 * C::T64), db = qb + C::T64;
+        const int sb = it % SB;
 #pragma unroll
         for (int kk = 0; kk < 64 / 16; ++kk) {
           // dV += P̃ᵀ·dO ; dK += dSᵀ·Q  (B = dO / Q tiles read MN-major)
-          umma_bf16(tmem + DV_COL, smem_desc(pw + kk * 32, 16, 1024),
-                    smem_desc(db + kk * 2048, C::A64, 1024), idesc_acc, (it | kk) != 0 ? 1u : 0u);
-          umma_bf16(tmem + DK_COL, smem_desc(dw + kk * 32, 16, 1024),
-                    smem_desc(qb + kk * 2048, C::A64, 1024), idesc_acc, (it | kk) != 0 ? 1u : 0u);
+          const uint64_t bdo = smem_desc(db + kk * 2048, C::A64, 1024);
+          const uint64_t bq = smem_desc(qb + kk * 2048, C::A64, 1024);
+          if constexpr (!STORED) {  // A from TMEM: queries 32h.. of half h at columns 32h..+16
+            const uint32_t col = (uint32_t)(sb * 64 + (kk >> 1) * 32 + (kk & 1) * 8);
+            umma_bf16_ts(tmem + DV_COL, tmem + S_COL + col, bdo, idesc_acc, (it | kk) != 0 ? 1u : 0u);
+            umma_bf16_ts(tmem + DK_COL, tmem + DP_COL + col, bq, idesc_acc, (it | kk) != 0 ? 1u : 0u);
+          } else {
+            umma_bf16(tmem + DV_COL, smem_desc(pw + kk * 32, 16, 1024), bdo, idesc_acc,
+                      (it | kk) != 0 ? 1u : 0u);
+            umma_bf16(tmem + DK_COL, smem_desc(dw + kk * 32, 16, 1024), bq, idesc_acc,
+                      (it | kk) != 0 ? 1u : 0u);
+          }
         }
         umma_commit(&w_free[st]);
         umma_commit(&qd_empty[qs]);
@@ -310,18 +321,26 @@ __global__ void __launch_bounds__(320, 1)
         pw[i >> 1] = pack_bf16(pv[0], pv[1]);
         dw[i >> 1] = pack_bf16(dv[0], dv[1]);
       }
-      // [128 keys x 64 queries] K-major SW128 tiles: this half's queries = chunks 4h..4h+3
-      uint8_t* prow = smem + W_OFF + st * 2 * C::W_BYTES + row * 128;
-      uint8_t* drow = prow + C::W_BYTES;
+      if constexpr (!STORED) {
+        // P̃ᵀ / dSᵀ as bf16 pairs over the first 16 of this half's (consumed) 32 Sᵀ / dPᵀ columns
+        tmem_st16u(tl + S_COL + sb * 64 + half * 32, pw);
+        tmem_st16u(tl + DP_COL + sb * 64 + half * 32, dw);
+        tmem_st_wait();
+        tc_fence_before();
+      } else {
+        // [128 keys x 64 queries] K-major SW128 tiles: this half's queries = chunks 4h..4h+3
+        uint8_t* prow = smem + W_OFF + st * 2 * C::W_BYTES + row * 128;
+        uint8_t* drow = prow + C::W_BYTES;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int phys = (4 * half + u) ^ (row & 7);
-        *reinterpret_cast<uint4*>(prow + phys * 16) =
-            make_uint4(pw[4 * u], pw[4 * u + 1], pw[4 * u + 2], pw[4 * u + 3]);
-        *reinterpret_cast<uint4*>(drow + phys * 16) =
-            make_uint4(dw[4 * u], dw[4 * u + 1], dw[4 * u + 2], dw[4 * u + 3]);
+        for (int u = 0; u < 4; ++u) {
+          const int phys = (4 * half + u) ^ (row & 7);
+          *reinterpret_cast<uint4*>(prow + phys * 16) =
+              make_uint4(pw[4 * u], pw[4 * u + 1], pw[4 * u + 2], pw[4 * u + 3]);
+          *reinterpret_cast<uint4*>(drow + phys * 16) =
+              make_uint4(dw[4 * u], dw[4 * u + 1], dw[4 * u + 2], dw[4 * u + 3]);
+        }
+        fence_proxy_async();
       }
-      fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&w_full[st]);
     }
@@ -367,10 +386,11 @@ struct DqLayout {
   template <bool STORED>
   struct L {
     // (K, V [, P, mask]) ring depth (head_dim 160: 48 KB K/V tiles leave room for fewer)
-    static constexpr int NS = HD > 128 ? (STORED ? 1 : 2) : (STORED ? 2 : 4);
+    // recompute regimes: dS in TMEM (TS-form MMA), its 32 KB of smem go to the ring
+    static constexpr int NS = HD > 128 ? (STORED ? 1 : 2) : (STORED ? 2 : 5);
     static constexpr int Q_OFF = 0, D_OFF = C::T128, KV_OFF = 2 * C::T128;
     static constexpr int W_OFF = KV_OFF + NS * 2 * C::T64;
-    static constexpr int SMM_OFF = W_OFF + 2 * C::W_BYTES;
+    static constexpr int SMM_OFF = W_OFF + (STORED ? 2 * C::W_BYTES : 0);
     static constexpr int BAR_OFF = SMM_OFF + (STORED ? NS * (SMT + MKT) : 0);
     static constexpr int SMEM = BAR_OFF + 256 + 1024;
   };
@@ -498,9 +518,16 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t dsw = smem_u32(smem + W_OFF + st * C::W_BYTES);
         const uint32_t kb = smem_u32(smem + KV_OFF + ks * 2 * C::T64);
 #pragma unroll
-        for (int kk = 0; kk < 64 / 16; ++kk)
-          umma_bf16(tmem + DQ_COL, smem_desc(dsw + kk * 32, 16, 1024),
-                    smem_desc(kb + kk * 2048, C::A64, 1024), idesc_acc, (it | kk) != 0 ? 1u : 0u);
+        for (int kk = 0; kk < 64 / 16; ++kk) {
+          const uint64_t bk = smem_desc(kb + kk * 2048, C::A64, 1024);
+          if constexpr (!STORED) {  // dS from TMEM: keys 32h.. of half h at columns 32h..+16
+            const uint32_t col = (uint32_t)(st * 64 + (kk >> 1) * 32 + (kk & 1) * 8);
+            umma_bf16_ts(tmem + DQ_COL, tmem + col, bk, idesc_acc, (it | kk) != 0 ? 1u : 0u);
+          } else {
+            umma_bf16(tmem + DQ_COL, smem_desc(dsw + kk * 32, 16, 1024), bk, idesc_acc,
+                      (it | kk) != 0 ? 1u : 0u);
+          }
+        }
         umma_commit(&w_free[st]);
         umma_commit(&kv_empty[ks]);
         if (!kAhead && it + 1 < nkv) issue_sd(it + 1);
@@ -576,14 +603,20 @@ __global__ void __launch_bounds__(320, 1)
         }
         dw[i >> 1] = pack_bf16(dv[0], dv[1]);
       }
-      uint8_t* drow = smem + W_OFF + st * C::W_BYTES + row * 128;
+      if constexpr (!STORED) {
+        tmem_st16u(tl + st * 64 + half * 32, dw);  // over this half's consumed S columns
+        tmem_st_wait();
+        tc_fence_before();
+      } else {
+        uint8_t* drow = smem + W_OFF + st * C::W_BYTES + row * 128;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int phys = (4 * half + u) ^ (row & 7);
-        *reinterpret_cast<uint4*>(drow + phys * 16) =
-            make_uint4(dw[4 * u], dw[4 * u + 1], dw[4 * u + 2], dw[4 * u + 3]);
+        for (int u = 0; u < 4; ++u) {
+          const int phys = (4 * half + u) ^ (row & 7);
+          *reinterpret_cast<uint4*>(drow + phys * 16) =
+              make_uint4(dw[4 * u], dw[4 * u + 1], dw[4 * u + 2], dw[4 * u + 3]);
+        }
+        fence_proxy_async();
       }
-      fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&w_full[st]);
     }
