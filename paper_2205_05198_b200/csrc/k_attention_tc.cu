@@ -137,9 +137,17 @@ __global__ void __launch_bounds__(256) keep_bits_k(DropKey key, int64_t head_off
         if (blo <= 0xffffffffu - 31u) {  // no carry into the high half inside this word
           const uint32_t hx = bhi ^ (bhi >> 30);
           const uint32_t hc = hx * 0x1ce4e5b9u;
+          if ((blo >> 30) == ((blo + 31u) >> 30)) {
+            const uint32_t c30 = __funnelshift_r(blo, bhi, 30);
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (keep_fast(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm)) word |= 1u << j;
+            for (int j = 0; j < 32; ++j)
+              if (keep_fast<true>(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm, c30))
+                word |= 1u << j;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (keep_fast(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm)) word |= 1u << j;
+          }
         } else {
 #pragma unroll 1
           for (int j = 0; j < 32; ++j)

@@ -48,12 +48,18 @@ __device__ __forceinline__ void xs_fma(uint32_t& lo, uint32_t& hi, uint32_t m) {
   lo = lo ^ a ^ b;
   hi ^= c;
 }
+// C30: the caller guarantees lo >> 30 is the same for every key of the word, so the low half
+// of the first xor-shift is a word constant: c30 = funnelshift_r(lo, hi0, 30) (one op per key
+// saved, 2.3 % of the pass; tools/micro/bench_rng2.cu).
+template <bool C30 = false>
 __device__ __forceinline__ bool keep_fast(uint32_t lo, uint32_t hi0, uint32_t hc,
                                           uint32_t hi_xs, uint32_t mixed_lo, uint32_t mixed_hi,
-                                          uint32_t t_lo, uint32_t t_hi, const ShiftMuls& sm) {
+                                          uint32_t t_lo, uint32_t t_hi, const ShiftMuls& sm,
+                                          uint32_t c30 = 0) {
   // first mix_post; the high half (hi0) is loop-invariant: hi_xs = hi0 ^ (hi0 >> 30) and
   // hc = hi_xs * 0x1ce4e5b9 are precomputed per 32-key word.
-  lo ^= __funnelshift_r(lo, hi0, 30);
+  if constexpr (C30) lo ^= c30;
+  else lo ^= __funnelshift_r(lo, hi0, 30);
   uint32_t hi;
   {
     const uint64_t w = (uint64_t)lo * 0x1ce4e5b9u + ((uint64_t)hc << 32);

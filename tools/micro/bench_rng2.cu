@@ -8,8 +8,8 @@ using namespace spl::rngk;
 template <int VAR>
 __device__ __forceinline__ bool keep_var(uint32_t lo, uint32_t hi0, uint32_t hc, uint32_t mixed_lo,
                                          uint32_t mixed_hi, uint32_t t_lo, uint32_t t_hi,
-                                         const ShiftMuls& sm) {
-  lo ^= __funnelshift_r(lo, hi0, 30);
+                                         const ShiftMuls& sm, uint32_t c30 = 0) {
+  if (VAR & 64) lo ^= c30; else lo ^= __funnelshift_r(lo, hi0, 30);
   uint32_t hi;
   {
     const uint64_t w = (uint64_t)lo * 0x1ce4e5b9u + ((uint64_t)hc << 32);
@@ -18,9 +18,15 @@ __device__ __forceinline__ bool keep_var(uint32_t lo, uint32_t hi0, uint32_t hc,
   }
   if (VAR & 1) xs_alu(lo, hi, 27); else xs_fma(lo, hi, sm.m27);
   mul_c<0x133111ebu, 0x94d049bbu>(lo, hi);
-  if (VAR & 2) xs_alu(lo, hi, 31); else xs_fma(lo, hi, sm.m31);
-  lo ^= mixed_lo;
-  hi ^= mixed_hi;
+  if (VAR & 32) {  // xor-shift 31 fused with ^ mix64(key) into 3-input LOP3s
+    const uint32_t f = __funnelshift_r(lo, hi, 31), g = hi >> 31;
+    lo = lo ^ f ^ mixed_lo;
+    hi = hi ^ g ^ mixed_hi;
+  } else {
+    if (VAR & 2) xs_alu(lo, hi, 31); else xs_fma(lo, hi, sm.m31);
+    lo ^= mixed_lo;
+    hi ^= mixed_hi;
+  }
   {
     const uint64_t w = ((uint64_t)hi << 32 | lo) + 0x9e3779b97f4a7c15ULL;
     hi = (uint32_t)(w >> 32);
@@ -60,9 +66,16 @@ __global__ void __launch_bounds__(256) kb(uint64_t mixed, uint64_t tsh, int nrow
       if (blo <= 0xffffffffu - 31u) {
         const uint32_t hx = bhi ^ (bhi >> 30);
         const uint32_t hc = hx * 0x1ce4e5b9u;
+        if ((VAR & 64) && (blo >> 30) == ((blo + 31u) >> 30)) {  // lo >> 30 constant in the word
+          const uint32_t c30 = __funnelshift_r(blo, bhi, 30);
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (keep_var<VAR>(blo + j, bhi, hc, mixed_lo, mixed_hi, t_lo, t_hi, sm)) word |= 1u << j;
+          for (int j = 0; j < 32; ++j)
+            if (keep_var<VAR>(blo + j, bhi, hc, mixed_lo, mixed_hi, t_lo, t_hi, sm, c30)) word |= 1u << j;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (keep_var<VAR & ~64>(blo + j, bhi, hc, mixed_lo, mixed_hi, t_lo, t_hi, sm)) word |= 1u << j;
+        }
       }
       if (check) {
         uint32_t ref = 0;
@@ -104,15 +117,12 @@ int main() {
   int* bad;
   cudaMalloc(&bits, (size_t)nrows * W * 4);
   cudaMalloc(&bad, 4);
-  run<0>(bits, bad, nrows, W, s);
-  run<3>(bits, bad, nrows, W, s);
-  run<7>(bits, bad, nrows, W, s);
   run<11>(bits, bad, nrows, W, s);
-  run<5>(bits, bad, nrows, W, s);
-  run<6>(bits, bad, nrows, W, s);
-  run<2>(bits, bad, nrows, W, s);
-  run<3>(bits, bad, nrows, W, s);
-  run<0>(bits, bad, nrows, W, s);
+  run<43>(bits, bad, nrows, W, s);
+  run<75>(bits, bad, nrows, W, s);
+  run<107>(bits, bad, nrows, W, s);
+  run<11>(bits, bad, nrows, W, s);
+  run<107>(bits, bad, nrows, W, s);
   printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
