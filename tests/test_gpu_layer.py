@@ -390,3 +390,33 @@ def test_step_host_async_pipelined(spl, orc):
     for j in range(2):
         assert torch.equal(hy[j], y) and torch.equal(hdx[j], dx)
     assert np.array_equal(A.grads(), B.grads())
+
+
+@pytest.mark.parametrize("shape,t", [(dict(heads=32, hidden=3072, seq=256, batch=2), 8),    # head_dim 96
+                                     (dict(heads=16, hidden=2560, seq=256, batch=1), 8)])   # head_dim 160
+def test_full_width_self_consistency(spl, orc, shape, t):
+    """SURVEY.md §8c for shapes beyond what the fp64 oracle runs in seconds: the same layer on t
+    simulated ranks (SP) equals the one-rank layer (same seed, masks identical by construction),
+    and the three recompute regimes agree, within the bf16 tolerances."""
+    import torch
+    cfg = orc.BlockConfig(**shape, dropout_p=0.1, seed=42)
+    c = to_spl_cfg(spl, cfg)
+    shp = (cfg.seq, cfg.batch, cfg.hidden)
+    g = torch.Generator().manual_seed(5)
+    x = (torch.rand(shp, generator=g) * 2 - 1).to(torch.bfloat16)
+    dy = (torch.rand(shp, generator=g) * 2 - 1).to(torch.bfloat16)
+    res = {}
+    for tt, rc in ((1, "selective"), (t, "selective"), (t, "none"), (t, "full")):
+        L = spl.SeqparLayer(c, tt, rc, True, "bf16", check_finite=False)
+        L.init_params(77)
+        xs = [u.contiguous().cuda() for u in torch.chunk(x, tt, 0)]
+        ds = [u.contiguous().cuda() for u in torch.chunk(dy, tt, 0)]
+        y = torch.cat(L.forward(xs)).float().cpu()
+        dx = torch.cat(L.backward(ds)).float().cpu()
+        res[(tt, rc)] = (y.numpy(), dx.numpy(), L.grads())
+        L.close()
+    ref = res[(1, "selective")]
+    for key, (y, dx, gr) in res.items():
+        assert rel_l2(y, ref[0]) <= 1e-2, key
+        assert rel_l2(dx, ref[1]) <= 1e-2, key
+        assert rel_l2(gr, ref[2]) <= 2e-2, key
