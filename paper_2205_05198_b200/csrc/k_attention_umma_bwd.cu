@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(320, 1)
       kw_o = 0u;
       dl_o = (it < nq && q < S) ? delta[brow + q] : 0.f;
       if (!STORED && it < nq) {
-        lse_o = q < S ? a.lse[brow + q] * kLog2e : INFINITY;
+        lse_o = q < S ? a.lse[brow + q] : INFINITY;  // scaled at use: keeps the load in flight
         kw_o = !drop_on ? 0xffffffffu
                : (q < S && (k0 >> 5) + qd < W) ? kbits[(brow + q) * W + (k0 >> 5) + qd] : 0u;
       }
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(320, 1)
     for (int it = 0; it < nq; ++it) {
       const int st = it & 1;
       const int qb = q_start + it * 64;
-      const float lse_l = lse_n, dl_l = dl_n;
+      const float lse_l = lse_n * kLog2e, dl_l = dl_n;
       const uint32_t kw_l = kw_n;
       row_stats(it + 1, lse_n, dl_n, kw_n);
       if (STORED) mbar_wait(&qd_full[it % NS], (it / NS) & 1);  // stored P / mask tiles landed
