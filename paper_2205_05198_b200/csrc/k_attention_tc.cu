@@ -112,7 +112,7 @@ struct Rng {
 // fmaheavy ran at 89% (ncu) and the all-funnel-shift form is 7% faster (tools/micro/
 // bench_rng2.cu), so keep_fast uses funnel shifts throughout.
 
-__global__ void __launch_bounds__(256) keep_bits_k(DropKey key, int64_t head_offset, int lh,
+__global__ void __launch_bounds__(1024, 1) keep_bits_k(DropKey key, int64_t head_offset, int lh,
                                                    int b, int s, int W, int causal,
                                                    uint32_t* __restrict__ bits, ShiftMuls sm) {
   const Rng rng(key);
@@ -875,9 +875,11 @@ void attn_keep_bits(const AttnArgs& a, cudaStream_t st) {
   require(a.lh * a.b * a.s < (1ll << 31), "keep bits: too many rows");
   const int W = (int)((a.s + 31) / 32);
   const int64_t rows = a.lh * a.b * a.s;
-  int64_t grid = (rows + 7) / 8;  // 8 warps (rows) per CTA
-  if (grid > kNumSMs * 16) grid = kNumSMs * 16;
-  keep_bits_k<<<(unsigned)grid, 256, 0, st>>>(a.drop, a.head_offset, (int)a.lh, (int)a.b,
+  // one 1024-thread CTA per SM (64 registers a thread: more independent hashes in flight per
+  // warp than 8 x 256 threads at 32 registers; 1.84 vs 1.92 ms per 22B pass, bench_rng2.cu)
+  int64_t grid = (rows + 31) / 32;  // 32 warps (rows) per CTA
+  if (grid > kNumSMs) grid = kNumSMs;
+  keep_bits_k<<<(unsigned)grid, 1024, 0, st>>>(a.drop, a.head_offset, (int)a.lh, (int)a.b,
                                               (int)a.s, W, a.causal, a.keepbits,
                                               ShiftMuls{4u, 32u, 2u, 1u});
   SPL_CHECK_LAUNCH();

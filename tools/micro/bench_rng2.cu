@@ -50,8 +50,8 @@ __device__ __forceinline__ bool keep_ref(uint64_t mixed, uint64_t tsh, uint64_t 
   return mix_post((mix_post(idx_cg) ^ mixed) + kG) >= tsh;
 }
 
-template <int VAR>
-__global__ void __launch_bounds__(256) kb(uint64_t mixed, uint64_t tsh, int nrows, int W, int s,
+template <int VAR, int NT = 256, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) kb(uint64_t mixed, uint64_t tsh, int nrows, int W, int s,
                                           uint32_t* bits, ShiftMuls sm, int check, int* bad) {
   const uint32_t mixed_lo = (uint32_t)mixed, mixed_hi = (uint32_t)(mixed >> 32);
   const uint32_t t_lo = (uint32_t)tsh, t_hi = (uint32_t)(tsh >> 32);
@@ -87,28 +87,29 @@ __global__ void __launch_bounds__(256) kb(uint64_t mixed, uint64_t tsh, int nrow
   }
 }
 
-template <int VAR>
-void run(uint32_t* bits, int* bad, int nrows, int W, int s) {
+template <int VAR, int NT = 256, int MINB = 1>
+void run(uint32_t* bits, int* bad, int nrows, int W, int s, int ctas_per_sm = 8) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   ShiftMuls sm{4u, 32u, 2u, 1u};
   const uint64_t mixed = 0x1234567890abcdefULL, tsh = 0x1999999999999800ULL;
   cudaMemset(bad, 0, 4);
-  kb<VAR><<<148 * 4, 256>>>(mixed, tsh, nrows / 64, W, s, bits, sm, 1, bad);
+  kb<VAR, NT, MINB><<<148 * 4, NT>>>(mixed, tsh, nrows / 64, W, s, bits, sm, 1, bad);
   int nb = 0;
   cudaMemcpy(&nb, bad, 4, cudaMemcpyDeviceToHost);
-  const int grid = 148 * 8;
-  kb<VAR><<<grid, 256>>>(mixed, tsh, nrows, W, s, bits, sm, 0, bad);
+  const int grid = 148 * ctas_per_sm;
+  kb<VAR, NT, MINB><<<grid, NT>>>(mixed, tsh, nrows, W, s, bits, sm, 0, bad);
   cudaEventRecord(a);
-  for (int i = 0; i < 5; ++i) kb<VAR><<<grid, 256>>>(mixed, tsh, nrows, W, s, bits, sm, 0, bad);
+  for (int i = 0; i < 5; ++i) kb<VAR, NT, MINB><<<grid, NT>>>(mixed, tsh, nrows, W, s, bits, sm, 0, bad);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
   cudaEventElapsedTime(&ms, a, b);
   cudaFuncAttributes at;
-  cudaFuncGetAttributes(&at, kb<VAR>);
-  printf("VAR %2d regs=%3d  %.3f ms  mismatches=%d\n", VAR, at.numRegs, ms / 5, nb);
+  cudaFuncGetAttributes(&at, kb<VAR, NT, MINB>);
+  printf("VAR %3d NT %3d MINB %d ctas/SM %2d regs=%3d  %.3f ms  mismatches=%d\n", VAR, NT, MINB,
+         ctas_per_sm, at.numRegs, ms / 5, nb);
 }
 
 int main() {
@@ -117,12 +118,12 @@ int main() {
   int* bad;
   cudaMalloc(&bits, (size_t)nrows * W * 4);
   cudaMalloc(&bad, 4);
-  run<11>(bits, bad, nrows, W, s);
-  run<43>(bits, bad, nrows, W, s);
-  run<75>(bits, bad, nrows, W, s);
-  run<107>(bits, bad, nrows, W, s);
-  run<11>(bits, bad, nrows, W, s);
-  run<107>(bits, bad, nrows, W, s);
+  run<75, 256, 8>(bits, bad, nrows, W, s, 8);
+  run<75, 512, 1>(bits, bad, nrows, W, s, 1);
+  run<75, 512, 2>(bits, bad, nrows, W, s, 2);
+  run<75, 256, 4>(bits, bad, nrows, W, s, 4);
+  run<75, 1024, 1>(bits, bad, nrows, W, s, 1);
+  run<75, 256, 8>(bits, bad, nrows, W, s, 8);
   printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
