@@ -1123,7 +1123,7 @@ class Layer final : public LayerBase {
   cudaStream_t st_rng_ = nullptr;
   cudaStream_t st_up_ = nullptr, st_down_ = nullptr;  // host-step H2D / D2H copies
   cudaEvent_t ev_x_[2] = {}, ev_dy_[2] = {}, ev_f_[2] = {}, ev_b_[2] = {}, ev_free_[2] = {};
-  uint64_t host_steps_ = 0;  // side stream: data-independent dropout keep bits
+  uint64_t host_steps_ = 0;
   cudaStream_t st_comm_ = nullptr;  // backward collectives overlapped with the GEMMs
   cudaEvent_t ev_cfork_ = nullptr, ev_regather_ = nullptr, ev_rs_ = nullptr;
   cudaStream_t caller_ = 0;  // legacy default stream unless set
