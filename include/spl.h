@@ -172,6 +172,12 @@ int spl_total_first_stage_bytes(int64_t a, int64_t h, int64_t s, int64_t b, int6
                                 int64_t interleave, int64_t act_bytes, int64_t mask_bytes,
                                 int64_t* bytes_out);
 
+/* Per-layer, per-rank communication volume of the tensor-parallel (4 all-reduces) or the
+ * tensor+sequence-parallel schedule (4 all-gathers + 4 reduce-scatters): the reference's
+ * layer_comm_bytes_tensor_parallel / _tensor_sequence (collectives.cpp:75-87). */
+int spl_layer_comm_bytes(int64_t s, int64_t b, int64_t h, int64_t t, int64_t elem_bytes,
+                         int sequence_parallel, int64_t* bytes_out);
+
 /* Layer stack: L layers of one desc (layer l uses layer_index = d->layer_index + l, so every
  * layer draws its own dropout masks) on t simulated ranks, sharing ONE transient workspace;
  * each layer keeps only its own saved activations. The p = 1 stage that

@@ -5,4 +5,5 @@ from ._lib import lib, header_symbols, SplError, SplStateError  # noqa: F401
 from .seqpar import (BlockConfig, SeqparLayer, SeqparForward, SeqparBackward,  # noqa: F401
                      seqpar_block_forward, seqpar_block_backward, per_layer_bytes,
                      per_layer_bytes_exact, param_count, PARAM_NAMES, SeqparStack,
-                     layer_component_breakdown, percent_of_baseline, total_first_stage_bytes)
+                     layer_component_breakdown, percent_of_baseline, total_first_stage_bytes,
+                     layer_comm_bytes)

@@ -89,6 +89,7 @@ def lib():
         "spl_percent_of_baseline": (I32, [I64, I64, I64, I64, I64, I32, I32, I64, I64, P(I64), P(I64)]),
         "spl_total_first_stage_bytes": (I32, [I64, I64, I64, I64, I64, I32, I32, I64, I64, I64,
                                               I64, I64, P(I64)]),
+        "spl_layer_comm_bytes": (I32, [I64, I64, I64, I64, I64, I32, P(I64)]),
         "spl_stack_create_local": (I32, [P(LayerDesc), I32, I32, I32, P(H)]),
         "spl_stack_destroy": (I32, [H]),
         "spl_stack_layers": (I32, [H]),

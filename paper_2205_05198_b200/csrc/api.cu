@@ -381,6 +381,20 @@ int spl_total_first_stage_bytes(int64_t a, int64_t hh, int64_t s, int64_t b, int
   });
 }
 
+int spl_layer_comm_bytes(int64_t s, int64_t b, int64_t hh, int64_t t, int64_t elem_bytes,
+                         int sequence_parallel, int64_t* bytes_out) {
+  return guard([&] {
+    spl::require(s >= 1 && b >= 1 && hh >= 1 && t >= 1 && elem_bytes >= 1 && bytes_out != nullptr,
+                 "shape fields must be >= 1");
+    const __int128 tensor = (__int128)s * b * hh * elem_bytes;
+    // collectives.cpp:75-87: 4 all-reduces at 2(t-1)/t each, or 4 all-gathers + 4
+    // reduce-scatters at (t-1)/t each — the same volume, 8·(N/t)·(t-1)
+    const __int128 v = sequence_parallel ? (__int128)8 * (tensor / t) * (t - 1)
+                                         : (__int128)4 * 2 * (tensor / t) * (t - 1);
+    *bytes_out = fit64(v);
+  });
+}
+
 int spl_stack_create_local(const spl_layer_desc* d, int device, int t, int layers,
                            spl_stack** out) {
   return guard([&] {

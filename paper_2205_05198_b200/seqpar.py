@@ -364,6 +364,14 @@ def total_first_stage_bytes(a, h, s, b, t, kind, sequence_parallel, layers, pipe
     return out.value
 
 
+def layer_comm_bytes(s: int, b: int, h: int, t: int, elem: int = 2,
+                     sequence_parallel: bool = True) -> int:
+    """layer_comm_bytes_tensor_sequence / _tensor_parallel (collectives.cpp:75-87)."""
+    out = C.c_int64()
+    check(lib().spl_layer_comm_bytes(s, b, h, t, elem, int(sequence_parallel), C.byref(out)))
+    return out.value
+
+
 class SeqparStack:
     """L layers (layer_index = cfg.layer_index + l) on t simulated ranks sharing one workspace
     (spl_stack_*): the p = 1 stage of total_first_stage_bytes / simulate_memory."""

@@ -83,3 +83,13 @@ def test_accountant_extras_match_oracle(orc):
         else:
             assert spl.total_first_stage_bytes(a, h, s, b, t, kind, sp, L, p, m, act, mask) == \
                 orc.total_first_stage_bytes(a, h, s, b, t, kind, sp, L, p, m, act, mask)
+
+
+def test_layer_comm_bytes_match_oracle(orc):
+    """collectives.cpp:75-87 through the C ABI: SP and TP move the same volume (verify.cpp:285-321)."""
+    for (s, b, h) in ((2048, 4, 6144), (2048, 1, 12288), (128, 2, 256), (2048, 1, 25600)):
+        for t in (1, 2, 4, 8):
+            sp = spl.layer_comm_bytes(s, b, h, t, 2, True)
+            tp = spl.layer_comm_bytes(s, b, h, t, 2, False)
+            assert sp == orc.layer_comm_bytes_sp(s, b, h, t) and tp == orc.layer_comm_bytes_tp(s, b, h, t)
+            assert sp == tp == (0 if t == 1 else 8 * (2 * s * b * h // t) * (t - 1))

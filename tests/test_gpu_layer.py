@@ -224,6 +224,7 @@ def test_comm_log_counts(spl, orc):
     assert c["schedule"]["all_reduces"] == 0
     assert c["regather"]["all_gathers"] == 2 and c["grad_sync"]["all_reduces"] == 6
     assert c["schedule"]["ring_elements"] * 2 == orc.layer_comm_bytes_sp(cfg.seq, cfg.batch, cfg.hidden, 2)
+    assert c["schedule"]["ring_elements"] * 2 == spl.layer_comm_bytes(cfg.seq, cfg.batch, cfg.hidden, 2, 2, True)
 
 
 def test_errors(spl, orc):
