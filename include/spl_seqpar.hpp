@@ -10,6 +10,10 @@
 //   ActivationLedger            block.hpp:61-73         ActivationLedger (+ physical bytes)
 //   CommLog                     collectives.hpp:30-52   CommLog
 //   per_layer_bytes             activation_memory.hpp:83 per_layer_bytes
+//   layer_component_breakdown   activation_memory.cpp:84 layer_component_breakdown
+//   percent_of_baseline         activation_memory.cpp:195 percent_of_baseline (num/den)
+//   total_first_stage_bytes     activation_memory.cpp:119 total_first_stage_bytes
+//   layer_comm_bytes_tensor_*   collectives.cpp:75-87   layer_comm_bytes_tensor_parallel/_sequence
 // Errors: std::invalid_argument / std::domain_error exactly where the reference throws them.
 // Tensors are host fp64 (as in the reference); device buffers are managed here with the CUDA
 // runtime; the layer computes in fp32 (exact) or bf16 on the GPU.
@@ -362,6 +366,55 @@ inline int64_t per_layer_bytes(int64_t a, int64_t h, int64_t s, int64_t b, int64
                                int64_t mask = 1) {
   int64_t out = 0;
   check(spl_per_layer_bytes(a, h, s, b, t, (int)kind, sequence_parallel ? 1 : 0, act, mask, &out));
+  return out;
+}
+
+// layer_component_breakdown (activation_memory.cpp:84-104), serial layer
+struct LayerMemoryBreakdown {
+  int64_t attention = 0, mlp = 0, layer_norms = 0, total = 0;
+};
+inline LayerMemoryBreakdown layer_component_breakdown(int64_t a, int64_t h, int64_t s, int64_t b,
+                                                      int64_t act = 2, int64_t mask = 1) {
+  int64_t o[4];
+  check(spl_layer_component_breakdown(a, h, s, b, act, mask, o));
+  return {o[0], o[1], o[2], o[3]};
+}
+
+// percent_of_baseline (activation_memory.cpp:195-200) as an exact fraction
+struct Fraction {
+  int64_t num = 0, den = 1;
+};
+inline Fraction percent_of_baseline(int64_t a, int64_t h, int64_t s, int64_t b, int64_t t,
+                                    RecomputeKind kind, bool sequence_parallel, int64_t act = 2,
+                                    int64_t mask = 1) {
+  Fraction f;
+  check(spl_percent_of_baseline(a, h, s, b, t, (int)kind, sequence_parallel ? 1 : 0, act, mask,
+                                &f.num, &f.den));
+  return f;
+}
+
+// total_first_stage_bytes (activation_memory.cpp:112-123): L layers, p stages, m interleave
+inline int64_t total_first_stage_bytes(int64_t a, int64_t h, int64_t s, int64_t b, int64_t t,
+                                       RecomputeKind kind, bool sequence_parallel, int64_t layers,
+                                       int64_t pipeline = 1, int64_t interleave = 1,
+                                       int64_t act = 2, int64_t mask = 1) {
+  int64_t out = 0;
+  check(spl_total_first_stage_bytes(a, h, s, b, t, (int)kind, sequence_parallel ? 1 : 0, layers,
+                                    pipeline, interleave, act, mask, &out));
+  return out;
+}
+
+// layer_comm_bytes_tensor_parallel / _tensor_sequence (collectives.cpp:75-87)
+inline int64_t layer_comm_bytes_tensor_parallel(int64_t seq, int64_t batch, int64_t hidden,
+                                                int64_t t, int64_t elem_bytes) {
+  int64_t out = 0;
+  check(spl_layer_comm_bytes(seq, batch, hidden, t, elem_bytes, 0, &out));
+  return out;
+}
+inline int64_t layer_comm_bytes_tensor_sequence(int64_t seq, int64_t batch, int64_t hidden,
+                                                int64_t t, int64_t elem_bytes) {
+  int64_t out = 0;
+  check(spl_layer_comm_bytes(seq, batch, hidden, t, elem_bytes, 1, &out));
   return out;
 }
 

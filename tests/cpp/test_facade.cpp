@@ -168,6 +168,15 @@ int main() {
     CHECK(seqpar::per_layer_bytes(64, 6144, 2048, 4, 1, K::None, false) == 7079985152LL);
     CHECK(seqpar::per_layer_bytes(64, 6144, 2048, 4, 8, K::None, true) == 884998144LL);
     CHECK(seqpar::per_layer_bytes(64, 6144, 2048, 4, 8, K::Selective, true) == 213909504LL);
+    // test_activation_memory.cpp:59-66, 97-99, 198-206; collectives.cpp:75-87
+    const auto bd = seqpar::layer_component_breakdown(2, 8, 4, 1);
+    CHECK(bd.attention == 512 && bd.mlp == 608 && bd.layer_norms == 128 && bd.total == 1248);
+    const auto pb = seqpar::percent_of_baseline(128, 20480, 2048, 1, 8, K::Selective, true);
+    CHECK(pb.num == 17 && pb.den == 84);
+    CHECK(seqpar::total_first_stage_bytes(128, 20480, 2048, 1, 8, K::Selective, true, 105, 35, 3) ==
+          24777850880LL);
+    CHECK(seqpar::layer_comm_bytes_tensor_sequence(2048, 4, 6144, 8, 2) ==
+          seqpar::layer_comm_bytes_tensor_parallel(2048, 4, 6144, 8, 2));
   }
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
