@@ -67,7 +67,6 @@ __device__ __forceinline__ bool keep_fast(uint32_t lo, uint32_t hi0, uint32_t hc
     lo = (uint32_t)w;
   }
   (void)hi_xs;
-  (void)sm;
   // Every xor-shift in funnel-shift (ALU) form: measured fastest on B200 (tools/micro/
   // bench_rng2.cu: 1.97 ms vs 2.12 ms for three in IMAD.HI form, 1.07e9 keys).
   xs_alu(lo, hi, 27);
@@ -76,9 +75,9 @@ __device__ __forceinline__ bool keep_fast(uint32_t lo, uint32_t hi0, uint32_t hc
   // ^ mix64(key), + G (64-bit add as IMAD.WIDE with a 64-bit addend)
   lo ^= mixed_lo;
   hi ^= mixed_hi;
-  {
-    const uint64_t w = ((uint64_t)hi << 32 | lo) + 0x9e3779b97f4a7c15ULL;
-    hi = (uint32_t)(w >> 32);
+  {  // 64-bit + G as IMAD.WIDE.U32 (lo * sm.one + G: moves an ALU op to the FMA pipe)
+    const uint64_t w = (uint64_t)lo * sm.one + 0x9e3779b97f4a7c15ULL;
+    hi = hi + (uint32_t)(w >> 32);
     lo = (uint32_t)w;
   }
   xs_alu(lo, hi, 30);
