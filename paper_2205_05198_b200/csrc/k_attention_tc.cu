@@ -836,8 +836,6 @@ void attn_fwd_tc<bf16>(const AttnArgs& a, cudaStream_t st) {
   });
 }
 
-bool attn_bwd_self_rng(const AttnArgs&) { return false; }
-
 static bool umma_bwd_on(const AttnArgs& a) {
   static const bool off = [] {
     const char* e = std::getenv("SPL_ATTN_UMMA");

@@ -59,6 +59,7 @@ struct FwdCfg {
   // [2 halves][128 rows] (m, l) exchanged between pass 1 and pass 2, when the P buffers are
   // not in use yet (smem is at the 227 KB limit for HD = 96/128)
   static constexpr int STAT_OFF = P_OFF;
+  static_assert(STAT_OFF % 1024 == 0, "stats exchange area alignment");
   static constexpr int XCH_OFF = BAR_OFF + 256;  // [2 halves][128 rows] floats (single pass)
   static constexpr int SMEM = XCH_OFF + 1024 + 1024;
   static constexpr int O_COL = 256;  // O accumulator columns [256, 256 + HD)

@@ -139,16 +139,14 @@ template <typename T>
 void attn_bwd(const AttnArgs& a, const void* dout, void* dqkv, float* delta, cudaStream_t st);
 // The counter-RNG pass alone: fills a.keepbits (data-independent; may run on a side stream).
 void attn_keep_bits(const AttnArgs& a, cudaStream_t st);
-// tcgen05/TMEM forward (selective regime, bf16, head_dim 64/96/128); used by attn_fwd<bf16>.
+// tcgen05/TMEM forward (bf16, head_dim 64/96/128/160; recompute regimes single-pass, the
+// no-recompute regime writes the stored interior); used by attn_fwd<bf16>.
 bool attn_fwd_umma_supported(const AttnArgs& a);
 void attn_fwd_umma(const AttnArgs& a, cudaStream_t st);
-// tcgen05/TMEM backward (recompute regimes): the dK/dV kernel runs the counter RNG itself and
-// writes a.keepbits for the dQ kernel. delta = rowdot(dO, O) must be computed first.
+// tcgen05/TMEM backward (recompute regimes: keep bits from attn_keep_bits; no-recompute: the
+// stored interior). delta = rowdot(dO, O) must be computed first.
 bool attn_bwd_umma_supported(const AttnArgs& a);
 void attn_bwd_umma(const AttnArgs& a, const void* dout, void* dqkv, const float* delta,
                    cudaStream_t st);
-// True when attn_bwd<bf16> will take the tcgen05 path, which generates its own keep bits
-// (the caller then skips the attn_keep_bits pass before the backward).
-bool attn_bwd_self_rng(const AttnArgs& a);
 
 }  // namespace spl::k

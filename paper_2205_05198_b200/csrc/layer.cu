@@ -990,9 +990,7 @@ class Layer final : public LayerBase {
     const int64_t h = h_;
     // recompute regimes regenerate the keep bits (full recomputation just re-ran the forward,
     // whose bits are still in the buffer); the no-recompute regime reads the stored mask
-    if (kind_ == SPL_RECOMPUTE_SELECTIVE &&
-        !(std::is_same_v<T, bf16> && k::attn_bwd_self_rng(attn_args(0))))
-      fork_keep_bits();
+    if (kind_ == SPL_RECOMPUTE_SELECTIVE) fork_keep_bits();
     const double eb = sizeof(T);
     const int nch_l = k::num_chunks(RL_, kChunkRows), nch_f = k::num_chunks(RF_, kChunkRows);
     const float inv_keep = k_mlp_.inv_keep;
