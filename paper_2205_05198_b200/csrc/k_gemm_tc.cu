@@ -42,6 +42,37 @@ struct TileCfg {
   static constexpr int TMEM_COLS = BN;  // fp32 accumulator, one column per N
 };
 
+// ------------------------------------------------------------------ fast GELU for the bf16 epilogues
+// erf from Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7, far below the bf16 rounding of the
+// outputs): one ex2 and one reciprocal on the MUFU pipe plus six FMAs, and the GELU derivative
+// shares the exponential with the normal pdf. erff's longer FMA chain in the epilogue cost the
+// GELU'-fused FC2 dgrad ~14 % of its throughput under the power cap (tools/gemm_bench.py).
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// returns erf(x / sqrt 2); *e_out = exp(-x^2 / 2)
+__device__ __forceinline__ float erf_scaled(float x, float* e_out) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  const float e = __expf(-z * z);
+  const float t = rcp_approx(fmaf(0.3275911f, z, 1.f));
+  const float poly =
+      t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f),
+               0.254829592f);
+  *e_out = e;
+  return copysignf(1.f - poly * e, x);
+}
+__device__ __forceinline__ float gelu_fast(float x) {
+  float e;
+  return 0.5f * x * (1.f + erf_scaled(x, &e));
+}
+__device__ __forceinline__ float gelu_grad_fast(float x) {
+  float e;
+  const float cdf = 0.5f * (1.f + erf_scaled(x, &e));
+  return fmaf(x * 0.3989422804014327f, e, cdf);
+}
+
 // ------------------------------------------------------------------ epilogue store
 template <int EPI>
 __device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t m, int64_t n0,
@@ -78,7 +109,7 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t m, int64_
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const float pre = __bfloat162float(__float2bfloat16_rn(o[i]));
-        o2[i] = gelu_erf(pre);
+        o2[i] = gelu_fast(pre);
       }
     }
     if constexpr (EPI == (int)Epi::GeluBwd) {
@@ -89,10 +120,10 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t m, int64_
           const uint4 t = *reinterpret_cast<const uint4*>(ax + i);
           const bf16* e = reinterpret_cast<const bf16*>(&t);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) o[i + j] *= gelu_erf_grad(__bfloat162float(e[j]));
+          for (int j = 0; j < 8; ++j) o[i + j] *= gelu_grad_fast(__bfloat162float(e[j]));
         }
       } else {
-        for (int i = 0; i < 32 && n0 + i < g.N; ++i) o[i] *= gelu_erf_grad(__bfloat162float(ax[i]));
+        for (int i = 0; i < 32 && n0 + i < g.N; ++i) o[i] *= gelu_grad_fast(__bfloat162float(ax[i]));
       }
     }
     bf16* c = static_cast<bf16*>(g.C) + m * g.ldc + n0;
