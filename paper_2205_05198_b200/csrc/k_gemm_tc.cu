@@ -328,7 +328,7 @@ template <bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b, const GemmArgs g, int tiles_m,
-                        int tiles_n, int group) {
+                        int tiles_n, int group, int l2_hint) {
   constexpr int TN = 256;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -373,6 +373,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs), bytes counted on the leader's full[s]
       int it = 0;
+      const uint64_t pol_a = l2_hint ? l2_policy_evict_last() : l2_policy_evict_normal();
       for (int tile = pair; tile < ntiles; tile += npairs) {
         int mb, nb;
         tile_coords(tile, tiles_m, tiles_n, group, mb, nb);
@@ -386,11 +387,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * P_STAGE_BYTES);
           const uint32_t fb = mapa_rank(smem_u32(&full_bar[s]), 0);
           const int k0 = kb * BK;
+          // A panels are reused across the whole N sweep of a raster group: evict_last keeps
+          // them in L2 while B tiles and the epilogue's output stream through
           if (A_MN) {
-            tma_load_2d_pair(sa, &map_a, fb, m0, k0);
-            tma_load_2d_pair(sa + 8192, &map_a, fb, m0 + 64, k0);
+            tma_load_2d_pair_hint(sa, &map_a, fb, m0, k0, pol_a);
+            tma_load_2d_pair_hint(sa + 8192, &map_a, fb, m0 + 64, k0, pol_a);
           } else {
-            tma_load_2d_pair(sa, &map_a, fb, k0, m0);
+            tma_load_2d_pair_hint(sa, &map_a, fb, k0, m0, pol_a);
           }
           if (B_MN) {
             tma_load_2d_pair(sb, &map_b, fb, n0, k0);
@@ -591,7 +594,11 @@ void launch_pair(const GemmArgs& g, cudaStream_t st) {
   const int ntiles = tiles_m * tiles_n;
   const int pairs = ntiles < kNumSMs / 2 ? ntiles : kNumSMs / 2;
   const int group = pick_group(g.K, 256, 256, tiles_m, tiles_n, pairs);
-  kern<<<2 * pairs, kThreads, P_SMEM, st>>>(ma, mb, g, tiles_m, tiles_n, group);
+  static const int l2_hint = [] {
+    const char* e = std::getenv("SPL_GEMM_L2HINT");
+    return (e != nullptr && e[0] == '0') ? 0 : 1;
+  }();
+  kern<<<2 * pairs, kThreads, P_SMEM, st>>>(ma, mb, g, tiles_m, tiles_n, group, l2_hint);
   SPL_CHECK_LAUNCH();
 }
 
