@@ -90,10 +90,45 @@ class LocalComm final : public Comm {
     own_ = false;
   }
   ~LocalComm() override {
+    free_p2p();
     if (scratch_ && own_) cudaFree(scratch_);
   }
 
+  // simulated ranks: every rank's slots and counters are plain buffers on the one device
+  bool p2p_setup(size_t slot_bytes) override {
+    if (slot_bytes <= slot_bytes_) return true;
+    free_p2p();
+    slot_bytes_ = slot_bytes;
+    for (int q = 0; q < t_; ++q) {
+      void *sl = nullptr, *fl = nullptr;
+      SPL_CUDA(cudaMalloc(&sl, slot_bytes * t_));
+      SPL_CUDA(cudaMalloc(&fl, sizeof(uint32_t) * (t_ + 1)));
+      SPL_CUDA(cudaMemset(fl, 0, sizeof(uint32_t) * (t_ + 1)));
+      slots_.push_back(sl);
+      flags_.push_back(static_cast<uint32_t*>(fl));
+    }
+    return true;
+  }
+  void* p2p_slot(int dst, int src) override {
+    return static_cast<char*>(slots_[dst]) + (size_t)src * slot_bytes_;
+  }
+  uint32_t* p2p_flag(int dst, int src) override { return flags_[dst] + src; }
+  const void* p2p_slot_local(int dst, int src) override { return p2p_slot(dst, src); }
+  uint32_t* p2p_flags_local(int dst) override { return flags_[dst]; }
+  uint32_t* p2p_gen(int dst) override { return flags_[dst] + t_; }
+
  private:
+  void free_p2p() {
+    for (void* p : slots_) cudaFree(p);
+    for (uint32_t* p : flags_) cudaFree(p);
+    slots_.clear();
+    flags_.clear();
+    slot_bytes_ = 0;
+  }
+  std::vector<void*> slots_;
+  std::vector<uint32_t*> flags_;  // per rank: [t arrival counters, generation]
+  size_t slot_bytes_ = 0;
+
   void ensure_scratch(size_t bytes, cudaStream_t st) {
     if (bytes <= scratch_bytes_) return;
     if (scratch_ && own_) {
@@ -131,7 +166,67 @@ class NcclComm final : public Comm {
     SPL_NCCL(ncclCommInitRank(&comm_, t, uid, rank));
   }
   ~NcclComm() override {
+    for (size_t q = 0; q < peer_slots_.size(); ++q)
+      if ((int)q != rank0_ && peer_slots_[q]) {
+        cudaIpcCloseMemHandle(peer_slots_[q]);
+        cudaIpcCloseMemHandle(peer_flags_[q]);
+      }
+    if (slots_) cudaFree(slots_);
+    if (flags_) cudaFree(flags_);
     if (comm_) ncclCommDestroy(comm_);
+  }
+
+  // One process per GPU: this rank's slots and counters are exported with CUDA IPC, the t
+  // handle pairs exchanged with one ncclAllGather, and the peers' buffers mapped (NVLink P2P).
+  bool p2p_setup(size_t slot_bytes) override {
+    if (slot_bytes <= slot_bytes_) return true;
+    require(slots_ == nullptr, "fused reduce-scatter slots can only be sized once");
+    slot_bytes_ = slot_bytes;
+    SPL_CUDA(cudaMalloc(&slots_, slot_bytes * t_));
+    SPL_CUDA(cudaMalloc(&flags_, sizeof(uint32_t) * (t_ + 1)));
+    SPL_CUDA(cudaMemset(flags_, 0, sizeof(uint32_t) * (t_ + 1)));
+    cudaIpcMemHandle_t mine[2];
+    SPL_CUDA(cudaIpcGetMemHandle(&mine[0], slots_));
+    SPL_CUDA(cudaIpcGetMemHandle(&mine[1], flags_));
+    const size_t hb = sizeof(mine);
+    char* dev = nullptr;
+    SPL_CUDA(cudaMalloc(&dev, hb * (t_ + 1)));
+    SPL_CUDA(cudaMemcpy(dev + hb * t_, mine, hb, cudaMemcpyHostToDevice));
+    SPL_NCCL(ncclAllGather(dev + hb * t_, dev, hb, ncclUint8, comm_, 0));
+    SPL_CUDA(cudaStreamSynchronize(0));
+    std::vector<cudaIpcMemHandle_t> all(2 * t_);
+    SPL_CUDA(cudaMemcpy(all.data(), dev, hb * t_, cudaMemcpyDeviceToHost));
+    SPL_CUDA(cudaFree(dev));
+    peer_slots_.assign(t_, nullptr);
+    peer_flags_.assign(t_, nullptr);
+    for (int q = 0; q < t_; ++q) {
+      if (q == rank0_) {
+        peer_slots_[q] = slots_;
+        peer_flags_[q] = flags_;
+        continue;
+      }
+      SPL_CUDA(cudaIpcOpenMemHandle(&peer_slots_[q], all[2 * q], cudaIpcMemLazyEnablePeerAccess));
+      SPL_CUDA(cudaIpcOpenMemHandle(&peer_flags_[q], all[2 * q + 1], cudaIpcMemLazyEnablePeerAccess));
+    }
+    return true;
+  }
+  void* p2p_slot(int dst, int src) override {
+    return static_cast<char*>(peer_slots_[dst]) + (size_t)src * slot_bytes_;
+  }
+  uint32_t* p2p_flag(int dst, int src) override {
+    return static_cast<uint32_t*>(peer_flags_[dst]) + src;
+  }
+  const void* p2p_slot_local(int dst, int src) override {
+    (void)dst;
+    return static_cast<char*>(slots_) + (size_t)src * slot_bytes_;
+  }
+  uint32_t* p2p_flags_local(int dst) override {
+    (void)dst;
+    return static_cast<uint32_t*>(flags_);
+  }
+  uint32_t* p2p_gen(int dst) override {
+    (void)dst;
+    return static_cast<uint32_t*>(flags_) + t_;
   }
   void all_gather(const void* const* shard, void* const* full, int64_t n, DType dt,
                   cudaStream_t st) override {
@@ -150,6 +245,10 @@ class NcclComm final : public Comm {
 
  private:
   ncclComm_t comm_ = nullptr;
+  void* slots_ = nullptr;
+  void* flags_ = nullptr;
+  size_t slot_bytes_ = 0;
+  std::vector<void*> peer_slots_, peer_flags_;
 };
 
 }  // namespace

@@ -43,6 +43,21 @@ class Comm {
   // Use a caller-owned device buffer as that scratch (a layer's workspace, shared in a stack).
   virtual void use_scratch(void* p, size_t bytes) { (void)p; (void)bytes; }
 
+  // ---- landing slots of the reduce-scatter fused into the producing GEMM (peer memory).
+  // Destination rank q owns t slots of `slot_bytes` (one per source rank), t arrival counters
+  // and a generation counter. A source GEMM writes its rows of shard q straight into
+  // slot(q, src); signal() bumps q's counter for src; the consumer on q waits for all t
+  // counters to pass its generation, sums the slots in rank order and advances the generation.
+  // Counters live on the device, so the protocol survives CUDA-graph replays.
+  virtual bool p2p_setup(size_t slot_bytes) { (void)slot_bytes; return false; }
+  // writer side (device of `src`): q's slot for src, q's arrival counter for src
+  virtual void* p2p_slot(int dst, int src) { (void)dst; (void)src; return nullptr; }
+  virtual uint32_t* p2p_flag(int dst, int src) { (void)dst; (void)src; return nullptr; }
+  // reader side (device of `dst`): its slot array base, counters and generation
+  virtual const void* p2p_slot_local(int dst, int src) { (void)dst; (void)src; return nullptr; }
+  virtual uint32_t* p2p_flags_local(int dst) { (void)dst; return nullptr; }
+  virtual uint32_t* p2p_gen(int dst) { (void)dst; return nullptr; }
+
   void log(CommTag tag, int kind, int64_t logical_elems) {
     CommCounters& c = counters[tag];
     if (kind == 0) c.all_gathers++;

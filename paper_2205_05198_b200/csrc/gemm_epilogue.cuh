@@ -18,24 +18,24 @@ template <typename T>
 __device__ __forceinline__ void epi_store(const GemmArgs& g, int64_t m, int64_t n, float acc) {
   switch (g.epi) {
     case Epi::Store:
-      static_cast<T*>(g.C)[m * g.ldc + n] = from_f<T>(acc);
+      gemm_row<T>(g, m)[n] = from_f<T>(acc);
       break;
     case Epi::Bias:
-      static_cast<T*>(g.C)[m * g.ldc + n] = from_f<T>(acc + g.bias[n]);
+      gemm_row<T>(g, m)[n] = from_f<T>(acc + g.bias[n]);
       break;
     case Epi::BiasGelu: {
       const T pre = from_f<T>(acc + g.bias[n]);
-      static_cast<T*>(g.C)[m * g.ldc + n] = pre;
+      gemm_row<T>(g, m)[n] = pre;
       static_cast<T*>(g.C2)[m * g.ldc + n] = from_f<T>(gelu_erf(to_f(pre)));
       break;
     }
     case Epi::GeluBwd: {
       const float x = to_f(static_cast<const T*>(g.aux)[m * g.ldaux + n]);
-      static_cast<T*>(g.C)[m * g.ldc + n] = from_f<T>(acc * gelu_erf_grad(x));
+      gemm_row<T>(g, m)[n] = from_f<T>(acc * gelu_erf_grad(x));
       break;
     }
     case Epi::F32:
-      static_cast<float*>(g.C)[m * g.ldc + n] = acc;
+      gemm_row<float>(g, m)[n] = acc;
       break;
   }
 }

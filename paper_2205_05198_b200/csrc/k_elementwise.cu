@@ -392,11 +392,67 @@ __global__ void __launch_bounds__(512) ln_fwd_v(const T* __restrict__ x,
   }
 }
 
+// ---- fused reduce-scatter consumer: slots landed by peers (or simulated ranks)
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// every source has signalled past this rank's generation (thread 0 polls, the CTA waits)
+__device__ __forceinline__ void wait_slots(const SlotSrc& a) {
+  if (a.flags == nullptr) return;
+  if (threadIdx.x == 0) {
+    const uint32_t target = ld_acquire_sys(a.gen) + 1u;
+    for (int q = 0; q < a.n; ++q)
+      while ((int32_t)(ld_acquire_sys(a.flags + q) - target) < 0) __nanosleep(64);
+    __threadfence();
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ uint4 ld16_coherent(const void* p) {  // data landed by a peer (L2)
+  uint4 r;
+  asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+// rank-ordered fp32 sum of the slots at element offset `off`, rounded to T (as rs_local_k)
+template <typename T>
+__device__ __forceinline__ uint4 sum_slots(const SlotSrc& a, int64_t off) {
+  constexpr int VW = kVW<T>;
+  float acc[VW], v[VW];
+  unpack<T>(ld16_coherent(static_cast<const T*>(a.p[0]) + off), acc);
+  for (int q = 1; q < a.n; ++q) {
+    unpack<T>(ld16_coherent(static_cast<const T*>(a.p[q]) + off), v);
+#pragma unroll
+    for (int j = 0; j < VW; ++j) acc[j] += v[j];
+  }
+  return pack<T>(acc);
+}
+
+__global__ void p2p_signal_k(FlagPtrs f) {
+  __threadfence_system();  // this rank's landed rows (previous kernel) before the counters
+  if ((int)threadIdx.x < f.n)
+    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(f.p[threadIdx.x]) : "memory");
+}
+__global__ void p2p_advance_k(uint32_t* gen) { *gen += 1u; }
+
+template <typename T>
+__global__ void reduce_slots_k(SlotSrc a, T* __restrict__ out, int64_t nvec) {
+  wait_slots(a);
+  constexpr int VW = kVW<T>;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x)
+    st16(out + i * VW, sum_slots<T>(a, i * VW));
+}
+
 // Bias + dropout + residual (+ LayerNorm of the result). The dropout keep bits of the VW
 // elements of a vector come from the counter RNG in its hot-loop form (rng_fast.cuh): the
 // high half of the 64-bit counter is shared by the vector unless its low half carries.
-template <typename T, int VPT, bool LN>
-__global__ void __launch_bounds__(512) bdr_v(const T* __restrict__ a, const float* __restrict__ bias,
+// SL: the input partial is the rank-ordered sum of the fused reduce-scatter's landing slots.
+template <typename T, int VPT, bool LN, bool SL>
+__global__ void __launch_bounds__(512) bdr_v(const T* __restrict__ a, SlotSrc slots,
+                                              const float* __restrict__ bias,
                                               const T* __restrict__ resid, T* __restrict__ r_out,
                                               uint8_t* __restrict__ mask_out,
                                               T* __restrict__ ln_out, const float* __restrict__ g,
@@ -413,12 +469,14 @@ __global__ void __launch_bounds__(512) bdr_v(const T* __restrict__ a, const floa
   const uint32_t mixed_lo = (uint32_t)key.mixed, mixed_hi = (uint32_t)(key.mixed >> 32);
   const uint32_t t_lo = (uint32_t)tsh, t_hi = (uint32_t)(tsh >> 32);
   uint4 ar[VPT], xr[VPT];
+  if constexpr (SL) wait_slots(slots);
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
     const int vi = threadIdx.x + i * blockDim.x;
     if (vi < nvec) {
       const int64_t off = row * h + (int64_t)vi * VW;
-      ar[i] = ld16(a + off);
+      if constexpr (SL) ar[i] = sum_slots<T>(slots, off);
+      else ar[i] = ld16(a + off);
       xr[i] = ld16(resid + off);
     }
   }
@@ -851,9 +909,9 @@ void bias_dropout_residual(const T* a, const float* bias, const T* resid, T* r_o
     const int vpt = pick_vpt(h / VW);
     const unsigned nt = (unsigned)vthreads(h / VW, vpt);
 #define SPL_BDRV(VPTX, LNX)                                                                   \
-  bdr_v<T, VPTX, LNX><<<(unsigned)rows, nt, 0, st>>>(a, bias, resid, r_out, mask_out, ln_out, \
-                                                     gain, lnb, mean, rstd, (int)h, key,      \
-                                                     base_index, eps, nonfinite, sm)
+  bdr_v<T, VPTX, LNX, false><<<(unsigned)rows, nt, 0, st>>>(a, SlotSrc{}, bias, resid, r_out, \
+                                                     mask_out, ln_out, gain, lnb, mean, rstd, \
+                                                     (int)h, key, base_index, eps, nonfinite, sm)
     if (vpt == 4) {
       if (ln_out) SPL_BDRV(4, true); else SPL_BDRV(4, false);
     } else {
@@ -876,6 +934,51 @@ void bias_dropout_residual(const T* a, const float* bias, const T* resid, T* r_o
     if (ln_out) SPL_BDR(1, true); else SPL_BDR(1, false);
   }
 #undef SPL_BDR
+  SPL_CHECK_LAUNCH();
+}
+
+void p2p_signal(const FlagPtrs& f, cudaStream_t st) {
+  require(f.n >= 1 && f.n <= kMaxScatterRanks, "p2p_signal: bad rank count");
+  p2p_signal_k<<<1, 32, 0, st>>>(f);
+  SPL_CHECK_LAUNCH();
+}
+void p2p_advance(uint32_t* gen, cudaStream_t st) {
+  p2p_advance_k<<<1, 1, 0, st>>>(gen);
+  SPL_CHECK_LAUNCH();
+}
+
+template <typename T>
+void bias_dropout_residual_slots(const SlotSrc& a, const float* bias, const T* resid, T* r_out,
+                                 uint8_t* mask_out, T* ln_out, const float* gain, const float* lnb,
+                                 float* mean, float* rstd, int64_t rows, int64_t h, DropKey key,
+                                 uint64_t base_index, float eps, int* nonfinite, cudaStream_t st) {
+  if (rows == 0) return;
+  constexpr int VW = vec_width<T>();
+  require(h % VW == 0 && pick_vpt(h / VW) != 0 && a.n >= 1,
+          "fused reduce-scatter consumer: hidden must be a multiple of the vector width");
+  const rngk::ShiftMuls sm{4u, 32u, 2u, 1u};
+  const int vpt = pick_vpt(h / VW);
+  const unsigned nt = (unsigned)vthreads(h / VW, vpt);
+#define SPL_BDRS(VPTX, LNX)                                                                    \
+  bdr_v<T, VPTX, LNX, true><<<(unsigned)rows, nt, 0, st>>>(nullptr, a, bias, resid, r_out,      \
+                                                           mask_out, ln_out, gain, lnb, mean,  \
+                                                           rstd, (int)h, key, base_index, eps, \
+                                                           nonfinite, sm)
+  if (vpt == 4) {
+    if (ln_out) SPL_BDRS(4, true); else SPL_BDRS(4, false);
+  } else {
+    if (ln_out) SPL_BDRS(8, true); else SPL_BDRS(8, false);
+  }
+#undef SPL_BDRS
+  SPL_CHECK_LAUNCH();
+}
+
+template <typename T>
+void reduce_slots(const SlotSrc& a, T* out, int64_t n, cudaStream_t st) {
+  constexpr int VW = vec_width<T>();
+  require(n % VW == 0 && a.n >= 1, "reduce_slots: size must be a multiple of the vector width");
+  const int64_t nvec = n / VW;
+  reduce_slots_k<T><<<grid_for(nvec, 256), 256, 0, st>>>(a, out, nvec);
   SPL_CHECK_LAUNCH();
 }
 
@@ -993,6 +1096,11 @@ void f32_to_f64(const float* in, double* out, int64_t n, cudaStream_t st) {
                                 uint64_t, double, double, double, cudaStream_t);             \
   template void layernorm_fwd<T>(const T*, const float*, const float*, T*, float*, float*,   \
                                  int64_t, int64_t, float, cudaStream_t);                     \
+  template void bias_dropout_residual_slots<T>(const SlotSrc&, const float*, const T*, T*,    \
+                                               uint8_t*, T*, const float*, const float*,      \
+                                               float*, float*, int64_t, int64_t, DropKey,     \
+                                               uint64_t, float, int*, cudaStream_t);          \
+  template void reduce_slots<T>(const SlotSrc&, T*, int64_t, cudaStream_t);                   \
   template void bias_dropout_residual<T>(const T*, const float*, const T*, T*, uint8_t*, T*,  \
                                          const float*, const float*, float*, float*, int64_t, \
                                          int64_t, DropKey, uint64_t, float, int*,             \

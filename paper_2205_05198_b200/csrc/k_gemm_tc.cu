@@ -80,7 +80,7 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t m, int64_
   if (m >= g.M) return;
   const bool full = n0 + 32 <= g.N;
   if constexpr (EPI == (int)Epi::F32) {
-    float* c = static_cast<float*>(g.C) + m * g.ldc + n0;
+    float* c = gemm_row<float>(g, m) + n0;
     if (full) {
 #pragma unroll
       for (int i = 0; i < 32; i += 4)
@@ -126,7 +126,7 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t m, int64_
         for (int i = 0; i < 32 && n0 + i < g.N; ++i) o[i] *= gelu_grad_fast(__bfloat162float(ax[i]));
       }
     }
-    bf16* c = static_cast<bf16*>(g.C) + m * g.ldc + n0;
+    bf16* c = gemm_row<bf16>(g, m) + n0;
     bf16* c2 = EPI == (int)Epi::BiasGelu ? static_cast<bf16*>(g.C2) + m * g.ldc + n0 : nullptr;
     if (full) {
 #pragma unroll

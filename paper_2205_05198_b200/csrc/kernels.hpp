@@ -7,6 +7,10 @@
 
 namespace spl::k {
 
+// tensor-parallel ranks a fused reduce-scatter addresses (the local-rank limit of LocalComm)
+constexpr int kMaxScatterRanks = 16;
+
+
 // ---------------------------------------------------------------- parameters
 // LayerParams::random on the device (block.cpp:234-265): out[i, j] (ld_out) =
 //   lo + (hi - lo) * uniform01(key, (row0 + i) * ld_full + col0 + j) + add
@@ -31,6 +35,33 @@ void bias_dropout_residual(const T* a, const float* bias, const T* resid, T* r_o
                            uint8_t* mask_out, T* ln_out, const float* gain, const float* lnb,
                            float* mean, float* rstd, int64_t rows, int64_t h, DropKey key,
                            uint64_t base_index, float eps, int* nonfinite, cudaStream_t st);
+
+// ---- consumer side of the reduce-scatter fused into a row-parallel GEMM (GemmArgs::scatter):
+// the t landing slots of this rank, summed in rank order 0..t-1 in fp32 and rounded to T
+// (collectives.cpp:40-46), after waiting until all t sources signalled past the generation.
+struct SlotSrc {
+  const void* p[kMaxScatterRanks] = {};
+  int n = 0;
+  const uint32_t* flags = nullptr;  // t arrival counters (this rank)
+  const uint32_t* gen = nullptr;    // this rank's generation counter
+};
+struct FlagPtrs {
+  uint32_t* p[kMaxScatterRanks] = {};
+  int n = 0;
+};
+// source side, after its GEMM: system-scope release increment of every destination's counter
+void p2p_signal(const FlagPtrs& f, cudaStream_t st);
+// destination side, after its consumer: generation += 1
+void p2p_advance(uint32_t* gen, cudaStream_t st);
+// BDR(+LN) whose input partial is the sum of the slots (the forward's ḡ + 568-578 / 588-600)
+template <typename T>
+void bias_dropout_residual_slots(const SlotSrc& a, const float* bias, const T* resid, T* r_out,
+                                 uint8_t* mask_out, T* ln_out, const float* gain, const float* lnb,
+                                 float* mean, float* rstd, int64_t rows, int64_t h, DropKey key,
+                                 uint64_t base_index, float eps, int* nonfinite, cudaStream_t st);
+// out[n] = rank-ordered sum of the slots (the backward's g-dual reduce-scatters)
+template <typename T>
+void reduce_slots(const SlotSrc& a, T* out, int64_t n, cudaStream_t st);
 
 // out = dy * mask / (1 - p) (block.cpp:77-79) and per-chunk column sums of out (the bias
 // gradient, tensor.cpp:109-114) into partials[chunk][h].
@@ -99,7 +130,24 @@ struct GemmArgs {
   void* C2 = nullptr;       // BiasGelu second output (ldc)
   const void* aux = nullptr;  // GeluBwd pre-activation (ld = ldaux)
   int64_t ldaux = 0;
+  // Row scatter (the reduce-scatter fused into a row-parallel GEMM): when scatter_n > 0, row m
+  // of C is written to scatter[m / scatter_rows] + (m % scatter_rows) * ldc instead of
+  // C + m * ldc — i.e. into the landing slot this rank owns in the buffer of the rank that
+  // holds that sequence shard (peer memory over NVLink, or a local buffer for simulated ranks).
+  static constexpr int kMaxScatter = kMaxScatterRanks;
+  void* scatter[kMaxScatter] = {};
+  int scatter_n = 0;
+  int64_t scatter_rows = 0;
 };
+// Base of output row m of a GEMM (honours the row scatter).
+template <typename U>
+__host__ __device__ inline U* gemm_row(const GemmArgs& g, int64_t m) {
+  if (g.scatter_n > 0) {
+    const int64_t q = m / g.scatter_rows;
+    return static_cast<U*>(g.scatter[q]) + (m - q * g.scatter_rows) * g.ldc;
+  }
+  return static_cast<U*>(g.C) + m * g.ldc;
+}
 template <typename T>
 void gemm(const GemmArgs& a, cudaStream_t st);
 // Which implementation gemm<T> used for these args (for the profiler): 1 = tcgen05.

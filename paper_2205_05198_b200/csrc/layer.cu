@@ -86,6 +86,15 @@ class Layer final : public LayerBase {
     }
     // The keep-bit RNG pass runs on the main stream by default: overlapping it with the GEMMs
     // on a side stream measured no faster (the GEMMs already hold the chip at its power cap).
+    {  // reduce-scatter fused into the row-parallel GEMMs: on for simulated ranks; NCCL ranks
+       // opt in with SPL_FUSED_RS=1 (CUDA IPC peer slots over NVLink) until measured on a node
+      const char* f = std::getenv("SPL_FUSED_RS");
+      const bool local = comm_->local() == t_;
+      const bool want = f != nullptr ? f[0] == '1' : local;
+      if (want && std::is_same_v<T, bf16> && sp_ && t_ > 1 && t_ <= k::kMaxScatterRanks &&
+          h_ % 8 == 0)
+        fused_rs_ = comm_->p2p_setup((size_t)(RL_ * h_) * sizeof(T));
+    }
     const char* e = std::getenv("SPL_KEEPBITS_SIDE");
     bits_serial_ = !(e != nullptr && e[0] == '1');
   }
@@ -777,12 +786,17 @@ class Layer final : public LayerBase {
 
   void gemm(int64_t M, int64_t N, int64_t K, const T* A, int64_t lda, Major am, const T* B,
             int64_t ldb, Major bm, void* C, int64_t ldc, Epi epi, const float* bias = nullptr,
-            void* C2 = nullptr, const T* aux = nullptr, int64_t ldaux = 0) {
+            void* C2 = nullptr, const T* aux = nullptr, int64_t ldaux = 0, int scatter_rank = -1) {
     GemmArgs g;
     g.M = M; g.N = N; g.K = K;
     g.A = A; g.lda = lda; g.amaj = am;
     g.B = B; g.ldb = ldb; g.bmaj = bm;
     g.C = C; g.ldc = ldc; g.epi = epi; g.bias = bias; g.C2 = C2; g.aux = aux; g.ldaux = ldaux;
+    if (scatter_rank >= 0) {  // the reduce-scatter fused into this row-parallel GEMM
+      for (int q = 0; q < t_; ++q) g.scatter[q] = comm_->p2p_slot(q, rank0_ + scatter_rank);
+      g.scatter_n = t_;
+      g.scatter_rows = RL_;
+    }
     const double es = sizeof(T);
     const double bytes = (M * K + K * N) * es + M * N * (epi == Epi::F32 ? 4.0 : es) *
                          (epi == Epi::BiasGelu ? 2 : 1) + (epi == Epi::GeluBwd ? M * N * es : 0);
@@ -852,6 +866,38 @@ class Layer final : public LayerBase {
              [&] { comm_->all_reduce(p.data(), RF_ * h_, dt(), st_); });
     }
   }
+  // ---- reduce-scatter fused into the row-parallel GEMMs (GemmArgs::scatter): the producing
+  // GEMM of local rank r lands its rows of shard q in q's slot for r (peer memory over
+  // NVLink for NCCL ranks, device buffers for simulated ranks), signal() publishes them, the
+  // consumer of shard r waits for all t sources and sums the slots in rank order.
+  int fused_rank(int r) const { return fused_rs_ ? r : -1; }
+  void fused_signal(int r) {
+    k::FlagPtrs f;
+    for (int q = 0; q < t_; ++q) f.p[q] = comm_->p2p_flag(q, rank0_ + r);
+    f.n = t_;
+    launch(K_COMM, 1, 0, 0, [&] { k::p2p_signal(f, st_); });
+  }
+  k::SlotSrc fused_src(int r) {
+    k::SlotSrc a;
+    for (int q = 0; q < t_; ++q) a.p[q] = comm_->p2p_slot_local(rank0_ + r, q);
+    a.n = t_;
+    a.flags = comm_->p2p_flags_local(rank0_ + r);
+    a.gen = comm_->p2p_gen(rank0_ + r);
+    return a;
+  }
+  void fused_advance(int r) {
+    uint32_t* gen = comm_->p2p_gen(rank0_ + r);
+    launch(K_COMM, 1, 0, 0, [&] { k::p2p_advance(gen, st_); });
+  }
+  // the backward's consumers read rs_out: sum the slots into it
+  void fused_reduce(int r) {
+    const k::SlotSrc a = fused_src(r);
+    launch(K_COMM, 1, 0, (double)t_ * RL_ * h_ * sizeof(T), [&] {
+      k::reduce_slots<T>(a, R_[r].rs_out, RL_ * h_, st_);
+    });
+    fused_advance(r);
+  }
+
   // Collective on the comm stream after everything issued so far on the compute stream;
   // returns the event the consumer waits on (nullptr when there is nothing to wait for).
   cudaEvent_t gather_async(std::function<const void*(int)> shard, std::function<void*(int)> full,
@@ -951,14 +997,27 @@ class Layer final : public LayerBase {
       k::AttnArgs a = attn_args(r);
       join_keep_bits();
       launch(K_ATTN, 1, attn_flops(false), 0, [&] { k::attn_fwd<T>(a, st_); });
-      // row-parallel projection partial (block.cpp:563)
-      gemm(RF_, h, lw_, R.api, lw_, Major::K, R.wo, h, Major::MN, R.part, h, Epi::Store);
+      // row-parallel projection partial (block.cpp:563); with the fused reduce-scatter its rows
+      // land directly in the slots of the ranks that own them
+      gemm(RF_, h, lw_, R.api, lw_, Major::K, R.wo, h, Major::MN, R.part, h, Epi::Store, nullptr,
+           nullptr, nullptr, 0, fused_rank(r));
+      if (fused_rs_) fused_signal(r);
     }
-    scatter(tag);  // ḡ (block.cpp:567)
+    if (fused_rs_) comm_->log(tag, 1, RF_ * h_);
+    else scatter(tag);  // ḡ (block.cpp:567)
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
       const uint64_t base = sp_ ? (uint64_t)((rank0_ + r) * RL_ * h) : 0;
       // bias + dropout + residual, fused with LN2 (block.cpp:568-578)
+      if (fused_rs_) {
+        const k::SlotSrc a = fused_src(r);
+        launch(K_ELEM, 1, 0, (2.0 * t_ + 3.0) * eb * RL_ * h + RL_ * h, [&] {
+          k::bias_dropout_residual_slots<T>(a, R.bo, R.x_s, R.r1, R.amask, R.y2, R.g2, R.be2,
+                                            R.mu2, R.rs2, RL_, h, k_attn_, base, eps, nullptr, st_);
+        });
+        fused_advance(r);
+        continue;
+      }
       launch(K_ELEM, 1, 0, (4.0 * eb + 1.0) * RL_ * h, [&] {
         k::bias_dropout_residual<T>(scattered(r), R.bo, R.x_s, R.r1, R.amask, R.y2, R.g2, R.be2,
                                     R.mu2, R.rs2, RL_, h, k_attn_, base, eps, nullptr, st_);
@@ -972,12 +1031,25 @@ class Layer final : public LayerBase {
       // FC1 + bias + GELU, keeping both pre- and post-activation (block.cpp:584-585)
       gemm(RF_, fw_, h, y2, h, Major::K, R.w1, fw_, Major::MN, R.gin, fw_, Epi::BiasGelu, R.b1,
            R.fin);
-      gemm(RF_, h, fw_, R.fin, fw_, Major::K, R.w2, h, Major::MN, R.part, h, Epi::Store);  // 586
+      gemm(RF_, h, fw_, R.fin, fw_, Major::K, R.w2, h, Major::MN, R.part, h, Epi::Store,  // 586
+           nullptr, nullptr, nullptr, 0, fused_rank(r));
+      if (fused_rs_) fused_signal(r);
     }
-    scatter(tag);  // block.cpp:588
+    if (fused_rs_) comm_->log(tag, 1, RF_ * h_);
+    else scatter(tag);  // block.cpp:588
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
       const uint64_t base = sp_ ? (uint64_t)((rank0_ + r) * RL_ * h) : 0;
+      if (fused_rs_) {
+        const k::SlotSrc a = fused_src(r);
+        launch(K_ELEM, 1, 0, (2.0 * t_ + 2.0) * eb * RL_ * h + RL_ * h, [&] {
+          k::bias_dropout_residual_slots<T>(a, R.b2, R.r1, y[r], R.mmask, nullptr, nullptr,
+                                            nullptr, nullptr, nullptr, RL_, h, k_mlp_, base, eps,
+                                            nonfinite, st_);
+        });
+        fused_advance(r);
+        continue;
+      }
       launch(K_ELEM, 1, 0, (3.0 * eb + 1.0) * RL_ * h, [&] {
         k::bias_dropout_residual<T>(scattered(r), R.b2, R.r1, y[r], R.mmask, nullptr, nullptr,
                                     nullptr, nullptr, nullptr, RL_, h, k_mlp_, base, eps,
@@ -1024,15 +1096,21 @@ class Layer final : public LayerBase {
         k::reduce_partials(R.partials, nch_f, fw_, R.db1, false, st_);
       });
       // FC1 dgrad (block.cpp:665) first, so its reduce-scatter overlaps the FC1 wgrad
-      gemm(RF_, h, fw_, R.dgin, fw_, Major::K, R.w1, fw_, Major::K, R.part, h, Epi::Store);
+      gemm(RF_, h, fw_, R.dgin, fw_, Major::K, R.w1, fw_, Major::K, R.part, h, Epi::Store,
+           nullptr, nullptr, nullptr, 0, fused_rank(r));
+      if (fused_rs_) fused_signal(r);
     }
-    cudaEvent_t rs_done = scatter_async(kSchedule, ev_rs_);  // g-dual: block.cpp:668-669
+    cudaEvent_t rs_done = nullptr;  // g-dual: block.cpp:668-669
+    if (fused_rs_) comm_->log(kSchedule, 1, RF_ * h_);
+    else rs_done = scatter_async(kSchedule, ev_rs_);
     wait_on(y2_ready);
     for (int r = 0; r < L_; ++r) {  // FC1 wgrad on the re-gathered Y2 (block.cpp:664)
       Rank& R = R_[r];
       gemm(h, fw_, RF_, gathered(r, R.y2), h, Major::MN, R.dgin, fw_, Major::MN, R.dw1, fw_, Epi::F32);
     }
     wait_on(rs_done);
+    if (fused_rs_)
+      for (int r = 0; r < L_; ++r) fused_reduce(r);
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
       const T* dy = static_cast<const T*>(dyv[r]);
@@ -1075,9 +1153,12 @@ class Layer final : public LayerBase {
       });
       // dY1 = dQ·Wqᵀ + dK·Wkᵀ + dV·Wvᵀ as one GEMM over the fused 3h/t weight (709-711)
       gemm(RF_, h, 3 * lw_, R.dqkv, 3 * lw_, Major::K, R.wqkv, 3 * lw_, Major::K, R.part, h,
-           Epi::Store);
+           Epi::Store, nullptr, nullptr, nullptr, 0, fused_rank(r));
+      if (fused_rs_) fused_signal(r);
     }
-    rs_done = scatter_async(kSchedule, ev_rs_);  // block.cpp:714-715, overlaps the QKV wgrad
+    rs_done = nullptr;  // block.cpp:714-715, overlaps the QKV wgrad
+    if (fused_rs_) comm_->log(kSchedule, 1, RF_ * h_);
+    else rs_done = scatter_async(kSchedule, ev_rs_);
     wait_on(y1_ready);
     for (int r = 0; r < L_; ++r) {  // QKV wgrad on the re-gathered Y1 (block.cpp:706-708)
       Rank& R = R_[r];
@@ -1085,6 +1166,8 @@ class Layer final : public LayerBase {
            R.dwqkv, 3 * lw_, Epi::F32);
     }
     wait_on(rs_done);
+    if (fused_rs_)
+      for (int r = 0; r < L_; ++r) fused_reduce(r);
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
       launch(K_ELEM, 2, 0, 5.0 * eb * RL_ * h, [&] {
@@ -1134,7 +1217,8 @@ class Layer final : public LayerBase {
   int* nonfinite_ = nullptr;
   bool have_fwd_ = false;
   bool bits_pending_ = false;
-  bool bits_serial_ = true;  // SPL_KEEPBITS_SIDE=1: RNG pass on the side stream
+  bool bits_serial_ = true;
+  bool fused_rs_ = false;  // reduce-scatters fused into the row-parallel GEMMs  // SPL_KEEPBITS_SIDE=1: RNG pass on the side stream
   bool graphs_ = false;
   std::vector<Graph> gfwd_, gbwd_;
   // profiling
