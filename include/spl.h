@@ -37,7 +37,8 @@ enum {
   SPL_EDOMAIN = 2, /* std::domain_error: non-finite layer output (block.cpp:454-456, 596-598)  */
   SPL_ECUDA = 3,
   SPL_ENCCL = 4,
-  SPL_ESTATE = 5   /* backward without a matching forward ("missing saved forward state")     */
+  SPL_ESTATE = 5,  /* backward without a matching forward ("missing saved forward state")     */
+  SPL_EBUDGET = 6  /* pipeline::InfeasibleBudgetError (pipeline_sim.hpp:98-103)                */
 };
 
 /* RecomputeKind order of config.hpp:51 (None, Full, Selective). */
@@ -226,6 +227,37 @@ int spl_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, i
 
 /* Capture forward+backward into CUDA graphs after the first call (1) or run eagerly (0). */
 int spl_set_graphs(spl_handle* h, int on);
+
+/* ---- Microbatch-level recompute window (pipeline_sim.cpp:26-56,
+ * 192-359). ModelShape (config.hpp:27-35) + ParallelLayout (config.hpp:39-48, without d) +
+ * the inner RecomputeStrategy + ByteConvention (config.hpp:74-80, logits 4 by default). */
+typedef struct spl_model_desc {
+  int64_t heads, hidden, layers, seq, vocab;
+  int64_t tensor, pipeline, interleave, microbatch, microbatches; /* t, p, m, b, n_mb */
+  int32_t recompute, sequence_parallel;                           /* inner strategy */
+  int64_t act_bytes, mask_bytes, logits_bytes;
+} spl_model_desc;
+/* t = p = m = b = n_mb = 1, selective, SP on, bytes {2, 1, 4}; shape fields zero. */
+void spl_model_desc_default(spl_model_desc* m);
+/* microbatch_bytes (pipeline_sim.cpp:192-220): activation bytes one microbatch pins on
+ * pipeline rank `stage` when fully stored / checkpointed under the inner strategy. */
+int spl_microbatch_bytes(const spl_model_desc* m, int64_t stage, int64_t* fully_stored,
+                         int64_t* checkpointed);
+/* microbatch_window_plan (pipeline_sim.cpp:297-359): modes[p*n_mb] (row = rank, 1 = fully
+ * stored), stage_counts[2p] (fully stored, checkpointed per rank), the recomputed fraction
+ * num/den and the minimum feasible budget. The inner strategy must be full or selective
+ * (SPL_EINVAL); a budget below the all-checkpointed peak returns SPL_EBUDGET with
+ * *min_feasible_budget set (InfeasibleBudgetError::min_feasible_budget). */
+int spl_window_plan(const spl_model_desc* m, int64_t budget, uint8_t* modes,
+                    int64_t* stage_counts, int64_t* recomputed_num, int64_t* recomputed_den,
+                    int64_t* min_feasible_budget);
+/* simulate_memory_with_modes (pipeline_sim.cpp:222-275) for one rank: bytes held after each
+ * event of the rank's program (2·n_mb events, plus one recompute event before every
+ * checkpointed backward when the strategy recomputes) into bytes_after (capacity `cap`,
+ * *n_events set) and the peak. modes_row: n_mb entries, 1 = fully stored. */
+int spl_stage_timeline(const spl_model_desc* m, int64_t stage, const uint8_t* modes_row,
+                       int dealloc, int64_t* bytes_after, int64_t cap, int64_t* n_events,
+                       int64_t* peak);
 
 #ifdef __cplusplus
 }

@@ -7,3 +7,5 @@ from .seqpar import (BlockConfig, SeqparLayer, SeqparForward, SeqparBackward,  #
                      per_layer_bytes_exact, param_count, PARAM_NAMES, SeqparStack,
                      layer_component_breakdown, percent_of_baseline, total_first_stage_bytes,
                      layer_comm_bytes)
+from .window import (ModelShape, InfeasibleBudget, in_flight, microbatch_bytes,  # noqa: F401
+                     window_plan, stage_timeline)

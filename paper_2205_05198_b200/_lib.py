@@ -10,7 +10,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libspl.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "spl.h")
 
-SPL_OK, SPL_EINVAL, SPL_EDOMAIN, SPL_ECUDA, SPL_ENCCL, SPL_ESTATE = range(6)
+SPL_OK, SPL_EINVAL, SPL_EDOMAIN, SPL_ECUDA, SPL_ENCCL, SPL_ESTATE, SPL_EBUDGET = range(7)
 RECOMPUTE = {"none": 0, "full": 1, "selective": 2}
 DTYPE = {"f32": 0, "fp32": 0, "float32": 0, "bf16": 1, "bfloat16": 1}
 KCLASS = ["gemm", "attention", "elementwise", "collective", "other"]
@@ -33,6 +33,15 @@ class LayerDesc(C.Structure):
                 ("ln_eps", C.c_double), ("recompute", C.c_int32),
                 ("sequence_parallel", C.c_int32), ("dtype", C.c_int32),
                 ("check_finite", C.c_int32), ("act_bytes", C.c_int64), ("mask_bytes", C.c_int64)]
+
+
+class ModelDesc(C.Structure):
+    _fields_ = [("heads", C.c_int64), ("hidden", C.c_int64), ("layers", C.c_int64),
+                ("seq", C.c_int64), ("vocab", C.c_int64), ("tensor", C.c_int64),
+                ("pipeline", C.c_int64), ("interleave", C.c_int64), ("microbatch", C.c_int64),
+                ("microbatches", C.c_int64), ("recompute", C.c_int32),
+                ("sequence_parallel", C.c_int32), ("act_bytes", C.c_int64),
+                ("mask_bytes", C.c_int64), ("logits_bytes", C.c_int64)]
 
 
 class LedgerEntry(C.Structure):
@@ -98,6 +107,11 @@ def lib():
         "spl_stack_forward": (I32, [H, P(VP), P(VP)]),
         "spl_stack_backward": (I32, [H, P(VP), P(VP)]),
         "spl_stack_memory": (I32, [H, I32, P(I64)]),
+        "spl_model_desc_default": (None, [P(ModelDesc)]),
+        "spl_microbatch_bytes": (I32, [P(ModelDesc), I64, P(I64), P(I64)]),
+        "spl_window_plan": (I32, [P(ModelDesc), I64, P(C.c_uint8), P(I64), P(I64), P(I64), P(I64)]),
+        "spl_stage_timeline": (I32, [P(ModelDesc), I64, P(C.c_uint8), I32, P(I64), I64, P(I64),
+                                     P(I64)]),
         "spl_gemm_bf16": (I32, [I64, I64, I64, VP, I64, I32, VP, I64, I32, VP, I64, I32, VP, VP,
                                 VP, I64, VP, P(I32)]),
     }

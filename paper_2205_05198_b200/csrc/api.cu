@@ -7,6 +7,7 @@
 #include <string>
 
 #include "layer.hpp"
+#include "window.hpp"
 
 struct spl_handle {
   std::unique_ptr<spl::LayerBase> layer;
@@ -567,6 +568,57 @@ int spl_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, i
     g.bias = bias; g.C2 = C2; g.aux = aux; g.ldaux = ldaux;
     if (backend) *backend = spl::k::gemm_backend<spl::bf16>(g);
     spl::k::gemm<spl::bf16>(g, static_cast<cudaStream_t>(stream));
+  });
+}
+
+// ---- microbatch-level recompute window (pipeline_sim.cpp:26-56, 192-359)
+void spl_model_desc_default(spl_model_desc* m) {
+  std::memset(m, 0, sizeof(*m));
+  m->tensor = m->pipeline = m->interleave = m->microbatch = m->microbatches = 1;
+  m->recompute = SPL_RECOMPUTE_SELECTIVE;
+  m->sequence_parallel = 1;
+  m->act_bytes = 2;
+  m->mask_bytes = 1;
+  m->logits_bytes = 4;
+}
+
+int spl_microbatch_bytes(const spl_model_desc* m, int64_t stage, int64_t* fully_stored,
+                         int64_t* checkpointed) {
+  return guard([&] {
+    spl::require(m && fully_stored && checkpointed, "null argument");
+    const spl::MbBytes b = spl::microbatch_bytes(*m, stage);
+    *fully_stored = b.fully_stored;
+    *checkpointed = b.checkpointed;
+  });
+}
+
+int spl_window_plan(const spl_model_desc* m, int64_t budget, uint8_t* modes,
+                    int64_t* stage_counts, int64_t* recomputed_num, int64_t* recomputed_den,
+                    int64_t* min_feasible_budget) {
+  return guard([&] {
+    spl::require(m != nullptr, "null model desc");
+    const spl::WindowPlanOut plan = spl::window_plan(*m, budget, min_feasible_budget);
+    if (modes) std::memcpy(modes, plan.modes.data(), plan.modes.size());
+    if (stage_counts)
+      std::memcpy(stage_counts, plan.stage_counts.data(), plan.stage_counts.size() * 8);
+    if (recomputed_num) *recomputed_num = fit64(plan.rec_num);
+    if (recomputed_den) *recomputed_den = fit64(plan.rec_den);
+  });
+}
+
+int spl_stage_timeline(const spl_model_desc* m, int64_t stage, const uint8_t* modes_row,
+                       int dealloc, int64_t* bytes_after, int64_t cap, int64_t* n_events,
+                       int64_t* peak) {
+  return guard([&] {
+    spl::require(m != nullptr, "null model desc");
+    std::vector<int64_t> tl;
+    const int64_t pk = spl::stage_timeline(*m, stage, modes_row, dealloc != 0, &tl);
+    if (n_events) *n_events = (int64_t)tl.size();
+    if (peak) *peak = pk;
+    if (bytes_after) {
+      spl::require(cap >= (int64_t)tl.size(), "bytes_after capacity too small");
+      std::memcpy(bytes_after, tl.data(), tl.size() * 8);
+    }
   });
 }
 

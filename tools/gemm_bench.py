@@ -45,7 +45,33 @@ def bench(M, N, K, a_mn, b_mn, epi, reps=20):
     return 2.0 * M * N * K / (ms * 1e-3) / 1e12, ms
 
 
+def layer_cases(h, tokens, t):
+    """The 12 GEMMs of one layer rank at hidden h, s*b = tokens, tensor-parallel width t."""
+    q, f = 3 * h // t, 4 * h // t
+    return [("QKV fwd", tokens, q, h, 0, 1, 1), ("proj fwd", tokens, h, h // t, 0, 1, 0),
+            ("FC1 fwd", tokens, f, h, 0, 1, 2), ("FC2 fwd", tokens, h, f, 0, 1, 0),
+            ("FC2 dgrad", tokens, f, h, 0, 0, 3), ("FC1 dgrad", tokens, h, f, 0, 0, 0),
+            ("proj dgrad", tokens, h // t, h, 0, 0, 0), ("QKV dgrad", tokens, h, q, 0, 0, 0),
+            ("QKV wgrad", h, q, tokens, 1, 1, 4), ("proj wgrad", h // t, h, tokens, 1, 1, 4),
+            ("FC1 wgrad", h, f, tokens, 1, 1, 4), ("FC2 wgrad", f, h, tokens, 1, 1, 4)]
+
+
+SHAPES = {"22B": (6144, 8192), "175B": (12288, 2048), "530B": (20480, 2048), "1T": (25600, 2048)}
+
+
 def main():
+    if len(sys.argv) > 1:  # python tools/gemm_bench.py 175B [t]
+        h, tokens = SHAPES[sys.argv[1]]
+        t = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+        tot_f = tot_ms = 0.0
+        for name, M, N, K, am, bm, epi in layer_cases(h, tokens, t):
+            tf, ms = bench(M, N, K, am, bm, epi)
+            tot_f += 2.0 * M * N * K
+            tot_ms += ms
+            print(f"{name:12s} M={M:6d} N={N:6d} K={K:6d} {EPI[epi]:10s} {ms:7.3f} ms {tf:7.0f} TFLOP/s",
+                  flush=True)
+        print(f"{sys.argv[1]} t={t}: {tot_ms:.3f} ms, {tot_f / tot_ms / 1e9:.0f} TFLOP/s overall")
+        return
     cases = [  # name, M, N, K, a_mn, b_mn, epi
         ("QKV fwd", 8192, 18432, 6144, 0, 1, 1),
         ("FC1 fwd", 8192, 24576, 6144, 0, 1, 2),
