@@ -259,6 +259,30 @@ int spl_stage_timeline(const spl_model_desc* m, int64_t stage, const uint8_t* mo
                        int dealloc, int64_t* bytes_after, int64_t cap, int64_t* n_events,
                        int64_t* peak);
 
+/* Window executor: rank `stage` of a p-stage pipeline running its 1F1B program
+ * (pipeline_sim.cpp:40-56) over n_mb microbatches on one device with `layers` layers and t
+ * simulated ranks. modes_row[n_mb] (1 = fully stored, e.g. a row of spl_window_plan) picks per
+ * microbatch a no-recompute stack or one of the inner regime d->recompute; the slot count per
+ * mode is the most microbatches of that mode alive at once. All slots of a layer share its
+ * parameters and gradients; spl_window_run accumulates the gradients over the microbatches
+ * (running fp32 sum in microbatch-backward order). Microbatch i (1-based) draws the dropout
+ * masks of MaskKey microbatch d->microbatch + i - 1. Runs eagerly (no CUDA graphs). */
+typedef struct spl_window spl_window;
+int spl_window_create_local(const spl_layer_desc* d, int device, int t, int layers, int64_t p,
+                            int64_t stage, int64_t n_mb, const uint8_t* modes_row,
+                            spl_window** out);
+int spl_window_destroy(spl_window* w);
+/* Borrowed handle of layer l (parameters, gradients; do not spl_destroy it). */
+int spl_window_layer(spl_window* w, int layer, spl_handle** out);
+int spl_window_set_stream(spl_window* w, void* cuda_stream);
+/* x, dy, y, dx: n_mb x local-rank device pointers, microbatch-major. */
+int spl_window_run(spl_window* w, const void* const* x, const void* const* dy, void* const* y,
+                   void* const* dx);
+/* out[0] fully-stored slots, [1] checkpointed slots, [2] saved-activation ledger bytes held by
+ * all slots (rank 0), [3] peak ledger bytes of live microbatches during the last run, [4]
+ * parameter + gradient bytes, [5] workspace bytes. */
+int spl_window_memory(spl_window* w, int64_t out[6]);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,4 +8,4 @@ from .seqpar import (BlockConfig, SeqparLayer, SeqparForward, SeqparBackward,  #
                      layer_component_breakdown, percent_of_baseline, total_first_stage_bytes,
                      layer_comm_bytes)
 from .window import (ModelShape, InfeasibleBudget, in_flight, microbatch_bytes,  # noqa: F401
-                     window_plan, stage_timeline)
+                     window_plan, stage_timeline, SeqparWindow)

@@ -112,6 +112,13 @@ def lib():
         "spl_window_plan": (I32, [P(ModelDesc), I64, P(C.c_uint8), P(I64), P(I64), P(I64), P(I64)]),
         "spl_stage_timeline": (I32, [P(ModelDesc), I64, P(C.c_uint8), I32, P(I64), I64, P(I64),
                                      P(I64)]),
+        "spl_window_create_local": (I32, [P(LayerDesc), I32, I32, I32, I64, I64, I64,
+                                          P(C.c_uint8), P(H)]),
+        "spl_window_destroy": (I32, [H]),
+        "spl_window_layer": (I32, [H, I32, P(H)]),
+        "spl_window_set_stream": (I32, [H, VP]),
+        "spl_window_run": (I32, [H, P(VP), P(VP), P(VP), P(VP)]),
+        "spl_window_memory": (I32, [H, P(I64)]),
         "spl_gemm_bf16": (I32, [I64, I64, I64, VP, I64, I32, VP, I64, I32, VP, I64, I32, VP, VP,
                                 VP, I64, VP, P(I32)]),
     }

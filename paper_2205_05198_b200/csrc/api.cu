@@ -44,12 +44,13 @@ void check_handle(const spl_handle* h) {
 }
 
 spl_handle* make_handle(const spl_layer_desc* d, int device, std::unique_ptr<spl::Comm> comm,
-                        std::shared_ptr<spl::WorkPool> pool = nullptr) {
+                        std::shared_ptr<spl::WorkPool> pool = nullptr,
+                        std::shared_ptr<spl::WorkPool> params = nullptr) {
   auto* h = new spl_handle();
   h->device = device;
   try {
     SPL_CUDA(cudaSetDevice(device));
-    h->layer = spl::make_layer(*d, device, std::move(comm), std::move(pool));
+    h->layer = spl::make_layer(*d, device, std::move(comm), std::move(pool), std::move(params));
     SPL_CUDA(cudaEventCreate(&h->t0));
     SPL_CUDA(cudaEventCreate(&h->t1));
   } catch (...) {
@@ -396,22 +397,31 @@ int spl_layer_comm_bytes(int64_t s, int64_t b, int64_t hh, int64_t t, int64_t el
   });
 }
 
-int spl_stack_create_local(const spl_layer_desc* d, int device, int t, int layers,
-                           spl_stack** out) {
-  return guard([&] {
-    spl::require(d != nullptr && out != nullptr, "null argument");
+}  // extern "C"
+
+namespace {
+// L layers on t simulated ranks over one workspace pool (`pool`, created when null); `params`
+// (one pool per layer, or empty) shares parameters and gradients with other stacks.
+spl_stack* build_stack(const spl_layer_desc* d, int device, int t, int layers,
+                       std::shared_ptr<spl::WorkPool> pool,
+                       const std::vector<std::shared_ptr<spl::WorkPool>>& params) {
+    spl::require(d != nullptr, "null argument");
     spl::require(t >= 1, "t must be >= 1");
     spl::require(layers >= 1, "L must be >= 1");
     SPL_CUDA(cudaSetDevice(device));
     auto* st = new spl_stack();
     st->device = device;
     try {
-      st->pool = std::make_shared<spl::WorkPool>();
-      st->pool->device = device;
+      st->pool = pool;
+      if (!st->pool) {
+        st->pool = std::make_shared<spl::WorkPool>();
+        st->pool->device = device;
+      }
       for (int l = 0; l < layers; ++l) {
         spl_layer_desc dl = *d;
         dl.layer_index = d->layer_index + (uint32_t)l;
-        st->layers.push_back(make_handle(&dl, device, spl::make_local_comm(t), st->pool));
+        st->layers.push_back(make_handle(&dl, device, spl::make_local_comm(t), st->pool,
+                                         params.empty() ? nullptr : params[(size_t)l]));
       }
       st->local = st->layers[0]->layer->local_ranks();
       const int64_t rows = d->sequence_parallel ? d->seq / t : d->seq;
@@ -426,7 +436,72 @@ int spl_stack_create_local(const spl_layer_desc* d, int device, int t, int layer
       destroy_stack(st);
       throw;
     }
-    *out = st;
+    return st;
+}
+
+void stack_forward(spl_stack* st, const void* const* x, void* const* y) {
+  spl::require(x != nullptr && y != nullptr, "expected one input shard per rank");
+  const int L = (int)st->layers.size();
+  std::vector<const void*> in(x, x + st->local);
+  std::vector<void*> out(st->local);
+  for (int l = 0; l < L; ++l) {
+    for (int r = 0; r < st->local; ++r) out[r] = l == L - 1 ? y[r] : st->ping[l & 1][r];
+    st->layers[l]->layer->forward(in.data(), out.data());
+    for (int r = 0; r < st->local; ++r) in[r] = out[r];
+  }
+}
+
+void stack_backward(spl_stack* st, const void* const* dy, void* const* dx) {
+  spl::require(dy != nullptr && dx != nullptr, "expected one gradient shard per rank");
+  const int L = (int)st->layers.size();
+  std::vector<const void*> g(dy, dy + st->local);
+  std::vector<void*> out(st->local);
+  for (int l = L - 1; l >= 0; --l) {
+    for (int r = 0; r < st->local; ++r) out[r] = l == 0 ? dx[r] : st->ping[l & 1][r];
+    st->layers[l]->layer->backward(g.data(), out.data());
+    for (int r = 0; r < st->local; ++r) g[r] = out[r];
+  }
+}
+}  // namespace
+
+// Microbatch window: one pipeline rank's 1F1B program (pipeline_sim.cpp:40-56) over n_mb
+// microbatches. Fully stored microbatches run on no-recompute slot stacks, checkpointed ones on
+// slot stacks of the inner regime; every slot of layer l shares layer l's parameters and
+// gradients (one parameter pool per layer), slots of one regime share one workspace.
+struct spl_window {
+  std::vector<spl_stack*> slots[2];  // [0] checkpointed, [1] fully stored
+  std::vector<std::shared_ptr<spl::WorkPool>> params;
+  std::vector<uint8_t> modes;
+  std::vector<spl::ProgEvent> prog;
+  uint32_t mb_base = 1;
+  int device = 0, local = 0;
+  int64_t slot_ledger[2] = {0, 0};  // ledger bytes of one slot (rank 0), per mode
+  int64_t live_peak = 0;
+};
+
+namespace {
+void destroy_window(spl_window* w) {
+  for (auto& v : w->slots)
+    for (spl_stack* st : v) destroy_stack(st);
+  w->params.clear();
+  delete w;
+}
+void check_window(const spl_window* w) {
+  if (w == nullptr || (w->slots[0].empty() && w->slots[1].empty()))
+    spl::raise(SPL_EINVAL, "null window");
+}
+spl_stack* window_first(spl_window* w) {
+  return w->slots[1].empty() ? w->slots[0][0] : w->slots[1][0];
+}
+}  // namespace
+
+extern "C" {
+
+int spl_stack_create_local(const spl_layer_desc* d, int device, int t, int layers,
+                           spl_stack** out) {
+  return guard([&] {
+    spl::require(out != nullptr, "null argument");
+    *out = build_stack(d, device, t, layers, nullptr, {});
   });
 }
 
@@ -456,30 +531,14 @@ int spl_stack_set_stream(spl_stack* st, void* stream) {
 int spl_stack_forward(spl_stack* st, const void* const* x, void* const* y) {
   return guard([&] {
     check_stack(st);
-    spl::require(x != nullptr && y != nullptr, "expected one input shard per rank");
-    const int L = (int)st->layers.size();
-    std::vector<const void*> in(x, x + st->local);
-    std::vector<void*> out(st->local);
-    for (int l = 0; l < L; ++l) {
-      for (int r = 0; r < st->local; ++r) out[r] = l == L - 1 ? y[r] : st->ping[l & 1][r];
-      st->layers[l]->layer->forward(in.data(), out.data());
-      for (int r = 0; r < st->local; ++r) in[r] = out[r];
-    }
+    stack_forward(st, x, y);
   });
 }
 
 int spl_stack_backward(spl_stack* st, const void* const* dy, void* const* dx) {
   return guard([&] {
     check_stack(st);
-    spl::require(dy != nullptr && dx != nullptr, "expected one gradient shard per rank");
-    const int L = (int)st->layers.size();
-    std::vector<const void*> g(dy, dy + st->local);
-    std::vector<void*> out(st->local);
-    for (int l = L - 1; l >= 0; --l) {
-      for (int r = 0; r < st->local; ++r) out[r] = l == 0 ? dx[r] : st->ping[l & 1][r];
-      st->layers[l]->layer->backward(g.data(), out.data());
-      for (int r = 0; r < st->local; ++r) g[r] = out[r];
-    }
+    stack_backward(st, dy, dx);
   });
 }
 
@@ -619,6 +678,147 @@ int spl_stage_timeline(const spl_model_desc* m, int64_t stage, const uint8_t* mo
       spl::require(cap >= (int64_t)tl.size(), "bytes_after capacity too small");
       std::memcpy(bytes_after, tl.data(), tl.size() * 8);
     }
+  });
+}
+
+// ---- microbatch window executor
+int spl_window_create_local(const spl_layer_desc* d, int device, int t, int layers, int64_t p,
+                            int64_t stage, int64_t n_mb, const uint8_t* modes_row,
+                            spl_window** out) {
+  return guard([&] {
+    spl::require(d != nullptr && modes_row != nullptr && out != nullptr, "null argument");
+    spl::require(p >= 1 && stage >= 0 && stage < p, "stage must lie in [0, p)");
+    spl::require(n_mb >= p, "n_mb < p (pipeline cannot be filled)");
+    spl::require(layers >= 1, "L must be >= 1");
+    auto* w = new spl_window();
+    w->device = device;
+    w->mb_base = d->microbatch;
+    w->modes.assign(modes_row, modes_row + n_mb);
+    w->prog = spl::rank_program(p, stage, n_mb);
+    try {
+      // slots per mode = the most microbatches of that mode alive at once in the program
+      int live[2] = {0, 0}, need[2] = {0, 0};
+      for (const spl::ProgEvent& ev : w->prog) {
+        const int m = w->modes[(size_t)ev.microbatch - 1] ? 1 : 0;
+        live[m] += ev.forward ? 1 : -1;
+        need[m] = std::max(need[m], live[m]);
+      }
+      spl::require(need[0] == 0 || d->recompute != SPL_RECOMPUTE_NONE,
+                   "checkpointed microbatches need a full or selective inner strategy");
+      for (int l = 0; l < layers; ++l) {
+        w->params.push_back(std::make_shared<spl::WorkPool>());
+        w->params.back()->device = device;
+      }
+      for (int m = 1; m >= 0; --m) {
+        spl_layer_desc dm = *d;
+        if (m == 1) dm.recompute = SPL_RECOMPUTE_NONE;
+        std::shared_ptr<spl::WorkPool> pool;
+        for (int i = 0; i < need[m]; ++i) {
+          spl_stack* st = build_stack(&dm, device, t, layers, pool, w->params);
+          w->slots[m].push_back(st);
+          pool = st->pool;
+          for (spl_handle* h : st->layers) h->layer->set_graphs(false);
+        }
+        if (need[m] > 0)
+          for (spl_handle* h : w->slots[m][0]->layers) {
+            int64_t lb, pb, ub;
+            h->layer->saved_bytes(0, &lb, &pb, &ub);
+            w->slot_ledger[m] += lb;
+          }
+      }
+      w->local = window_first(w)->local;
+    } catch (...) {
+      destroy_window(w);
+      throw;
+    }
+    *out = w;
+  });
+}
+
+int spl_window_destroy(spl_window* w) {
+  return guard([&] {
+    if (w) destroy_window(w);
+  });
+}
+
+int spl_window_layer(spl_window* w, int layer, spl_handle** out) {
+  return guard([&] {
+    check_window(w);
+    spl_stack* st = window_first(w);
+    spl::require(layer >= 0 && layer < (int)st->layers.size() && out != nullptr,
+                 "layer index out of range");
+    *out = st->layers[(size_t)layer];
+  });
+}
+
+int spl_window_set_stream(spl_window* w, void* stream) {
+  return guard([&] {
+    check_window(w);
+    for (auto& v : w->slots)
+      for (spl_stack* st : v)
+        for (spl_handle* h : st->layers)
+          h->layer->set_caller_stream(static_cast<cudaStream_t>(stream));
+  });
+}
+
+int spl_window_run(spl_window* w, const void* const* x, const void* const* dy, void* const* y,
+                   void* const* dx) {
+  return guard([&] {
+    check_window(w);
+    spl::require(x && dy && y && dx, "expected n_mb x local-rank pointer arrays");
+    const size_t n_mb = w->modes.size();
+    std::vector<int> slot_of(n_mb, -1);
+    std::vector<uint8_t> busy[2] = {std::vector<uint8_t>(w->slots[0].size(), 0),
+                                    std::vector<uint8_t>(w->slots[1].size(), 0)};
+    int64_t live = 0;
+    w->live_peak = 0;
+    bool first_backward = true;
+    for (const spl::ProgEvent& ev : w->prog) {
+      const size_t i = (size_t)ev.microbatch - 1;
+      const int m = w->modes[i] ? 1 : 0;
+      const size_t off = i * (size_t)w->local;
+      if (ev.forward) {
+        size_t k = 0;
+        while (k < busy[m].size() && busy[m][k]) ++k;
+        spl::require(k < busy[m].size(), "window: no free activation slot");
+        busy[m][k] = 1;
+        slot_of[i] = (int)k;
+        spl_stack* st = w->slots[m][k];
+        for (spl_handle* h : st->layers) h->layer->set_microbatch(w->mb_base + (uint32_t)i);
+        stack_forward(st, x + off, y + off);
+        live += w->slot_ledger[m];
+        w->live_peak = std::max(w->live_peak, live);
+      } else {
+        spl::require(slot_of[i] >= 0, "window: backward before forward");
+        spl_stack* st = w->slots[m][(size_t)slot_of[i]];
+        for (spl_handle* h : st->layers) {
+          h->layer->set_microbatch(w->mb_base + (uint32_t)i);
+          h->layer->set_grad_accumulate(!first_backward);
+        }
+        stack_backward(st, dy + off, dx + off);
+        first_backward = false;
+        busy[m][(size_t)slot_of[i]] = 0;
+        slot_of[i] = -1;
+        live -= w->slot_ledger[m];
+      }
+    }
+  });
+}
+
+int spl_window_memory(spl_window* w, int64_t out[6]) {
+  return guard([&] {
+    check_window(w);
+    out[0] = (int64_t)w->slots[1].size();
+    out[1] = (int64_t)w->slots[0].size();
+    out[2] = out[0] * w->slot_ledger[1] + out[1] * w->slot_ledger[0];
+    out[3] = w->live_peak;
+    out[4] = 0;
+    for (auto& pp : w->params) out[4] += pp->bytes();
+    out[5] = 0;
+    for (auto& v : w->slots)
+      if (!v.empty()) out[5] += v[0]->pool->bytes();
+    for (auto& v : w->slots)
+      for (spl_stack* st : v) out[5] += 2 * st->ping_bytes * st->local;
   });
 }
 

@@ -35,7 +35,7 @@ __device__ __forceinline__ void epi_store(const GemmArgs& g, int64_t m, int64_t 
       break;
     }
     case Epi::F32:
-      gemm_row<float>(g, m)[n] = acc;
+      gemm_row<float>(g, m)[n] = g.accumulate ? gemm_row<float>(g, m)[n] + acc : acc;
       break;
   }
 }

@@ -82,11 +82,20 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t m, int64_
   if constexpr (EPI == (int)Epi::F32) {
     float* c = gemm_row<float>(g, m) + n0;
     if (full) {
+      if (g.accumulate) {  // running fp32 sum over microbatches: C_old + (this GEMM)
 #pragma unroll
-      for (int i = 0; i < 32; i += 4)
-        *reinterpret_cast<float4*>(c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        for (int i = 0; i < 32; i += 4) {
+          const float4 o = *reinterpret_cast<const float4*>(c + i);
+          *reinterpret_cast<float4*>(c + i) =
+              make_float4(o.x + v[i], o.y + v[i + 1], o.z + v[i + 2], o.w + v[i + 3]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      }
     } else {
-      for (int i = 0; i < 32 && n0 + i < g.N; ++i) c[i] = v[i];
+      for (int i = 0; i < 32 && n0 + i < g.N; ++i) c[i] = g.accumulate ? c[i] + v[i] : v[i];
     }
     return;
   } else {

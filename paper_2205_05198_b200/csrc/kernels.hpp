@@ -138,6 +138,7 @@ struct GemmArgs {
   void* scatter[kMaxScatter] = {};
   int scatter_n = 0;
   int64_t scatter_rows = 0;
+  int accumulate = 0;  // Epi::F32 only: C += A·B (gradient accumulation across microbatches)
 };
 // Base of output row m of a GEMM (honours the row scatter).
 template <typename U>

@@ -46,8 +46,9 @@ template <typename T>
 class Layer final : public LayerBase {
  public:
   Layer(const spl_layer_desc& d, int device, std::unique_ptr<Comm> comm,
-        std::shared_ptr<WorkPool> pool)
-      : d_(d), dev_(device), comm_(std::move(comm)), pool_(std::move(pool)) {
+        std::shared_ptr<WorkPool> pool, std::shared_ptr<WorkPool> params)
+      : d_(d), dev_(device), comm_(std::move(comm)), pool_(std::move(pool)),
+        params_(std::move(params)) {
     t_ = comm_->t();
     L_ = comm_->local();
     rank0_ = comm_->rank0();
@@ -65,9 +66,7 @@ class Layer final : public LayerBase {
     RL_ = sp_ ? RF_ / t_ : RF_;
     kind_ = d.recompute;
     scale_ = (float)(1.0 / std::sqrt((double)hd_));
-    k_soft_ = make_drop_key(d.seed, d.layer_index, kSoftmaxDrop, d.microbatch, d.dropout_p);
-    k_attn_ = make_drop_key(d.seed, d.layer_index, kAttnOutDrop, d.microbatch, d.dropout_p);
-    k_mlp_ = make_drop_key(d.seed, d.layer_index, kMlpDrop, d.microbatch, d.dropout_p);
+    make_keys();
     SPL_CUDA(cudaSetDevice(dev_));
     SPL_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     SPL_CUDA(cudaStreamCreateWithFlags(&st_rng_, cudaStreamNonBlocking));
@@ -97,6 +96,8 @@ class Layer final : public LayerBase {
     }
     const char* e = std::getenv("SPL_KEEPBITS_SIDE");
     bits_serial_ = !(e != nullptr && e[0] == '1');
+    const char* c = std::getenv("SPL_SERIAL_COMM");
+    comm_serial_ = c != nullptr && c[0] == '1';
   }
 
   ~Layer() override {
@@ -593,12 +594,32 @@ class Layer final : public LayerBase {
   }
   void set_graphs(bool on) override {
     graphs_ = on;
-    if (!on)
-      for (auto* set : {&gfwd_, &gbwd_}) {
-        for (Graph& g : *set)
-          if (g.exec) SPL_CUDA(cudaGraphExecDestroy(g.exec));
-        set->clear();
-      }
+    if (!on) drop_graphs();
+  }
+  void drop_graphs() {
+    for (auto* set : {&gfwd_, &gbwd_}) {
+      for (Graph& g : *set)
+        if (g.exec) SPL_CUDA(cudaGraphExecDestroy(g.exec));
+      set->clear();
+    }
+  }
+  // Captured graphs hold the keys and the epilogue modes by value: re-capture on change.
+  void set_microbatch(uint32_t microbatch) override {
+    if (microbatch == d_.microbatch) return;
+    d_.microbatch = microbatch;
+    make_keys();
+    drop_graphs();
+  }
+  void set_grad_accumulate(bool on) override {
+    if (on == grad_acc_) return;
+    grad_acc_ = on;
+    drop_graphs();
+  }
+  void make_keys() {
+    const spl_layer_desc& d = d_;
+    k_soft_ = make_drop_key(d.seed, d.layer_index, kSoftmaxDrop, d.microbatch, d.dropout_p);
+    k_attn_ = make_drop_key(d.seed, d.layer_index, kAttnOutDrop, d.microbatch, d.dropout_p);
+    k_mlp_ = make_drop_key(d.seed, d.layer_index, kMlpDrop, d.microbatch, d.dropout_p);
   }
 
  private:
@@ -607,7 +628,7 @@ class Layer final : public LayerBase {
     float *bqkv = nullptr, *bo = nullptr, *b1 = nullptr, *b2 = nullptr, *g1 = nullptr,
           *be1 = nullptr, *g2 = nullptr, *be2 = nullptr;
     float *dwqkv = nullptr, *dbqkv = nullptr, *dwo = nullptr, *dw1 = nullptr, *db1 = nullptr,
-          *dw2 = nullptr, *repl = nullptr;
+          *dw2 = nullptr, *repl = nullptr, *repl_new = nullptr;
     T *x_s = nullptr, *y1_s = nullptr, *qkv = nullptr, *sm = nullptr, *sd = nullptr,
       *api = nullptr, *r1 = nullptr, *y2 = nullptr, *gin = nullptr, *fin = nullptr;
     uint8_t *mask_i = nullptr, *amask = nullptr, *mmask = nullptr;
@@ -639,6 +660,17 @@ class Layer final : public LayerBase {
   U* alloc(int64_t n, int cat, int r) {
     void* p = nullptr;
     const size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(U);
+    if ((cat == kParam || cat == kGrad) && params_) {  // window slot: shared parameters
+      const size_t i = param_next_++;
+      if (i < params_->bufs.size()) {
+        require(params_->bufs[i].second == bytes, "parameter pool: layer shapes differ");
+        return static_cast<U*>(params_->bufs[i].first);
+      }
+      SPL_CUDA(cudaMalloc(&p, bytes));
+      SPL_CUDA(cudaMemset(p, 0, bytes));
+      params_->bufs.push_back({p, bytes});
+      return static_cast<U*>(p);
+    }
     if (cat == kWork && pool_) {  // stack member: the i-th workspace request is shared
       const size_t i = work_next_++;
       if (i < pool_->bufs.size()) {
@@ -696,6 +728,7 @@ class Layer final : public LayerBase {
       R.db1 = alloc<float>(fw_, kGrad, r);
       R.dw2 = alloc<float>(fw_ * h_, kGrad, r);
       R.repl = alloc<float>(6 * h_, kGrad, r);
+      R.repl_new = alloc<float>(6 * h_, kWork, r);
       R.x_s = alloc<T>(RL_ * h_, kSaved, r);
       R.y1_s = alloc<T>(RL_ * h_, saved, r);
       R.qkv = alloc<T>(RF_ * 3 * lw_, saved, r);
@@ -792,6 +825,7 @@ class Layer final : public LayerBase {
     g.A = A; g.lda = lda; g.amaj = am;
     g.B = B; g.ldb = ldb; g.bmaj = bm;
     g.C = C; g.ldc = ldc; g.epi = epi; g.bias = bias; g.C2 = C2; g.aux = aux; g.ldaux = ldaux;
+    g.accumulate = epi == Epi::F32 && grad_acc_;
     if (scatter_rank >= 0) {  // the reduce-scatter fused into this row-parallel GEMM
       for (int q = 0; q < t_; ++q) g.scatter[q] = comm_->p2p_slot(q, rank0_ + scatter_rank);
       g.scatter_n = t_;
@@ -906,6 +940,14 @@ class Layer final : public LayerBase {
       comm_->log(tag, 0, RF_ * h_);
       return nullptr;
     }
+    if (comm_serial_) {
+      auto s = cptrs(shard);
+      auto f = mptrs(full);
+      comm_->log(tag, 0, RF_ * h_);
+      launch(K_COMM, 1, 0, (double)RF_ * h_ * sizeof(T) * (t_ - 1) / t_,
+             [&] { comm_->all_gather(s.data(), f.data(), RL_ * h_, dt(), st_); });
+      return nullptr;
+    }
     SPL_CUDA(cudaEventRecord(ev_cfork_, st_));
     SPL_CUDA(cudaStreamWaitEvent(st_comm_, ev_cfork_, 0));
     auto s = cptrs(shard);
@@ -917,7 +959,7 @@ class Layer final : public LayerBase {
     return done;
   }
   cudaEvent_t scatter_async(CommTag tag, cudaEvent_t done) {
-    if (t_ == 1) {
+    if (t_ == 1 || comm_serial_) {
       scatter(tag);
       return nullptr;
     }
@@ -1072,7 +1114,7 @@ class Layer final : public LayerBase {
       const T* dy = static_cast<const T*>(dyv[r]);
       launch(K_ELEM, 2, 0, (2.0 * eb + 1.0) * RL_ * h, [&] {
         k::dropout_bwd_colsum<T>(dy, R.mmask, inv_keep, R.d_s, R.partials, RL_, h, kChunkRows, st_);
-        k::reduce_partials(R.partials, nch_l, h, R.repl + 1 * h, false, st_);  // b2 partial
+        k::reduce_partials(R.partials, nch_l, h, repl_w(R) + 1 * h, false, st_);  // b2 partial
       });
     }
     if (sp_)
@@ -1093,7 +1135,7 @@ class Layer final : public LayerBase {
       // b1 grad (block.cpp:663)
       launch(K_ELEM, 2, 0, eb * RF_ * fw_, [&] {
         k::colsum_partial<T>(R.dgin, RF_, fw_, fw_, R.partials, kChunkRows, st_);
-        k::reduce_partials(R.partials, nch_f, fw_, R.db1, false, st_);
+        k::reduce_partials(R.partials, nch_f, fw_, R.db1, grad_acc_, st_);
       });
       // FC1 dgrad (block.cpp:665) first, so its reduce-scatter overlaps the FC1 wgrad
       gemm(RF_, h, fw_, R.dgin, fw_, Major::K, R.w1, fw_, Major::K, R.part, h, Epi::Store,
@@ -1119,8 +1161,8 @@ class Layer final : public LayerBase {
                             R.partials + (int64_t)nch_l * h, RL_, h, kChunkRows, st_);
       });
       launch(K_ELEM, 2, 0, 0, [&] {
-        k::reduce_partials(R.partials, nch_l, h, R.repl + 4 * h, false, st_);
-        k::reduce_partials(R.partials + (int64_t)nch_l * h, nch_l, h, R.repl + 5 * h, false, st_);
+        k::reduce_partials(R.partials, nch_l, h, repl_w(R) + 4 * h, false, st_);
+        k::reduce_partials(R.partials + (int64_t)nch_l * h, nch_l, h, repl_w(R) + 5 * h, false, st_);
       });
     }
     // ---- attention branch (block.cpp:683-726)
@@ -1128,7 +1170,7 @@ class Layer final : public LayerBase {
       Rank& R = R_[r];
       launch(K_ELEM, 2, 0, (2.0 * eb + 1.0) * RL_ * h, [&] {
         k::dropout_bwd_colsum<T>(R.dr1, R.amask, inv_keep, R.d_s, R.partials, RL_, h, kChunkRows, st_);
-        k::reduce_partials(R.partials, nch_l, h, R.repl + 0 * h, false, st_);  // bo partial
+        k::reduce_partials(R.partials, nch_l, h, repl_w(R) + 0 * h, false, st_);  // bo partial
       });
     }
     if (sp_)
@@ -1149,7 +1191,7 @@ class Layer final : public LayerBase {
              [&] { k::attn_bwd<T>(a, R.dproj, R.dqkv, R.delta, st_); });  // 701-702
       launch(K_ELEM, 2, 0, eb * RF_ * 3 * lw_, [&] {
         k::colsum_partial<T>(R.dqkv, RF_, 3 * lw_, 3 * lw_, R.partials, kChunkRows, st_);
-        k::reduce_partials(R.partials, nch_f, 3 * lw_, R.dbqkv, false, st_);  // 703-705
+        k::reduce_partials(R.partials, nch_f, 3 * lw_, R.dbqkv, grad_acc_, st_);  // 703-705
       });
       // dY1 = dQ·Wqᵀ + dK·Wkᵀ + dV·Wvᵀ as one GEMM over the fused 3h/t weight (709-711)
       gemm(RF_, h, 3 * lw_, R.dqkv, 3 * lw_, Major::K, R.wqkv, 3 * lw_, Major::K, R.part, h,
@@ -1176,19 +1218,24 @@ class Layer final : public LayerBase {
                             RL_, h, kChunkRows, st_);
       });
       launch(K_ELEM, 2, 0, 0, [&] {
-        k::reduce_partials(R.partials, nch_l, h, R.repl + 2 * h, false, st_);
-        k::reduce_partials(R.partials + (int64_t)nch_l * h, nch_l, h, R.repl + 3 * h, false, st_);
+        k::reduce_partials(R.partials, nch_l, h, repl_w(R) + 2 * h, false, st_);
+        k::reduce_partials(R.partials + (int64_t)nch_l * h, nch_l, h, repl_w(R) + 3 * h, false, st_);
       });
     }
     // replicated-parameter gradients: one packed all-reduce (the 6 GradSync ARs, 741-746)
     if (sp_ && t_ > 1) {
       std::vector<float*> bufs(L_);
-      for (int r = 0; r < L_; ++r) bufs[r] = R_[r].repl;
+      for (int r = 0; r < L_; ++r) bufs[r] = repl_w(R_[r]);
       for (int i = 0; i < 6; ++i) comm_->log(kGradSync, 2, h);
       launch(K_COMM, 1, 0, 2.0 * 6 * h * 4 * (t_ - 1) / t_,
              [&] { comm_->all_reduce_f32(bufs.data(), 6 * h, st_); });
     }
+    if (grad_acc_)  // replicated-parameter gradients of this microbatch onto the running sum
+      for (int r = 0; r < L_; ++r)
+        launch(K_ELEM, 1, 0, 12.0 * 6 * h,
+               [&] { k::reduce_partials(R_[r].repl_new, 1, 6 * h, R_[r].repl, true, st_); });
   }
+  float* repl_w(Rank& R) const { return grad_acc_ ? R.repl_new : R.repl; }
 
   spl_layer_desc d_;
   int dev_;
@@ -1212,12 +1259,16 @@ class Layer final : public LayerBase {
   std::vector<Alloc> allocs_;
   std::shared_ptr<WorkPool> pool_;  // shared workspace of a stack (nullptr: own buffers)
   size_t work_next_ = 0;
+  std::shared_ptr<WorkPool> params_;  // parameters + gradients shared by window slots
+  size_t param_next_ = 0;
+  bool grad_acc_ = false;
   std::vector<T*> stage_;
   void* pinned_ = nullptr;
   int* nonfinite_ = nullptr;
   bool have_fwd_ = false;
   bool bits_pending_ = false;
   bool bits_serial_ = true;
+  bool comm_serial_ = false;  // SPL_SERIAL_COMM=1: backward collectives on the main stream
   bool fused_rs_ = false;  // reduce-scatters fused into the row-parallel GEMMs  // SPL_KEEPBITS_SIDE=1: RNG pass on the side stream
   bool graphs_ = false;
   std::vector<Graph> gfwd_, gbwd_;
@@ -1238,11 +1289,14 @@ class Layer final : public LayerBase {
 }  // namespace
 
 std::unique_ptr<LayerBase> make_layer(const spl_layer_desc& d, int device,
-                                      std::unique_ptr<Comm> comm, std::shared_ptr<WorkPool> pool) {
+                                      std::unique_ptr<Comm> comm, std::shared_ptr<WorkPool> pool,
+                                      std::shared_ptr<WorkPool> params) {
   if (d.dtype == SPL_DTYPE_F32)
-    return std::make_unique<Layer<float>>(d, device, std::move(comm), std::move(pool));
+    return std::make_unique<Layer<float>>(d, device, std::move(comm), std::move(pool),
+                                          std::move(params));
   if (d.dtype == SPL_DTYPE_BF16)
-    return std::make_unique<Layer<bf16>>(d, device, std::move(comm), std::move(pool));
+    return std::make_unique<Layer<bf16>>(d, device, std::move(comm), std::move(pool),
+                                         std::move(params));
   raise(1, "unknown dtype");
 }
 

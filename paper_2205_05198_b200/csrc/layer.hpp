@@ -56,6 +56,10 @@ class LayerBase {
   virtual void set_caller_stream(cudaStream_t s) = 0;
   // Device bytes this layer allocated per BufCat (kWork: only buffers it owns, not a pool's).
   virtual void alloc_bytes(int64_t out[5]) const = 0;
+  // MaskKey microbatch field of the dropout masks of the next calls (rng.cpp:39-45).
+  virtual void set_microbatch(uint32_t microbatch) = 0;
+  // Backward adds its parameter gradients to the held ones instead of overwriting them.
+  virtual void set_grad_accumulate(bool on) = 0;
 };
 
 // Transient device buffers shared by the layers of a stack. Layers of one stack have identical
@@ -77,9 +81,13 @@ struct WorkPool {
   }
 };
 
+// `params`: parameters and gradients shared with the other handles built on the same pool (the
+// i-th parameter / gradient request maps to the same buffer) — the several activation slots
+// of one layer in a microbatch window.
 std::unique_ptr<LayerBase> make_layer(const spl_layer_desc& d, int device,
                                       std::unique_ptr<Comm> comm,
-                                      std::shared_ptr<WorkPool> pool = nullptr);
+                                      std::shared_ptr<WorkPool> pool = nullptr,
+                                      std::shared_ptr<WorkPool> params = nullptr);
 
 // Accountant (activation_memory.cpp:54-82) — exact, floor once.
 int per_layer_bytes_exact(int64_t a, int64_t h, int64_t s, int64_t b, int64_t t, int kind,

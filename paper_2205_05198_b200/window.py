@@ -92,3 +92,77 @@ def stage_timeline(m: ModelShape, stage: int, modes_row, dealloc: bool = True):
     check(lib().spl_stage_timeline(C.byref(m.c()), stage, row, int(dealloc), out, cap,
                                    C.byref(ne), C.byref(peak)))
     return [out[i] for i in range(ne.value)], peak.value
+
+
+class SeqparWindow:
+    """Window executor (spl_window_*): pipeline rank `stage` of p running its 1F1B program over
+    len(modes_row) microbatches with `layers` layers on t simulated ranks; modes_row[i] = 1 keeps
+    microbatch i+1 fully stored (no recompute), 0 checkpoints it under cfg's inner regime.
+    Gradients accumulate over the microbatches; layers(l) gives the parameter / gradient view."""
+
+    def __init__(self, cfg, t: int, layers: int, p: int, stage: int, modes_row,
+                 recompute: str = "selective", sequence_parallel: bool = True,
+                 dtype: str = "bf16", device: int = 0, check_finite: bool = False):
+        from .seqpar import BlockConfig, SeqparLayer, _desc
+        self.cfg, self.t, self.dtype, self.device = cfg, t, dtype, device
+        self.n_mb = len(modes_row)
+        d = _desc(cfg, recompute, sequence_parallel, dtype, check_finite)
+        row = (C.c_uint8 * self.n_mb)(*[1 if v else 0 for v in modes_row])
+        self._w = C.c_void_p()
+        check(lib().spl_window_create_local(C.byref(d), device, t, layers, p, stage, self.n_mb,
+                                            row, C.byref(self._w)))
+        self.layers = []
+        for l in range(layers):
+            h = C.c_void_p()
+            check(lib().spl_window_layer(self._w, l, C.byref(h)))
+            cl = BlockConfig(**{**cfg.__dict__, "layer_index": cfg.layer_index + l})
+            self.layers.append(SeqparLayer(cl, t, recompute, sequence_parallel, dtype, device,
+                                           check_finite, _borrow=h))
+        self.local = self.layers[0].local
+
+    def close(self):
+        for L in getattr(self, "layers", []):
+            L.close()
+        if getattr(self, "_w", None):
+            lib().spl_window_destroy(self._w)
+            self._w = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def shard_shape(self):
+        return self.layers[0].shard_shape()
+
+    def init_params(self, seed: int):
+        for L in self.layers:
+            L.init_params(seed)
+
+    def run(self, x: list, dy: list, y: list | None = None, dx: list | None = None):
+        """x, dy: n_mb lists of local-rank device shards. Returns (y, dx) in the same layout."""
+        import torch
+        check(lib().spl_window_set_stream(
+            self._w, C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+        if len(x) != self.n_mb or len(dy) != self.n_mb:
+            raise ValueError("expected one shard list per microbatch")
+        if y is None:
+            y = [[torch.empty_like(a) for a in mb] for mb in x]
+        if dx is None:
+            dx = [[torch.empty_like(a) for a in mb] for mb in x]
+
+        def arr(ts):
+            flat = [a for mb in ts for a in mb]
+            if len(flat) != self.n_mb * self.local:
+                raise ValueError("expected one shard per rank")
+            return (C.c_void_p * len(flat))(*[a.data_ptr() for a in flat])
+        check(lib().spl_window_run(self._w, arr(x), arr(dy), arr(y), arr(dx)))
+        return y, dx
+
+    def memory(self) -> dict:
+        out = (C.c_int64 * 6)()
+        check(lib().spl_window_memory(self._w, out))
+        keys = ["fully_stored_slots", "checkpointed_slots", "slots_ledger", "live_peak_ledger",
+                "params_and_grads", "workspace"]
+        return dict(zip(keys, list(out)))
