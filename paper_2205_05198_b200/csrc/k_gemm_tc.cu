@@ -367,6 +367,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
   }
+  // Both CTAs must be running before the 2-CTA TMEM allocation: its handshake writes into the
+  // peer's shared memory, and a peer that has not started yet (its SM still busy with another
+  // stream's kernel) loses it and waits forever — an intermittent hang seen under concurrency.
+  cluster_sync_all();
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
