@@ -78,7 +78,6 @@ def main():
                     "sim_peak_bytes": sim_peak, "device_live_peak_ledger": mem["live_peak_ledger"],
                     "slots": [mem["fully_stored_slots"], mem["checkpointed_slots"]],
                     "slots_ledger_bytes": mem["slots_ledger"],
-                    "peak_allocated_torch": torch.cuda.max_memory_allocated(),
                 }), flush=True)
             finally:
                 w.close()
