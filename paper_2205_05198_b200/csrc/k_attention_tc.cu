@@ -112,6 +112,7 @@ struct Rng {
 // fmaheavy ran at 89% (ncu) and the all-funnel-shift form is 7% faster (tools/micro/
 // bench_rng2.cu), so keep_fast uses funnel shifts throughout.
 
+template <bool TIE>
 __global__ void __launch_bounds__(1024, 1) keep_bits_k(DropKey key, int64_t head_offset, int lh,
                                                    int b, int s, int W, int causal,
                                                    uint32_t* __restrict__ bits, ShiftMuls sm) {
@@ -139,10 +140,28 @@ __global__ void __launch_bounds__(1024, 1) keep_bits_k(DropKey key, int64_t head
           const uint32_t hc = hx * 0x1ce4e5b9u;
           if ((blo >> 30) == ((blo + 31u) >> 30)) {
             const uint32_t c30 = __funnelshift_r(blo, bhi, 30);
+            if constexpr (TIE) {
+              bool tie = false;
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (keep_fast<true>(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm, c30))
-                word |= 1u << j;
+              for (int j = 0; j < 32; ++j) {
+                const uint32_t hf = hash_hi<true>(blo + j, bhi, hc, mixed_lo, mixed_hi, sm, c30);
+                if (hf > t_hi) word |= 1u << j;
+                tie |= hf == t_hi;
+              }
+              if (tie) {  // a key's high word equals the threshold's: decide on the low word
+                word = 0;
+#pragma unroll 1
+                for (int j = 0; j < 32; ++j)
+                  if (keep_fast<true>(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm,
+                                      c30))
+                    word |= 1u << j;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (keep_fast<true>(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm, c30))
+                  word |= 1u << j;
+            }
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
@@ -877,9 +896,13 @@ void attn_keep_bits(const AttnArgs& a, cudaStream_t st) {
   // warp than 8 x 256 threads at 32 registers; 1.84 vs 1.92 ms per 22B pass, bench_rng2.cu)
   int64_t grid = (rows + 31) / 32;  // 32 warps (rows) per CTA
   if (grid > kNumSMs) grid = kNumSMs;
-  keep_bits_k<<<(unsigned)grid, 1024, 0, st>>>(a.drop, a.head_offset, (int)a.lh, (int)a.b,
-                                              (int)a.s, W, a.causal, a.keepbits,
-                                              ShiftMuls{4u, 32u, 2u, 1u});
+  static const bool tie = [] {
+    const char* e = std::getenv("SPL_RNG_TIE");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  auto kern = tie ? keep_bits_k<true> : keep_bits_k<false>;
+  kern<<<(unsigned)grid, 1024, 0, st>>>(a.drop, a.head_offset, (int)a.lh, (int)a.b, (int)a.s, W,
+                                        a.causal, a.keepbits, ShiftMuls{4u, 32u, 2u, 1u});
   SPL_CHECK_LAUNCH();
 }
 

@@ -152,6 +152,31 @@ def test_masks_bit_exact(spl, orc, dtype):
         assert np.array_equal(got, ref.interior[1][r * lh:(r + 1) * lh])
 
 
+@pytest.mark.parametrize("side", ["keep", "drop"])
+def test_keep_bits_threshold_tie(spl, orc, side):
+    """The keep-bit pass decides a key on the high word of its hash and re-derives a word when a
+    high word equals the threshold's (probability 2^-32 per key): pick p so that key 0 of the
+    softmax-dropout mask ties, with the low word on either side of the threshold."""
+    import dataclasses
+    # head_dim 64: the tcgen05 attention, which reads the keep-bit pass's bits
+    cfg, x, dy, p = make_case(orc, dict(heads=4, hidden=256, seq=128, batch=2), key=5)
+    key = orc.mask_key_fold(cfg.seed, 0, 0, 1)  # softmax dropout (rng.cuh kSoftmaxDrop)
+    h = orc.hash_counter(key, 0)
+    lo = h & 0xffffffff
+    r = (lo >> 11) if side == "keep" else (lo >> 11) + 1  # threshold low word r<<11 vs lo
+    assert r < (1 << 21)
+    T = ((h >> 32) << 21) | r  # keep iff h >= T * 2^11 (rng.cpp:35-37, block.cpp:63)
+    ptie = T / float(2**53)
+    assert int(np.ceil(ptie * 2.0**53)) == T and 0 < ptie < 1
+    cfg = dataclasses.replace(cfg, dropout_p=ptie)
+    L, *_ = run(spl, cfg, 1, p, x, dy, "none", dtype="bf16")
+    s, b, a = cfg.seq, cfg.batch, cfg.heads
+    got = L.saved(0, "softmax_dropout_mask", (a, b, s, s))
+    want = orc.dropout_mask(key, a * b * s * s, ptie).reshape(a, b, s, s)
+    assert want[0, 0, 0, 0] == (1.0 if side == "keep" else 0.0)
+    assert np.array_equal(got, want)
+
+
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_recompute_bit_exact(spl, orc, dtype):
     """test_seqpar.cpp:248-271 on the device: the interior recomputed from the stored Q/K by
