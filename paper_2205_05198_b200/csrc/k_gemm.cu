@@ -12,12 +12,16 @@ void gemm_tc(const GemmArgs& a, cudaStream_t st);
 
 template <>
 void gemm<float>(const GemmArgs& a, cudaStream_t st) {
+  require(a.a_shards <= 1 && a.b_shards <= 1, "sharded GEMM operands need the tcgen05 path");
   gemm_simt<float>(a, st);
 }
 template <>
 void gemm<bf16>(const GemmArgs& a, cudaStream_t st) {
   if (gemm_tc_supported(a)) gemm_tc(a, st);
-  else gemm_simt<bf16>(a, st);
+  else {
+    require(a.a_shards <= 1 && a.b_shards <= 1, "sharded GEMM operands need the tcgen05 path");
+    gemm_simt<bf16>(a, st);
+  }
 }
 template <>
 int gemm_backend<float>(const GemmArgs&) {

@@ -333,10 +333,23 @@ constexpr int P_A_BYTES = 128 * BK * 2, P_B_BYTES = 128 * BK * 2;
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
 constexpr int P_SMEM = P_STAGES * P_STAGE_BYTES + 1024 + 256;
 
+// Tensor maps of the pair kernel: one per operand, or one per row block of a sharded operand.
+struct PairMaps {
+  CUtensorMap a[GemmArgs::kMaxShards];
+  CUtensorMap b[GemmArgs::kMaxShards];
+};
+// Map and token coordinate of a (possibly sharded) operand: block q = c / rows.
+__device__ __forceinline__ const CUtensorMap* shard_map(const CUtensorMap* maps, int n, int rows,
+                                                        int& c) {
+  if (n <= 1) return maps;
+  const int q = c / rows;
+  c -= q * rows;
+  return maps + q;
+}
+
 template <bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap map_a,
-                        const __grid_constant__ CUtensorMap map_b, const GemmArgs g, int tiles_m,
+    gemm_tc_pair_kernel(const __grid_constant__ PairMaps maps, const GemmArgs g, int tiles_m,
                         int tiles_n, int group, int l2_hint) {
   constexpr int TN = 256;
   extern __shared__ uint8_t smem_raw[];
@@ -364,8 +377,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&tempty[a], 8);  // one arrive per epilogue warp of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+    for (int i = 0; i < (g.a_shards > 1 ? g.a_shards : 1); ++i)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.a[i]) : "memory");
+    for (int i = 0; i < (g.b_shards > 1 ? g.b_shards : 1); ++i)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.b[i]) : "memory");
   }
   // Both CTAs must be running before the 2-CTA TMEM allocation: its handshake writes into the
   // peer's shared memory, and a peer that has not started yet (its SM still busy with another
@@ -402,17 +417,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int k0 = kb * BK;
           // A panels are reused across the whole N sweep of a raster group: evict_last keeps
           // them in L2 while B tiles and the epilogue's output stream through
+          // sharded operands: the token coordinate (A: K when MN-major, else M; B: K when
+          // MN-major) selects the row block, i.e. the rank whose shard holds these rows
+          const int sr = (int)g.shard_rows;
           if (A_MN) {
-            tma_load_2d_pair_hint(sa, &map_a, fb, m0, k0, pol_a);
-            tma_load_2d_pair_hint(sa + 8192, &map_a, fb, m0 + 64, k0, pol_a);
+            int ka = k0;
+            const CUtensorMap* ma = shard_map(maps.a, g.a_shards, sr, ka);
+            tma_load_2d_pair_hint(sa, ma, fb, m0, ka, pol_a);
+            tma_load_2d_pair_hint(sa + 8192, ma, fb, m0 + 64, ka, pol_a);
           } else {
-            tma_load_2d_pair_hint(sa, &map_a, fb, k0, m0, pol_a);
+            int ma0 = m0;
+            const CUtensorMap* ma = shard_map(maps.a, g.a_shards, sr, ma0);
+            tma_load_2d_pair_hint(sa, ma, fb, k0, ma0, pol_a);
           }
           if (B_MN) {
-            tma_load_2d_pair(sb, &map_b, fb, n0, k0);
-            tma_load_2d_pair(sb + 8192, &map_b, fb, n0 + 64, k0);
+            int kb0 = k0;
+            const CUtensorMap* mbp = shard_map(maps.b, g.b_shards, sr, kb0);
+            tma_load_2d_pair(sb, mbp, fb, n0, kb0);
+            tma_load_2d_pair(sb + 8192, mbp, fb, n0 + 64, kb0);
           } else {
-            tma_load_2d_pair(sb, &map_b, fb, k0, n0);
+            tma_load_2d_pair(sb, &maps.b[0], fb, k0, n0);
           }
         }
       }
@@ -598,11 +622,30 @@ void launch_pair(const GemmArgs& g, cudaStream_t st) {
     return true;
   }();
   (void)attr;
-  // per-CTA halves: A 128 rows, B 128 columns
-  const CUtensorMap ma = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64, BK)
-                              : make_map(g.A, g.K, g.M, g.lda, BK, 128);
-  const CUtensorMap mb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, BK)
-                              : make_map(g.B, g.K, g.N, g.ldb, BK, 128);
+  // per-CTA halves: A 128 rows, B 128 columns; a sharded operand gets one map per row block
+  PairMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  if (g.a_shards > 1) {
+    require(g.a_shards <= GemmArgs::kMaxShards && g.shard_rows % (A_MN ? BK : 128) == 0 &&
+                (A_MN ? g.K : g.M) == g.a_shards * g.shard_rows,
+            "gemm_tc: sharded A needs row blocks aligned to the tile");
+    for (int q = 0; q < g.a_shards; ++q)
+      maps.a[q] = A_MN ? make_map(g.a_shard[q], g.M, g.shard_rows, g.lda, 64, BK)
+                       : make_map(g.a_shard[q], g.K, g.shard_rows, g.lda, BK, 128);
+  } else {
+    maps.a[0] = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64, BK)
+                     : make_map(g.A, g.K, g.M, g.lda, BK, 128);
+  }
+  if (g.b_shards > 1) {
+    require(B_MN && g.b_shards <= GemmArgs::kMaxShards && g.shard_rows % BK == 0 &&
+                g.K == g.b_shards * g.shard_rows,
+            "gemm_tc: sharded B must be MN-major with K row blocks aligned to the tile");
+    for (int q = 0; q < g.b_shards; ++q)
+      maps.b[q] = make_map(g.b_shard[q], g.N, g.shard_rows, g.ldb, 64, BK);
+  } else {
+    maps.b[0] = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, BK)
+                     : make_map(g.B, g.K, g.N, g.ldb, BK, 128);
+  }
   const int tiles_m = (int)((g.M + 255) / 256), tiles_n = (int)((g.N + 255) / 256);
   const int ntiles = tiles_m * tiles_n;
   const int pairs = ntiles < kNumSMs / 2 ? ntiles : kNumSMs / 2;
@@ -611,7 +654,7 @@ void launch_pair(const GemmArgs& g, cudaStream_t st) {
     const char* e = std::getenv("SPL_GEMM_L2HINT");
     return (e != nullptr && e[0] == '0') ? 0 : 1;
   }();
-  kern<<<2 * pairs, kThreads, P_SMEM, st>>>(ma, mb, g, tiles_m, tiles_n, group, l2_hint);
+  kern<<<2 * pairs, kThreads, P_SMEM, st>>>(maps, g, tiles_m, tiles_n, group, l2_hint);
   SPL_CHECK_LAUNCH();
 }
 
@@ -655,6 +698,10 @@ bool gemm_tc_supported(const GemmArgs& g) {
   if (g.N % 32 != 0) return false;
   if (g.lda % 8 || g.ldb % 8 || g.ldc % 8) return false;
   if (!aligned16(g.A) || !aligned16(g.B) || !aligned16(g.C)) return false;
+  for (int q = 0; q < g.a_shards; ++q)
+    if (!aligned16(g.a_shard[q])) return false;
+  for (int q = 0; q < g.b_shards; ++q)
+    if (!aligned16(g.b_shard[q])) return false;
   if (g.epi == Epi::BiasGelu && !aligned16(g.C2)) return false;
   if (g.epi == Epi::GeluBwd && (g.ldaux % 8 || !aligned16(g.aux))) return false;
   const bool amn = g.amaj == Major::MN, bmn = g.bmaj == Major::MN;
@@ -678,7 +725,13 @@ static bool pair_enabled() {
   return on;
 }
 
+bool gemm_tc_pair_path(const GemmArgs& g) {
+  return g.N >= 256 && g.M >= 256 && pair_enabled() && gemm_tc_supported(g);
+}
+
 void gemm_tc(const GemmArgs& g, cudaStream_t st) {
+  if (g.a_shards > 1 || g.b_shards > 1)
+    require(g.N >= 256 && g.M >= 256 && pair_enabled(), "sharded GEMM operands need the pair kernel");
   if (g.N >= 256 && g.M >= 256 && pair_enabled()) dispatch_bn<0>(g, st);
   else if (g.N >= 256) dispatch_bn<256>(g, st);
   else dispatch_bn<128>(g, st);

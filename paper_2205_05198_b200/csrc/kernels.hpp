@@ -139,6 +139,15 @@ struct GemmArgs {
   int scatter_n = 0;
   int64_t scatter_rows = 0;
   int accumulate = 0;  // Epi::F32 only: C += A·B (gradient accumulation across microbatches)
+  // Sharded operand (the all-gather fused into the GEMM): when a_shards > 1, A's token
+  // dimension (M for Major::K, K for Major::MN) is split into a_shards row blocks of shard_rows
+  // rows, block q at a_shard[q] (leading dimension lda); likewise B (Major::MN: along K). The
+  // TMA producer of the CTA-pair kernel picks the block of each tile, so no gathered copy exists.
+  static constexpr int kMaxShards = 8;
+  const void* a_shard[kMaxShards] = {};
+  const void* b_shard[kMaxShards] = {};
+  int a_shards = 0, b_shards = 0;
+  int64_t shard_rows = 0;
 };
 // Base of output row m of a GEMM (honours the row scatter).
 template <typename U>
@@ -154,6 +163,9 @@ void gemm(const GemmArgs& a, cudaStream_t st);
 // Which implementation gemm<T> used for these args (for the profiler): 1 = tcgen05.
 template <typename T>
 int gemm_backend(const GemmArgs& a);
+// True when a bf16 GEMM of these arguments runs on the CTA-pair tcgen05 kernel (the only one
+// that takes sharded operands).
+bool gemm_tc_pair_path(const GemmArgs& a);
 
 // ---------------------------------------------------------------- attention
 // Q/K/V packed in one [s*b, ld] buffer: row = s_i*b + b_j; Q cols [qoff + hl*hd, +hd),

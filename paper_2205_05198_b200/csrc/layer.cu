@@ -94,6 +94,14 @@ class Layer final : public LayerBase {
           h_ % 8 == 0)
         fused_rs_ = comm_->p2p_setup((size_t)(RL_ * h_) * sizeof(T));
     }
+    {  // all-gather fused into the consuming GEMMs (their TMA reads every rank's shard): on for
+       // simulated ranks when every consumer runs on the CTA-pair kernel (SPL_FUSED_AG=0: off)
+      const char* f = std::getenv("SPL_FUSED_AG");
+      const bool want = f != nullptr ? f[0] == '1' : true;
+      if (want && std::is_same_v<T, bf16> && sp_ && t_ > 1 && t_ <= GemmArgs::kMaxShards &&
+          comm_->local() == t_ && RL_ % 128 == 0)
+        fused_ag_ = fused_ag_eligible();
+    }
     const char* e = std::getenv("SPL_KEEPBITS_SIDE");
     bits_serial_ = !(e != nullptr && e[0] == '1');
     const char* c = std::getenv("SPL_SERIAL_COMM");
@@ -817,14 +825,73 @@ class Layer final : public LayerBase {
     prof_bytes_[cls] += bytes;
   }
 
-  void gemm(int64_t M, int64_t N, int64_t K, const T* A, int64_t lda, Major am, const T* B,
-            int64_t ldb, Major bm, void* C, int64_t ldc, Epi epi, const float* bias = nullptr,
-            void* C2 = nullptr, const T* aux = nullptr, int64_t ldaux = 0, int scatter_rank = -1) {
+  // Which gathered tensor a GEMM operand is: with the fused all-gather the operand is read
+  // from every rank's shard instead of the gathered copy.
+  enum Gath : int { kNoGath = 0, kGY1, kGY2, kGD };
+  const void* shard_of(Gath w, int q) const {
+    return w == kGY1 ? (const void*)R_[q].y1_s : w == kGY2 ? (const void*)R_[q].y2
+                                                           : (const void*)R_[q].d_s;
+  }
+  GemmArgs gemm_args(int64_t M, int64_t N, int64_t K, const T* A, int64_t lda, Major am,
+                     const T* B, int64_t ldb, Major bm, void* C, int64_t ldc, Epi epi,
+                     Gath ga, Gath gb) const {
     GemmArgs g;
     g.M = M; g.N = N; g.K = K;
     g.A = A; g.lda = lda; g.amaj = am;
     g.B = B; g.ldb = ldb; g.bmaj = bm;
-    g.C = C; g.ldc = ldc; g.epi = epi; g.bias = bias; g.C2 = C2; g.aux = aux; g.ldaux = ldaux;
+    g.C = C; g.ldc = ldc; g.epi = epi;
+    if (ga != kNoGath || gb != kNoGath) {
+      g.shard_rows = RL_;
+      for (int q = 0; q < t_; ++q) {
+        if (ga != kNoGath) g.a_shard[q] = shard_of(ga, q);
+        if (gb != kNoGath) g.b_shard[q] = shard_of(gb, q);
+      }
+      g.a_shards = ga != kNoGath ? t_ : 0;
+      g.b_shards = gb != kNoGath ? t_ : 0;
+    }
+    return g;
+  }
+  // every GEMM that consumes a gathered tensor must run on the pair kernel (probed with the
+  // real buffers of rank 0)
+  bool fused_ag_eligible() const {
+    if (!(RF_ % 256 == 0)) return false;
+    const Rank& R = R_[0];
+    const GemmArgs probes[] = {
+        gemm_args(RF_, 3 * lw_, h_, nullptr, h_, Major::K, R.wqkv, 3 * lw_, Major::MN, R.qkv,
+                  3 * lw_, Epi::Bias, kGY1, kNoGath),
+        gemm_args(RF_, fw_, h_, nullptr, h_, Major::K, R.w1, fw_, Major::MN, R.gin, fw_,
+                  Epi::BiasGelu, kGY2, kNoGath),
+        gemm_args(RF_, fw_, h_, nullptr, h_, Major::K, R.w2, h_, Major::K, R.dgin, fw_,
+                  Epi::GeluBwd, kGD, kNoGath),
+        gemm_args(fw_, h_, RF_, R.fin, fw_, Major::MN, nullptr, h_, Major::MN, R.dw2, h_,
+                  Epi::F32, kNoGath, kGD),
+        gemm_args(h_, fw_, RF_, nullptr, h_, Major::MN, R.dgin, fw_, Major::MN, R.dw1, fw_,
+                  Epi::F32, kGY2, kNoGath),
+        gemm_args(RF_, lw_, h_, nullptr, h_, Major::K, R.wo, h_, Major::K, R.dproj, lw_,
+                  Epi::Store, kGD, kNoGath),
+        gemm_args(lw_, h_, RF_, R.api, lw_, Major::MN, nullptr, h_, Major::MN, R.dwo, h_,
+                  Epi::F32, kNoGath, kGD),
+        gemm_args(h_, 3 * lw_, RF_, nullptr, h_, Major::MN, R.dqkv, 3 * lw_, Major::MN,
+                  R.dwqkv, 3 * lw_, Epi::F32, kGY1, kNoGath)};
+    for (const GemmArgs& g : probes) {
+      GemmArgs p = g;
+      if (p.epi == Epi::BiasGelu) p.C2 = R.fin;
+      if (p.epi == Epi::GeluBwd) {
+        p.aux = R.gin;
+        p.ldaux = fw_;
+      }
+      if (!k::gemm_tc_pair_path(p)) return false;
+    }
+    return true;
+  }
+
+  void gemm(int64_t M, int64_t N, int64_t K, const T* A, int64_t lda, Major am, const T* B,
+            int64_t ldb, Major bm, void* C, int64_t ldc, Epi epi, const float* bias = nullptr,
+            void* C2 = nullptr, const T* aux = nullptr, int64_t ldaux = 0, int scatter_rank = -1,
+            Gath ga = kNoGath, Gath gb = kNoGath) {
+    if (!fused_ag_) ga = gb = kNoGath;
+    GemmArgs g = gemm_args(M, N, K, A, lda, am, B, ldb, bm, C, ldc, epi, ga, gb);
+    g.bias = bias; g.C2 = C2; g.aux = aux; g.ldaux = ldaux;
     g.accumulate = epi == Epi::F32 && grad_acc_;
     if (scatter_rank >= 0) {  // the reduce-scatter fused into this row-parallel GEMM
       for (int q = 0; q < t_; ++q) g.scatter[q] = comm_->p2p_slot(q, rank0_ + scatter_rank);
@@ -878,6 +945,7 @@ class Layer final : public LayerBase {
   void gather(std::function<const void*(int)> shard, std::function<void*(int)> full, CommTag tag) {
     comm_->log(tag, 0, RF_ * h_);
     if (t_ == 1) return;  // identity; callers read the shard itself (see gathered())
+    if (fused_ag_) return;  // the consuming GEMMs read the shards (GemmArgs::a_shard/b_shard)
     auto s = cptrs(shard);
     auto f = mptrs(full);
     launch(K_COMM, 1, 0, (double)RF_ * h_ * sizeof(T) * (t_ - 1) / t_,
@@ -936,7 +1004,7 @@ class Layer final : public LayerBase {
   // returns the event the consumer waits on (nullptr when there is nothing to wait for).
   cudaEvent_t gather_async(std::function<const void*(int)> shard, std::function<void*(int)> full,
                            CommTag tag, cudaEvent_t done) {
-    if (!(sp_ && t_ > 1)) {
+    if (!(sp_ && t_ > 1) || fused_ag_) {
       comm_->log(tag, 0, RF_ * h_);
       return nullptr;
     }
@@ -1034,7 +1102,7 @@ class Layer final : public LayerBase {
       const T* y1 = gathered(r, R.y1_s);
       // fused QKV projection, column-parallel (block.cpp:556-558)
       gemm(RF_, 3 * lw_, h, y1, h, Major::K, R.wqkv, 3 * lw_, Major::MN, R.qkv, 3 * lw_,
-           Epi::Bias, R.bqkv);
+           Epi::Bias, R.bqkv, nullptr, nullptr, 0, -1, kGY1);
       // attention interior + attention over values (block.cpp:559-562)
       k::AttnArgs a = attn_args(r);
       join_keep_bits();
@@ -1072,7 +1140,7 @@ class Layer final : public LayerBase {
       const T* y2 = gathered(r, R.y2);
       // FC1 + bias + GELU, keeping both pre- and post-activation (block.cpp:584-585)
       gemm(RF_, fw_, h, y2, h, Major::K, R.w1, fw_, Major::MN, R.gin, fw_, Epi::BiasGelu, R.b1,
-           R.fin);
+           R.fin, nullptr, 0, -1, kGY2);
       gemm(RF_, h, fw_, R.fin, fw_, Major::K, R.w2, h, Major::MN, R.part, h, Epi::Store,  // 586
            nullptr, nullptr, nullptr, 0, fused_rank(r));
       if (fused_rs_) fused_signal(r);
@@ -1129,9 +1197,10 @@ class Layer final : public LayerBase {
       const T* dmo = gathered_d(r, R.d_s);
       // FC2 dgrad fused with GELU backward (block.cpp:660, 662)
       gemm(RF_, fw_, h, dmo, h, Major::K, R.w2, h, Major::K, R.dgin, fw_, Epi::GeluBwd, nullptr,
-           nullptr, R.gin, fw_);
+           nullptr, R.gin, fw_, -1, kGD);
       // FC2 wgrad (block.cpp:661)
-      gemm(fw_, h, RF_, R.fin, fw_, Major::MN, dmo, h, Major::MN, R.dw2, h, Epi::F32);
+      gemm(fw_, h, RF_, R.fin, fw_, Major::MN, dmo, h, Major::MN, R.dw2, h, Epi::F32, nullptr,
+           nullptr, nullptr, 0, -1, kNoGath, kGD);
       // b1 grad (block.cpp:663)
       launch(K_ELEM, 2, 0, eb * RF_ * fw_, [&] {
         k::colsum_partial<T>(R.dgin, RF_, fw_, fw_, R.partials, kChunkRows, st_);
@@ -1148,7 +1217,8 @@ class Layer final : public LayerBase {
     wait_on(y2_ready);
     for (int r = 0; r < L_; ++r) {  // FC1 wgrad on the re-gathered Y2 (block.cpp:664)
       Rank& R = R_[r];
-      gemm(h, fw_, RF_, gathered(r, R.y2), h, Major::MN, R.dgin, fw_, Major::MN, R.dw1, fw_, Epi::F32);
+      gemm(h, fw_, RF_, gathered(r, R.y2), h, Major::MN, R.dgin, fw_, Major::MN, R.dw1, fw_, Epi::F32,
+           nullptr, nullptr, nullptr, 0, -1, kGY2);
     }
     wait_on(rs_done);
     if (fused_rs_)
@@ -1183,8 +1253,10 @@ class Layer final : public LayerBase {
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
       const T* dao = gathered_d(r, R.d_s);
-      gemm(RF_, lw_, h, dao, h, Major::K, R.wo, h, Major::K, R.dproj, lw_, Epi::Store);  // 699
-      gemm(lw_, h, RF_, R.api, lw_, Major::MN, dao, h, Major::MN, R.dwo, h, Epi::F32);    // 700
+      gemm(RF_, lw_, h, dao, h, Major::K, R.wo, h, Major::K, R.dproj, lw_, Epi::Store,  // 699
+           nullptr, nullptr, nullptr, 0, -1, kGD);
+      gemm(lw_, h, RF_, R.api, lw_, Major::MN, dao, h, Major::MN, R.dwo, h, Epi::F32,  // 700
+           nullptr, nullptr, nullptr, 0, -1, kNoGath, kGD);
       k::AttnArgs a = attn_args(r);
       join_keep_bits();
       launch(K_ATTN, 3, attn_flops(true), 0,
@@ -1205,7 +1277,7 @@ class Layer final : public LayerBase {
     for (int r = 0; r < L_; ++r) {  // QKV wgrad on the re-gathered Y1 (block.cpp:706-708)
       Rank& R = R_[r];
       gemm(h, 3 * lw_, RF_, gathered(r, R.y1_s), h, Major::MN, R.dqkv, 3 * lw_, Major::MN,
-           R.dwqkv, 3 * lw_, Epi::F32);
+           R.dwqkv, 3 * lw_, Epi::F32, nullptr, nullptr, nullptr, 0, -1, kGY1);
     }
     wait_on(rs_done);
     if (fused_rs_)
@@ -1269,6 +1341,7 @@ class Layer final : public LayerBase {
   bool bits_pending_ = false;
   bool bits_serial_ = true;
   bool comm_serial_ = false;  // SPL_SERIAL_COMM=1: backward collectives on the main stream
+  bool fused_ag_ = false;     // all-gather fused into the consuming GEMMs (simulated ranks)
   bool fused_rs_ = false;  // reduce-scatters fused into the row-parallel GEMMs  // SPL_KEEPBITS_SIDE=1: RNG pass on the side stream
   bool graphs_ = false;
   std::vector<Graph> gfwd_, gbwd_;

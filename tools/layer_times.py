@@ -20,9 +20,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 # Per-GPU compute = step minus the collective class, so the simulated ranks use the
-# collective-based reduce-scatter (the NCCL ranks' default) unless told otherwise: with the
-# fused reduce-scatter the slot reduction runs inside the consumers and cannot be separated.
+# collective-based reduce-scatter and all-gather (the NCCL ranks' default) unless told
+# otherwise: fused, the slot reduction / shard reads run inside the consumers.
 os.environ.setdefault("SPL_FUSED_RS", "0")
+os.environ.setdefault("SPL_FUSED_AG", "0")
 
 CONFIGS = {"22B": (64, 6144, 2048, 4), "175B": (96, 12288, 2048, 1), "530B": (128, 20480, 2048, 1),
            "1T": (160, 25600, 2048, 1)}
