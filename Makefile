@@ -19,7 +19,7 @@ SRC := $(wildcard $(PKG)/csrc/*.cu)
 OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
 HDR := $(wildcard $(PKG)/csrc/*.hpp $(PKG)/csrc/*.cuh) include/spl.h
 
-all: $(PKG)/libspl.so oracle build/test_facade
+all: $(PKG)/libspl.so oracle build/test_facade build/test_window_facade
 
 build/%.o: $(PKG)/csrc/%.cu $(HDR)
 	@mkdir -p build
@@ -31,6 +31,9 @@ $(PKG)/libspl.so: $(OBJ)
 build/test_facade: tests/cpp/test_facade.cpp include/spl_seqpar.hpp include/spl.h $(PKG)/libspl.so
 	g++ -std=c++17 -O2 -Wall -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -lspl \
 	    -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
+
+build/test_window_facade: tests/cpp/test_window_facade.cpp include/spl_pipeline.hpp include/spl.h $(PKG)/libspl.so
+	g++ -std=c++17 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -lspl -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 oracle:
 	$(MAKE) -C oracle

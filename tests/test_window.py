@@ -142,3 +142,17 @@ def test_window_matches_oracle_random():
             with pytest.raises(spl.InfeasibleBudget) as e:
                 spl.window_plan(m, lo - 1)
             assert e.value.min_feasible_budget == lo
+
+
+def test_cpp_pipeline_facade():
+    """The reference's window cases restated in C++ against include/spl_pipeline.hpp (the
+    actplan::pipeline signatures over the C ABI); host-only."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "build", "test_window_facade")
+    subprocess.run(["make", "build/test_window_facade"], cwd=root, check=True,
+                   capture_output=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 failures" in r.stdout
