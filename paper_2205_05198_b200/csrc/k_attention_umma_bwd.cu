@@ -11,6 +11,7 @@
 //   MMA   S = Q·Kᵀ, dP = dO·Vᵀ; warps dS (same keep bits); MMA dQ += dS·K.
 // The counter-RNG pass that fills the keep bits (attn_keep_bits) runs once per backward.
 #include <cstring>
+#include <type_traits>
 #include <mutex>
 #include <unordered_map>
 
@@ -291,6 +292,12 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(&w_free[st], ((it >> 1) & 1) ^ 1);
       const int q0h = qb + 32 * half;
       uint32_t pw[16], dw[16];
+      // interior tiles (every query and key in range, below the causal diagonal) skip the
+      // per-element validity test
+      const bool full = qb + 64 <= S && k0 + 128 <= S && !(CAUSAL && k0 + 127 > qb) &&
+                        !a.masked_only;
+      auto pd_loop = [&](auto masked) {
+      constexpr bool kMasked = decltype(masked)::value;
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
         float pv[2], dv[2];
@@ -298,7 +305,7 @@ __global__ void __launch_bounds__(320, 1)
         for (int u = 0; u < 2; ++u) {
           const int e = i + u;
           const int q = q0h + e;
-          const bool valid = q < S && key < S && !(CAUSAL && key > q);
+          const bool valid = !kMasked || (q < S && key < S && !(CAUSAL && key > q));
           const float dqe = __shfl_sync(0xffffffffu, dl_l, e);
           bool keep;
           float p;
@@ -321,6 +328,9 @@ __global__ void __launch_bounds__(320, 1)
         pw[i >> 1] = pack_bf16(pv[0], pv[1]);
         dw[i >> 1] = pack_bf16(dv[0], dv[1]);
       }
+      };
+      if (full) pd_loop(std::false_type{});
+      else pd_loop(std::true_type{});
       if constexpr (!STORED) {
         // P̃ᵀ / dSᵀ as bf16 pairs over the first 16 of this half's (consumed) 32 Sᵀ / dPᵀ columns
         tmem_st16u(tl + S_COL + sb * 64 + half * 32, pw);
@@ -583,26 +593,33 @@ __global__ void __launch_bounds__(320, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sd_free[st]);
       mbar_wait(&w_free[st], ((it >> 1) & 1) ^ 1);
-      const bool full = kc0 + 32 <= S && !(CAUSAL && kc0 + 31 > q0) && q0 + 128 <= S;
+      const bool full = kc0 + 32 <= S && !(CAUSAL && kc0 + 31 > q0) && q0 + 128 <= S &&
+                        !a.masked_only;
       uint32_t dw[16];
+      // two copies of the element loop: interior tiles skip the per-element bounds / causal test
+      auto ds_loop = [&](auto masked) {
+        constexpr bool kMasked = decltype(masked)::value;
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        float dv[2];
+        for (int i = 0; i < 32; i += 2) {
+          float dv[2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int e = i + u;
-          const bool keep = (word >> e) & 1u;
-          float p;
-          if constexpr (STORED)
-            p = __uint_as_float((e & 1) ? (pst[e >> 1] & 0xffff0000u) : (pst[e >> 1] << 16));
-          else
-            p = ex2(__uint_as_float(rs[e]) * sl2 - lse2);
-          if (!full && (kc0 + e >= S || qr >= S || (CAUSAL && kc0 + e > qr))) p = 0.f;
-          const float dpk = keep ? __uint_as_float(rp[e]) * inv_keep : 0.f;
-          dv[u] = p * (dpk - dl);
+          for (int u = 0; u < 2; ++u) {
+            const int e = i + u;
+            const bool keep = (word >> e) & 1u;
+            float p;
+            if constexpr (STORED)
+              p = __uint_as_float((e & 1) ? (pst[e >> 1] & 0xffff0000u) : (pst[e >> 1] << 16));
+            else
+              p = ex2(__uint_as_float(rs[e]) * sl2 - lse2);
+            if (kMasked && (kc0 + e >= S || qr >= S || (CAUSAL && kc0 + e > qr))) p = 0.f;
+            const float dpk = keep ? __uint_as_float(rp[e]) * inv_keep : 0.f;
+            dv[u] = p * (dpk - dl);
+          }
+          dw[i >> 1] = pack_bf16(dv[0], dv[1]);
         }
-        dw[i >> 1] = pack_bf16(dv[0], dv[1]);
-      }
+      };
+      if (full) ds_loop(std::false_type{});
+      else ds_loop(std::true_type{});
       if constexpr (!STORED) {
         tmem_st16u(tl + st * 64 + half * 32, dw);  // over this half's consumed S columns
         tmem_st_wait();
@@ -708,8 +725,14 @@ bool attn_bwd_umma_supported(const AttnArgs& a) {
          ((uintptr_t)a.o & 15) == 0 && a.s < (1 << 30);
 }
 
-void attn_bwd_umma(const AttnArgs& a, const void* dout, void* dqkv, const float* delta,
+void attn_bwd_umma(const AttnArgs& a_in, const void* dout, void* dqkv, const float* delta,
                    cudaStream_t st) {
+  static const int masked_only = [] {
+    const char* e = std::getenv("SPL_ATTN_MASKED_ONLY");
+    return (e != nullptr && e[0] == '1') ? 1 : 0;
+  }();
+  AttnArgs a = a_in;
+  a.masked_only = masked_only;
   const bf16* d = static_cast<const bf16*>(dout);
   bf16* g = static_cast<bf16*>(dqkv);
 #define SPL_BWD_CASE(HDX)                                                                        \

@@ -188,6 +188,7 @@ struct AttnArgs {
   // softmax-dropout keep bits [lh*b*s][ceil(s/32)] from attn_keep_bits (bf16 tensor-core path);
   // a transient buffer refilled before each attention forward and backward.
   uint32_t* keepbits = nullptr;
+  int masked_only = 0;  // backward: 1 = every tile through the per-element validity path (A/B)
 };
 inline int64_t keepbits_words(int64_t lh, int64_t b, int64_t s) { return lh * b * s * ((s + 31) / 32); }
 // Forward. If a.sm != nullptr the interior is materialised (softmax_out, mask, dropout_out).
