@@ -87,9 +87,23 @@ struct DkdvLayout {
     static constexpr int W_OFF = QD_OFF + NS * 2 * C::T64;
     static constexpr int SMM_OFF = W_OFF + (STORED ? 4 * C::W_BYTES : 0);
     static constexpr int BAR_OFF = SMM_OFF + (STORED ? NS * (SMT + MKT) : 0);
-    static constexpr int SMEM = BAR_OFF + 256 + 1024;
+    // [2 tiles][8 warps][32 queries] (log2 lse, rowdot) pairs, read as broadcasts
+    static constexpr int STAT_OFF = BAR_OFF + 256;
+    static constexpr int SMEM = STAT_OFF + 2 * 8 * 32 * 8 + 1024;
   };
 };
+
+// 32 x 32 bit transpose across a warp: lane r holds row r (bit c = column c) on entry and
+// column r (bit c = row c) on exit; five butterfly rounds of one shuffle each.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+  uint32_t m = 0x0000ffffu;
+#pragma unroll
+  for (int j = 16; j != 0; j >>= 1, m ^= m << j) {
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+    x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y & m) << j));
+  }
+  return x;
+}
 
 template <int HD, bool CAUSAL, bool STORED>
 __global__ void __launch_bounds__(320, 1)
@@ -278,6 +292,16 @@ __global__ void __launch_bounds__(320, 1)
       const float lse_l = lse_n * kLog2e, dl_l = dl_n;
       const uint32_t kw_l = kw_n;
       row_stats(it + 1, lse_n, dl_n, kw_n);
+      // this tile's row stats as smem broadcasts and the keep bits transposed to (this key,
+      // the 32 queries): no per-element shuffles
+      const bool shfl = a.stats_shfl != 0;
+      float2* stat = reinterpret_cast<float2*>(smem + Lay::STAT_OFF) + ((it & 1) * 8 + (warp - 2)) * 32;
+      uint32_t kt = 0u;
+      if (!shfl) {
+        stat[lane] = make_float2(lse_l, dl_l);
+        if constexpr (!STORED) kt = warp_transpose32(kw_l, lane);
+        __syncwarp();
+      }
       if (STORED) mbar_wait(&qd_full[it % NS], (it / NS) & 1);  // stored P / mask tiles landed
       const int sb = it % SB;
       mbar_wait(&sd_full[sb], (it / SB) & 1);
@@ -306,7 +330,8 @@ __global__ void __launch_bounds__(320, 1)
           const int e = i + u;
           const int q = q0h + e;
           const bool valid = !kMasked || (q < S && key < S && !(CAUSAL && key > q));
-          const float dqe = __shfl_sync(0xffffffffu, dl_l, e);
+          const float2 qs = shfl ? make_float2(0.f, 0.f) : stat[e];
+          const float dqe = shfl ? __shfl_sync(0xffffffffu, dl_l, e) : qs.y;
           bool keep;
           float p;
           if constexpr (STORED) {
@@ -316,8 +341,8 @@ __global__ void __launch_bounds__(320, 1)
             p = valid ? __bfloat162float(reinterpret_cast<const bf16*>(St)[qi * 128 + row]) : 0.f;
             keep = St[SMT + qi * 128 + row] != 0;
           } else {
-            keep = (__shfl_sync(0xffffffffu, kw_l, e) >> lane) & 1u;
-            const float lqe = __shfl_sync(0xffffffffu, lse_l, e);
+            keep = shfl ? (__shfl_sync(0xffffffffu, kw_l, e) >> lane) & 1u : (kt >> e) & 1u;
+            const float lqe = shfl ? __shfl_sync(0xffffffffu, lse_l, e) : qs.x;
             p = valid ? ex2(__uint_as_float(rs[e]) * sl2 - lqe) : 0.f;
           }
           keep = keep && valid;
@@ -731,8 +756,13 @@ void attn_bwd_umma(const AttnArgs& a_in, const void* dout, void* dqkv, const flo
     const char* e = std::getenv("SPL_ATTN_MASKED_ONLY");
     return (e != nullptr && e[0] == '1') ? 1 : 0;
   }();
+  static const int stats_shfl = [] {
+    const char* e = std::getenv("SPL_ATTN_SHFL");
+    return (e != nullptr && e[0] == '1') ? 1 : 0;
+  }();
   AttnArgs a = a_in;
   a.masked_only = masked_only;
+  a.stats_shfl = stats_shfl;
   const bf16* d = static_cast<const bf16*>(dout);
   bf16* g = static_cast<bf16*>(dqkv);
 #define SPL_BWD_CASE(HDX)                                                                        \

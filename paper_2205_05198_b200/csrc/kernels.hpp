@@ -189,6 +189,7 @@ struct AttnArgs {
   // a transient buffer refilled before each attention forward and backward.
   uint32_t* keepbits = nullptr;
   int masked_only = 0;  // backward: 1 = every tile through the per-element validity path (A/B)
+  int stats_shfl = 0;   // dK/dV: 1 = per-element shuffles for row stats / keep bits (A/B)
 };
 inline int64_t keepbits_words(int64_t lh, int64_t b, int64_t s) { return lh * b * s * ((s + 31) / 32); }
 // Forward. If a.sm != nullptr the interior is materialised (softmax_out, mask, dropout_out).
