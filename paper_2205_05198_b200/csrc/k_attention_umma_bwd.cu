@@ -295,10 +295,12 @@ __global__ void __launch_bounds__(320, 1)
       // this tile's row stats as smem broadcasts and the keep bits transposed to (this key,
       // the 32 queries): no per-element shuffles
       const bool shfl = a.stats_shfl != 0;
-      float2* stat = reinterpret_cast<float2*>(smem + Lay::STAT_OFF) + ((it & 1) * 8 + (warp - 2)) * 32;
+      // [-lse (log2) x 32 queries][-rowdot x 32 queries] of this warp, per tile parity
+      float* stat = reinterpret_cast<float*>(smem + Lay::STAT_OFF) + ((it & 1) * 8 + (warp - 2)) * 64;
       uint32_t kt = 0u;
       if (!shfl) {
-        stat[lane] = make_float2(lse_l, dl_l);
+        stat[lane] = -lse_l;
+        stat[32 + lane] = -dl_l;
         if constexpr (!STORED) kt = warp_transpose32(kw_l, lane);
         __syncwarp();
       }
@@ -322,6 +324,40 @@ __global__ void __launch_bounds__(320, 1)
                         !a.masked_only;
       auto pd_loop = [&](auto masked) {
       constexpr bool kMasked = decltype(masked)::value;
+      if constexpr (!STORED) {
+        if (!shfl) {  // element pairs in packed fp32x2 arithmetic (same ops as the scalar form)
+          const uint64_t sl2x2 = f32x2(sl2, sl2);
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const uint64_t nl2 = *reinterpret_cast<const uint64_t*>(stat + i);
+            const uint64_t nd2 = *reinterpret_cast<const uint64_t*>(stat + 32 + i);
+            float s0, s1;
+            f32x2_split(ffma2(f32x2(__uint_as_float(rs[i]), __uint_as_float(rs[i + 1])), sl2x2, nl2),
+                        s0, s1);
+            float p0 = ex2(s0), p1 = ex2(s1);
+            bool k0 = (kt >> i) & 1u, k1 = (kt >> (i + 1)) & 1u;
+            if constexpr (kMasked) {
+              const int qa = q0h + i, qb1 = q0h + i + 1;
+              const bool v0 = qa < S && key < S && !(CAUSAL && key > qa);
+              const bool v1 = qb1 < S && key < S && !(CAUSAL && key > qb1);
+              p0 = v0 ? p0 : 0.f;
+              p1 = v1 ? p1 : 0.f;
+              k0 = k0 && v0;
+              k1 = k1 && v1;
+            }
+            const uint64_t kf2 = f32x2(k0 ? inv_keep : 0.f, k1 ? inv_keep : 0.f);
+            const uint64_t p2 = f32x2(p0, p1);
+            float a0, a1, b0, b1;
+            f32x2_split(fmul2(p2, kf2), a0, a1);
+            f32x2_split(
+                fmul2(p2, ffma2(f32x2(__uint_as_float(rp[i]), __uint_as_float(rp[i + 1])), kf2, nd2)),
+                b0, b1);
+            pw[i >> 1] = pack_bf16(a0, a1);
+            dw[i >> 1] = pack_bf16(b0, b1);
+          }
+          return;
+        }
+      }
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
         float pv[2], dv[2];
@@ -330,7 +366,7 @@ __global__ void __launch_bounds__(320, 1)
           const int e = i + u;
           const int q = q0h + e;
           const bool valid = !kMasked || (q < S && key < S && !(CAUSAL && key > q));
-          const float2 qs = shfl ? make_float2(0.f, 0.f) : stat[e];
+          const float2 qs = shfl ? make_float2(0.f, 0.f) : make_float2(-stat[e], -stat[32 + e]);
           const float dqe = shfl ? __shfl_sync(0xffffffffu, dl_l, e) : qs.y;
           bool keep;
           float p;
