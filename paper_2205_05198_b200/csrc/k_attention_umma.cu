@@ -415,10 +415,15 @@ __global__ void __launch_bounds__(320, 1)
         const bool full = tile_full(j);
         const int k0 = j * 128 + half * 64;
         float v[64];
+        {  // scores · scale·log2e in packed fp32x2 multiplies (bit-identical to the scalar form)
+          const uint64_t sl2x2 = f32x2(sl2, sl2);
   #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          v[i] = __uint_as_float(r0[i]) * sl2;
-          v[32 + i] = __uint_as_float(r1[i]) * sl2;
+          for (int i = 0; i < 32; i += 2) {
+            f32x2_split(fmul2(f32x2(__uint_as_float(r0[i]), __uint_as_float(r0[i + 1])), sl2x2),
+                        v[i], v[i + 1]);
+            f32x2_split(fmul2(f32x2(__uint_as_float(r1[i]), __uint_as_float(r1[i + 1])), sl2x2),
+                        v[32 + i], v[32 + i + 1]);
+          }
         }
         if (!full) {
   #pragma unroll
@@ -460,15 +465,17 @@ __global__ void __launch_bounds__(320, 1)
         }
         uint32_t pk[32];
         float ls = 0.f;
+        const uint64_t nmm2 = f32x2(-mm, -mm);
   #pragma unroll
         for (int i = 0; i < 64; i += 2) {
-          float p2[2];
+          float x[2], p2[2];
+          f32x2_split(fadd2(f32x2(v[i], v[i + 1]), nmm2), x[0], x[1]);  // v - m, packed
   #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int e = i + u;
             const uint32_t word = e < 32 ? wcur.x : wcur.y;
             const bool keep = (word >> (e & 31)) & 1u;
-            const float p = ex2(v[e] - mm);
+            const float p = ex2(x[u]);
             ls += p;
             p2[u] = keep ? p : 0.f;
           }

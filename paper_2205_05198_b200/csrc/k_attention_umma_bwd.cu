@@ -662,6 +662,27 @@ __global__ void __launch_bounds__(320, 1)
       // two copies of the element loop: interior tiles skip the per-element bounds / causal test
       auto ds_loop = [&](auto masked) {
         constexpr bool kMasked = decltype(masked)::value;
+        if constexpr (!STORED) {  // element pairs in packed fp32x2 arithmetic (bit-identical)
+          const uint64_t sl2x2 = f32x2(sl2, sl2), nl2 = f32x2(-lse2, -lse2),
+                         nd2 = f32x2(-dl, -dl);
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float s0, s1;
+            f32x2_split(ffma2(f32x2(__uint_as_float(rs[i]), __uint_as_float(rs[i + 1])), sl2x2, nl2),
+                        s0, s1);
+            float p0 = ex2(s0), p1 = ex2(s1);
+            if (kMasked && (kc0 + i >= S || qr >= S || (CAUSAL && kc0 + i > qr))) p0 = 0.f;
+            if (kMasked && (kc0 + i + 1 >= S || qr >= S || (CAUSAL && kc0 + i + 1 > qr))) p1 = 0.f;
+            const uint64_t kf2 = f32x2((word >> i) & 1u ? inv_keep : 0.f,
+                                       (word >> (i + 1)) & 1u ? inv_keep : 0.f);
+            float d0, d1;
+            f32x2_split(fmul2(f32x2(p0, p1), ffma2(f32x2(__uint_as_float(rp[i]),
+                                                         __uint_as_float(rp[i + 1])), kf2, nd2)),
+                        d0, d1);
+            dw[i >> 1] = pack_bf16(d0, d1);
+          }
+          return;
+        }
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
           float dv[2];
