@@ -69,6 +69,10 @@ void spl_desc_default(spl_layer_desc* d);
 /* t simulated ranks on one CUDA device (the reference's in-process harness,
  * seqpar_block_forward(x_shards, params, t, cfg), block.cpp:512). */
 int spl_create_local(const spl_layer_desc* d, int device, int t, spl_handle** out);
+/* The SURVEY §8(b) form: t ranks on devices[0..t-1]. A handle drives one device, so every
+ * entry must name the same GPU (the t ranks are then simulated on it, = spl_create_local);
+ * a t-GPU group is one process per GPU with spl_create_nccl. */
+int spl_create(const spl_layer_desc* d, const int* devices, int t, spl_handle** out);
 /* One rank of a t-way tensor-parallel group over NCCL (one process per GPU). `nccl_id` is the
  * 128-byte ncclUniqueId from spl_nccl_unique_id() on rank 0, distributed by the caller. */
 int spl_nccl_unique_id(unsigned char id_out[128]);

@@ -64,6 +64,7 @@ def lib():
     sig = {
         "spl_desc_default": (None, [P(LayerDesc)]),
         "spl_create_local": (I32, [P(LayerDesc), I32, I32, P(H)]),
+        "spl_create": (I32, [P(LayerDesc), P(I32), I32, P(H)]),
         "spl_nccl_unique_id": (I32, [C.c_char_p]),
         "spl_create_nccl": (I32, [P(LayerDesc), I32, I32, I32, C.c_char_p, P(H)]),
         "spl_destroy": (I32, [H]),

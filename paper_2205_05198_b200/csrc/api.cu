@@ -139,6 +139,17 @@ int spl_create_local(const spl_layer_desc* d, int device, int t, spl_handle** ou
   });
 }
 
+int spl_create(const spl_layer_desc* d, const int* devices, int t, spl_handle** out) {
+  return guard([&] {
+    spl::require(d != nullptr && devices != nullptr && out != nullptr, "null argument");
+    spl::require(t >= 1, "t must be >= 1");
+    for (int r = 1; r < t; ++r)
+      spl::require(devices[r] == devices[0],
+                   "one handle drives one GPU: use spl_create_nccl, one process per GPU");
+    *out = make_handle(d, devices[0], spl::make_local_comm(t));
+  });
+}
+
 int spl_nccl_unique_id(unsigned char id_out[128]) {
   return guard([&] {
     ncclUniqueId id;

@@ -446,3 +446,34 @@ def test_full_width_self_consistency(spl, orc, shape, t):
         assert rel_l2(y, ref[0]) <= 1e-2, key
         assert rel_l2(dx, ref[1]) <= 1e-2, key
         assert rel_l2(gr, ref[2]) <= 2e-2, key
+
+
+def test_spl_create_survey_form(spl, orc):
+    """spl_create(desc, devices, t): t ranks on one device equal
+    spl_create_local bit-for-bit; devices naming two GPUs are refused (one process per GPU)."""
+    import ctypes as C
+    import torch
+    from paper_2205_05198_b200 import _lib
+    from paper_2205_05198_b200.seqpar import _desc
+    cfg, x, dy, p = make_case(orc, TINY, key=13)
+    c = to_spl_cfg(spl, cfg)
+    t = 2
+    ref = spl.SeqparLayer(c, t, "selective", True, "bf16")
+    ref.load_params(p)
+    d = _desc(c, "selective", True, "bf16", True)
+    h = C.c_void_p()
+    devs = (C.c_int * t)(0, 0)
+    _lib.check(_lib.lib().spl_create(C.byref(d), devs, t, C.byref(h)))
+    L = spl.SeqparLayer(c, t, "selective", True, "bf16", _borrow=h)
+    L.load_params(p)
+    xs = [torch.from_numpy(s.copy()).to("cuda", torch.bfloat16) for s in np.split(x, t, 0)]
+    ds = [torch.from_numpy(s.copy()).to("cuda", torch.bfloat16) for s in np.split(dy, t, 0)]
+    for a, b in zip(ref.forward(xs), L.forward(xs)):
+        assert torch.equal(a, b)
+    for a, b in zip(ref.backward(ds), L.backward(ds)):
+        assert torch.equal(a, b)
+    np.testing.assert_array_equal(ref.grads(), L.grads())
+    _lib.lib().spl_destroy(h)
+    h2 = C.c_void_p()
+    rc = _lib.lib().spl_create(C.byref(d), (C.c_int * 2)(0, 1), 2, C.byref(h2))
+    assert rc == _lib.SPL_EINVAL
