@@ -398,11 +398,14 @@ __global__ void __launch_bounds__(320, 1)
         return w;
       };
       auto pair_sync = [&] { asm volatile("bar.sync %0, 64;" ::"r"(2 + qd) : "memory"); };
+      // keep-bit words two tiles ahead (the loads miss L2 and were waited on one tile ahead)
       uint2 wnext = nkv > 0 ? load_words(0) : make_uint2(0u, 0u);
+      uint2 wnext2 = nkv > 1 ? load_words(1) : make_uint2(0u, 0u);
       for (int j = 0; j < nkv; ++j, ++sc) {
         const int sb = sc & 1, pb = j & 1;
         const uint2 wcur = wnext;
-        if (j + 1 < nkv) wnext = load_words(j + 1);
+        wnext = wnext2;
+        if (j + 2 < nkv) wnext2 = load_words(j + 2);
         mbar_wait(&s_full[sb], (sc >> 1) & 1);
         tc_fence_after();
         uint32_t r0[32], r1[32];
