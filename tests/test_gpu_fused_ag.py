@@ -25,12 +25,12 @@ def spl():
     return m
 
 
-def _run(spl, t, recompute, fused):
+def _run(spl, t, recompute, fused, causal=False):
     import torch
     old = os.environ.get("SPL_FUSED_AG")
     os.environ["SPL_FUSED_AG"] = "1" if fused else "0"
     try:
-        cfg = spl.BlockConfig(**SHAPE, dropout_p=0.1, seed=42)
+        cfg = spl.BlockConfig(**SHAPE, dropout_p=0.1, causal=causal, seed=42)
         L = spl.SeqparLayer(cfg, t, recompute, True, "bf16", check_finite=False)
     finally:
         if old is None:
@@ -67,3 +67,12 @@ def test_fused_allgather_bit_identical(spl, t, recompute):
     # the fused layer launched no all-gather copies: 2 (forward) + 2 (backward dgrad gathers)
     # + 2 re-gathers fewer (full recompute: + 2 in the re-run forward)
     assert n1 < n0
+
+
+def test_fused_allgather_causal(spl):
+    import torch
+    y0, dx0, g0, _, _ = _run(spl, 2, "selective", fused=False, causal=True)
+    y1, dx1, g1, _, _ = _run(spl, 2, "selective", fused=True, causal=True)
+    assert all(torch.equal(a, b) for a, b in zip(y0, y1))
+    assert all(torch.equal(a, b) for a, b in zip(dx0, dx1))
+    np.testing.assert_array_equal(g0, g1)

@@ -32,16 +32,21 @@ def _inputs(torch, n_mb, local, shp, seed):
     return [mk() for _ in range(n_mb)], [mk() for _ in range(n_mb)]
 
 
-@pytest.mark.parametrize("inner,t,p,stage,modes", [
-    ("selective", 1, 3, 0, [1, 0, 0, 1, 0]),
-    ("full", 2, 3, 1, [0, 1, 1, 0]),
-    ("selective", 2, 2, 0, [0, 0, 0]),
-    ("full", 1, 2, 1, [1, 1, 1]),
+# the last case is large enough for the fused all-gather (h/t >= 256, RF multiple of 256)
+WIDE = dict(heads=8, hidden=1024, seq=256, batch=2)
+
+
+@pytest.mark.parametrize("inner,t,p,stage,modes,shape", [
+    ("selective", 1, 3, 0, [1, 0, 0, 1, 0], SHAPE),
+    ("full", 2, 3, 1, [0, 1, 1, 0], SHAPE),
+    ("selective", 2, 2, 0, [0, 0, 0], SHAPE),
+    ("full", 1, 2, 1, [1, 1, 1], SHAPE),
+    ("selective", 2, 2, 0, [1, 0, 1], WIDE),
 ])
-def test_window_matches_standalone(spl, inner, t, p, stage, modes):
+def test_window_matches_standalone(spl, inner, t, p, stage, modes, shape):
     import torch
     L = 2
-    cfg = spl.BlockConfig(**SHAPE, dropout_p=0.1, seed=42)
+    cfg = spl.BlockConfig(**shape, dropout_p=0.1, seed=42)
     w = spl.SeqparWindow(cfg, t, L, p, stage, modes, recompute=inner)
     for l, lay in enumerate(w.layers):
         lay.init_params(100 + l)
@@ -52,7 +57,7 @@ def test_window_matches_standalone(spl, inner, t, p, stage, modes):
     got = [lay.grads() for lay in w.layers]
     acc = [None] * L
     for i, m in enumerate(modes):  # backward order of the rank program: microbatch 1..n_mb
-        ci = spl.BlockConfig(**SHAPE, dropout_p=0.1, seed=42, microbatch=i + 1)
+        ci = spl.BlockConfig(**shape, dropout_p=0.1, seed=42, microbatch=i + 1)
         st = spl.SeqparStack(ci, t, L, "none" if m else inner, check_finite=False)
         for l, lay in enumerate(st.layers):
             lay.init_params(100 + l)
