@@ -111,3 +111,36 @@ def test_window_errors(spl):
         spl.SeqparWindow(cfg, 1, 1, 2, 0, [1, 0], recompute="none")  # checkpointed needs inner
     with pytest.raises(ValueError):
         spl.SeqparWindow(cfg, 1, 1, 2, 2, [1, 0])  # stage >= p
+
+
+def test_window_f32_accumulation(spl):
+    """The exact-fp32 execution dtype (SIMT GEMMs): accumulated gradients equal the fp32 running
+    sum of standalone runs bit-for-bit (the SIMT epilogue's C += A·B path)."""
+    import torch
+    L, t, p, stage, modes = 1, 2, 2, 0, [1, 0, 0]
+    cfg = spl.BlockConfig(**SHAPE, dropout_p=0.1, seed=42)
+    w = spl.SeqparWindow(cfg, t, L, p, stage, modes, recompute="selective", dtype="f32")
+    w.layers[0].init_params(3)
+    g = torch.Generator(device="cuda:0").manual_seed(5)
+    shp = w.shard_shape()
+    mk = lambda: [(torch.rand(shp, generator=g, device="cuda") * 2 - 1) for _ in range(t)]  # noqa
+    x = [mk() for _ in modes]
+    dy = [mk() for _ in modes]
+    y, dx = w.run(x, dy)
+    torch.cuda.synchronize()
+    got = w.layers[0].grads()
+    acc = None
+    for i, m in enumerate(modes):
+        ci = spl.BlockConfig(**SHAPE, dropout_p=0.1, seed=42, microbatch=i + 1)
+        st = spl.SeqparStack(ci, t, L, "none" if m else "selective", dtype="f32", check_finite=False)
+        st.layers[0].init_params(3)
+        yi = st.forward(x[i])
+        dxi = st.backward(dy[i])
+        torch.cuda.synchronize()
+        for r in range(t):
+            assert torch.equal(yi[r], y[i][r]) and torch.equal(dxi[r], dx[i][r])
+        gi = st.layers[0].grads().astype(np.float32)
+        acc = gi if acc is None else (acc + gi).astype(np.float32)
+        st.close()
+    np.testing.assert_array_equal(got.astype(np.float32), acc)
+    w.close()
