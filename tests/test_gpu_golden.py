@@ -30,6 +30,11 @@ def grads_close(got_packed, case, orc, tol):
     for name, w in want.items():
         w = w.astype(np.float64)
         err = np.linalg.norm(got[name] - w)
+        if np.linalg.norm(w) <= 1e-12 * rms * np.sqrt(w.size):
+            # exactly zero in exact arithmetic (the key bias: softmax is shift-invariant), so
+            # only the rounding of the GPU's column sum is left: compare on the layer's scale
+            assert err <= tol * rms * np.sqrt(w.size), (name, err)
+            continue
         assert err <= tol * (np.linalg.norm(w) + 0.03 * rms * np.sqrt(w.size)), (name, err)
 
 
