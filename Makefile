@@ -29,11 +29,11 @@ $(PKG)/libspl.so: $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) $(NCCL_LINK)
 
 build/test_facade: tests/cpp/test_facade.cpp include/spl_seqpar.hpp include/spl.h $(PKG)/libspl.so
-	g++ -std=c++17 -O2 -Wall -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -lspl \
+	g++ -std=c++20 -O2 -Wall -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -lspl \
 	    -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
 
 build/test_window_facade: tests/cpp/test_window_facade.cpp include/spl_pipeline.hpp include/spl.h $(PKG)/libspl.so
-	g++ -std=c++17 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -lspl -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+	g++ -std=c++20 -O2 -Wall -Iinclude -o $@ $< -L$(PKG) -lspl -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 oracle:
 	$(MAKE) -C oracle

@@ -43,7 +43,8 @@ enum {
 
 /* RecomputeKind order of config.hpp:51 (None, Full, Selective). */
 enum { SPL_RECOMPUTE_NONE = 0, SPL_RECOMPUTE_FULL = 1, SPL_RECOMPUTE_SELECTIVE = 2 };
-enum { SPL_DTYPE_F32 = 0, SPL_DTYPE_BF16 = 1 };
+enum { SPL_DTYPE_F32 = 0, SPL_DTYPE_BF16 = 1,
+       SPL_DTYPE_F64 = 2 /* collectives only (the reference's own fp64 tensors) */ };
 
 /* BlockConfig (block.hpp:28-42) + RecomputeStrategy (config.hpp:53-70) + ByteConvention
  * (config.hpp:74-80) + execution dtype. */
@@ -78,6 +79,21 @@ int spl_create(const spl_layer_desc* d, const int* devices, int t, spl_handle** 
 int spl_nccl_unique_id(unsigned char id_out[128]);
 int spl_create_nccl(const spl_layer_desc* d, int device, int t, int rank,
                     const unsigned char nccl_id[128], spl_handle** out);
+/* One rank of a t-way group whose collectives run over CUDA-IPC-mapped peer memory instead of
+ * NCCL (P2P loads/stores over NVLink between GPUs; the same path lets several processes share
+ * one GPU). Two phases: spl_ipc_open allocates this rank's exported exchange region and returns
+ * its 64-byte IPC handle; the caller all-gathers the t handles (rank order, any host transport)
+ * and passes them to spl_create_ipc, which maps the peers and consumes the spl_ipc (also on
+ * failure; spl_ipc_close frees one that is never used). Collectives are sequenced by a device
+ * barrier of system-scope release/acquire flags; a peer that does not arrive within 20 s traps
+ * the kernel (the call fails, the GPU does not hang). Results are bit-identical to
+ * spl_create_local with the same t (rank-ordered fp32 sums). */
+typedef struct spl_ipc spl_ipc;
+int spl_ipc_open(const spl_layer_desc* d, int device, int t, int rank, spl_ipc** out,
+                 unsigned char handle_out[64]);
+int spl_create_ipc(const spl_layer_desc* d, spl_ipc* ipc, const unsigned char* handles,
+                   spl_handle** out);
+int spl_ipc_close(spl_ipc* ipc);
 int spl_destroy(spl_handle* h);
 int spl_local_ranks(const spl_handle* h);
 const char* spl_last_error(void);
@@ -151,6 +167,36 @@ int spl_saved_bytes(spl_handle* h, int local_rank, int64_t* ledger_bytes,
  * re-run of full recomputation). counters[tag*4 + {0 AG, 1 RS, 2 AR, 3 ring_elements}]. */
 int spl_comm_log(spl_handle* h, int64_t counters[16]);
 int spl_comm_log_reset(spl_handle* h);
+
+/* ---- Free-standing reference functions on device buffers (no handle).
+ *
+ * attention_interior(q, k, cfg, head_offset, local_heads) (block.hpp:100-101,
+ * block.cpp:381-417): q, k {s, b, local_heads·hd} in the desc dtype (f32 or bf16; the desc's
+ * recompute / SP fields are ignored); outputs {local_heads, b, s, s}: softmax_out and
+ * dropout_out in the desc dtype, dropout_mask as u8 0/1, the mask sliced from the global
+ * {a, b, s, s} mask at head_offset (mask_slice, block.cpp:42-68). Requires heads % local_heads
+ * == 0 and head_offset a multiple of local_heads (SPL_EINVAL otherwise). Asynchronous on
+ * `cuda_stream` (NULL: legacy default stream). */
+int spl_attention_interior_qk(const spl_layer_desc* d, int device, const void* q, const void* k,
+                              int64_t head_offset, int64_t local_heads, void* softmax_out,
+                              uint8_t* dropout_mask, void* dropout_out, void* cuda_stream);
+/* all_gather / reduce_scatter / all_reduce(span<const Tensor>, axis, CommLog*, CommTag)
+ * (collectives.hpp:57-62, collectives.cpp:21-73) over t simulated rank buffers on the current
+ * device: `shards[r]` / `partials[r]` are device pointers of one common `shape` (ndim dims),
+ * dtype SPL_DTYPE_F64 / F32 / BF16. Reductions sum in rank order 0..t-1 (fp64: bit-identical to
+ * the reference's ordered_sum; bf16: fp32 accumulation, one rounding). all_gather writes the
+ * concatenation along `axis`; reduce_scatter writes piece r of the sum along `axis` to out[r]
+ * (SPL_EINVAL "split axis not divisible by part count" when shape[axis] % t != 0).
+ * `log` (optional, 12 int64 = CommLog schedule/regather/grad_sync × {AG, RS, AR,
+ * ring_elements}) is incremented under `tag` (0/1/2) with the ring model of
+ * collectives.cpp:30-38. t <= 64. Asynchronous on `cuda_stream`. */
+int spl_all_gather(const void* const* shards, int t, const int64_t* shape, int ndim, int axis,
+                   int dtype, void* out, int64_t log[12], int tag, void* cuda_stream);
+int spl_reduce_scatter(const void* const* partials, int t, const int64_t* shape, int ndim,
+                       int axis, int dtype, void* const* out, int64_t log[12], int tag,
+                       void* cuda_stream);
+int spl_all_reduce(const void* const* partials, int t, const int64_t* shape, int ndim, int dtype,
+                   void* out, int64_t log[12], int tag, void* cuda_stream);
 
 /* Activation-memory accountant: per_layer_bytes / _exact (activation_memory.cpp:54-82),
  * kind = SPL_RECOMPUTE_*. Floor-once exact arithmetic. */

@@ -13,6 +13,7 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "spl.h")
 SPL_OK, SPL_EINVAL, SPL_EDOMAIN, SPL_ECUDA, SPL_ENCCL, SPL_ESTATE, SPL_EBUDGET = range(7)
 RECOMPUTE = {"none": 0, "full": 1, "selective": 2}
 DTYPE = {"f32": 0, "fp32": 0, "float32": 0, "bf16": 1, "bfloat16": 1}
+DTYPE_F64 = 2  # collectives only
 KCLASS = ["gemm", "attention", "elementwise", "collective", "other"]
 
 
@@ -67,6 +68,9 @@ def lib():
         "spl_create": (I32, [P(LayerDesc), P(I32), I32, P(H)]),
         "spl_nccl_unique_id": (I32, [C.c_char_p]),
         "spl_create_nccl": (I32, [P(LayerDesc), I32, I32, I32, C.c_char_p, P(H)]),
+        "spl_ipc_open": (I32, [P(LayerDesc), I32, I32, I32, P(H), C.c_char_p]),
+        "spl_create_ipc": (I32, [P(LayerDesc), H, C.c_char_p, P(H)]),
+        "spl_ipc_close": (I32, [H]),
         "spl_destroy": (I32, [H]),
         "spl_local_ranks": (I32, [H]),
         "spl_last_error": (C.c_char_p, []),
@@ -120,6 +124,10 @@ def lib():
         "spl_window_set_stream": (I32, [H, VP]),
         "spl_window_run": (I32, [H, P(VP), P(VP), P(VP), P(VP)]),
         "spl_window_memory": (I32, [H, P(I64)]),
+        "spl_attention_interior_qk": (I32, [P(LayerDesc), I32, VP, VP, I64, I64, VP, VP, VP, VP]),
+        "spl_all_gather": (I32, [P(VP), I32, P(I64), I32, I32, I32, VP, P(I64), I32, VP]),
+        "spl_reduce_scatter": (I32, [P(VP), I32, P(I64), I32, I32, I32, P(VP), P(I64), I32, VP]),
+        "spl_all_reduce": (I32, [P(VP), I32, P(I64), I32, I32, VP, P(I64), I32, VP]),
         "spl_gemm_bf16": (I32, [I64, I64, I64, VP, I64, I32, VP, I64, I32, VP, I64, I32, VP, VP,
                                 VP, I64, VP, P(I32)]),
     }

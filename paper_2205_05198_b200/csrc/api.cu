@@ -15,28 +15,14 @@ struct spl_handle {
   int device = 0;
 };
 
-namespace {
-thread_local std::string g_err;
+namespace spl {
+thread_local std::string g_last_error;
+}
 
+namespace {
 template <typename F>
 int guard(F&& f) {
-  try {
-    f();
-    g_err.clear();
-    return SPL_OK;
-  } catch (const spl::Error& e) {
-    g_err = e.what();
-    return e.code;
-  } catch (const std::invalid_argument& e) {
-    g_err = e.what();
-    return SPL_EINVAL;
-  } catch (const std::domain_error& e) {
-    g_err = e.what();
-    return SPL_EDOMAIN;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return SPL_ECUDA;
-  }
+  return spl::c_guard(std::forward<F>(f));
 }
 
 void check_handle(const spl_handle* h) {
@@ -116,7 +102,7 @@ int64_t fit64(__int128 v) {
 
 extern "C" {
 
-const char* spl_last_error(void) { return g_err.c_str(); }
+const char* spl_last_error(void) { return spl::g_last_error.c_str(); }
 
 void spl_desc_default(spl_layer_desc* d) {
   std::memset(d, 0, sizeof(*d));
@@ -165,6 +151,60 @@ int spl_create_nccl(const spl_layer_desc* d, int device, int t, int rank,
     SPL_CUDA(cudaSetDevice(device));
     *out = make_handle(d, device, spl::make_nccl_comm(t, rank, nccl_id));
   });
+}
+
+struct spl_ipc {
+  std::unique_ptr<spl::IpcRank> rank;
+  spl_layer_desc desc;
+  int device = 0, t = 1;
+};
+
+int spl_ipc_open(const spl_layer_desc* d, int device, int t, int rank, spl_ipc** out,
+                 unsigned char handle_out[64]) {
+  return guard([&] {
+    spl::require(d != nullptr && out != nullptr && handle_out != nullptr, "null argument");
+    spl::require(t >= 1 && rank >= 0 && rank < t, "IPC rank out of range");
+    spl::require(d->seq % t == 0 && d->hidden % t == 0 && d->heads % t == 0,
+                 "s, h and the head count must be divisible by t");
+    // the largest payload of one collective: a sequence shard (g, ḡ and their duals), the
+    // whole activation without SP (f̄ all-reduce), the fp32 replicated-parameter gradients
+    const size_t es = d->dtype == SPL_DTYPE_F32 ? 4 : 2;
+    const size_t rows = (size_t)(d->seq * d->batch) / (d->sequence_parallel ? (size_t)t : 1);
+    const size_t slot = std::max(rows * (size_t)d->hidden * es, (size_t)(6 * d->hidden) * 4);
+    auto* o = new spl_ipc();
+    try {
+      o->rank = spl::ipc_open(device, t, rank, slot);
+      o->rank->export_handle(handle_out);
+    } catch (...) {
+      delete o;
+      throw;
+    }
+    o->desc = *d;
+    o->device = device;
+    o->t = t;
+    *out = o;
+  });
+}
+
+int spl_create_ipc(const spl_layer_desc* d, spl_ipc* ipc, const unsigned char* handles,
+                   spl_handle** out) {
+  std::unique_ptr<spl_ipc> own(ipc);  // consumed whatever happens
+  return guard([&] {
+    spl::require(d != nullptr && own != nullptr && handles != nullptr && out != nullptr,
+                 "null argument");
+    spl::require(d->seq == own->desc.seq && d->batch == own->desc.batch &&
+                     d->hidden == own->desc.hidden && d->dtype == own->desc.dtype &&
+                     d->sequence_parallel == own->desc.sequence_parallel,
+                 "desc differs from the one the IPC rank was opened with");
+    SPL_CUDA(cudaSetDevice(own->device));
+    auto comm = spl::ipc_connect(std::move(own->rank), handles);
+    *out = make_handle(d, own->device, std::move(comm));
+  });
+}
+
+int spl_ipc_close(spl_ipc* ipc) {
+  delete ipc;
+  return SPL_OK;
 }
 
 int spl_destroy(spl_handle* h) {

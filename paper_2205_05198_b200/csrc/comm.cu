@@ -28,6 +28,126 @@ inline int grid_for(int64_t n) {
   return (int)(g < 1 ? 1 : g);
 }
 
+// ---------------------------------------------------------------- peer-memory protocol kernels
+__device__ __forceinline__ uint32_t ld_acq_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// A wait that gives up after 20 s (a peer that never arrives): it records the failure in
+// err[0] and traps, so the rank's next synchronisation fails loudly instead of the GPU hanging.
+__device__ __forceinline__ void spin_until_ge(const uint32_t* p, uint32_t target, int* err) {
+  const uint64_t t0 = gtimer();
+  while ((int32_t)(ld_acq_sys(p) - target) < 0) {
+    __nanosleep(256);
+    if (gtimer() - t0 > 20000000000ull) {
+      atomicExch(err, 1);
+      __trap();
+    }
+  }
+}
+
+struct PeerPtrs {
+  void* p[kMaxLocal];
+};
+
+// Fused reduce-scatter back-pressure: source `src` may overwrite its slot in destination q only
+// after q consumed the previous landing, i.e. q's generation reached src's arrivals at q.
+__global__ void p2p_ready_k(PeerPtrs gen, PeerPtrs arrivals, int n, int* err) {
+  const int q = threadIdx.x;
+  if (q < n) {
+    const uint32_t target = ld_acq_sys(static_cast<const uint32_t*>(arrivals.p[q]));
+    spin_until_ge(static_cast<const uint32_t*>(gen.p[q]), target, err);
+  }
+}
+
+// Barrier of an IPC group: generation g = ++ctrl[kGen]; write g into every rank's arrival slot
+// for this rank (release, system scope); wait until every rank's arrival here reached g.
+constexpr int kArrive = 0, kGen = 64, kRsFlags = 128, kRsGen = 192, kErr = 224, kCtrlWords = 256;
+__global__ void ipc_barrier_k(PeerPtrs ctrl, int t, int rank) {
+  uint32_t* mine = static_cast<uint32_t*>(ctrl.p[rank]);
+  int* err = reinterpret_cast<int*>(mine + kErr);
+  __shared__ uint32_t g;
+  if (threadIdx.x == 0) {
+    g = mine[kGen] + 1u;
+    mine[kGen] = g;
+    __threadfence_system();  // this rank's pushes (previous kernels) before the arrival flags
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < t) st_rel_sys(static_cast<uint32_t*>(ctrl.p[threadIdx.x]) + kArrive + rank, g);
+  if ((int)threadIdx.x < t) spin_until_ge(mine + kArrive + threadIdx.x, g, err);
+  __syncthreads();
+}
+
+// push: dst[q] + off_bytes(q) <- src + src_off(q), `bytes` each, q = 0..t-1. The inbox parity
+// is the current barrier generation's (read on the device, so graph replays stay in step).
+struct PushArgs {
+  const char* src;
+  int64_t src_stride;  // bytes between the pieces sent to consecutive ranks (0: same piece)
+  char* dst[kMaxLocal];
+  int64_t dst_off;     // offset of this rank's slot inside a parity half
+  int64_t parity_bytes;
+  const uint32_t* gen;
+  int64_t bytes;
+  int t;
+};
+__global__ void ipc_push_k(PushArgs a) {
+  const int64_t par = (int64_t)(*a.gen & 1u) * a.parity_bytes;
+  const bool v16 = (a.bytes % 16) == 0 && (a.src_stride % 16) == 0 && (a.dst_off % 16) == 0 &&
+                   ((uintptr_t)a.src % 16) == 0;
+  const int q = blockIdx.y;
+  const char* s = a.src + q * a.src_stride;
+  char* d = a.dst[q] + par + a.dst_off;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (v16) {
+    const int64_t nv = a.bytes / 16;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride)
+      reinterpret_cast<uint4*>(d)[i] = reinterpret_cast<const uint4*>(s)[i];
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.bytes; i += stride) d[i] = s[i];
+  }
+  __threadfence_system();
+}
+
+// gather: out[q*bytes ..] <- own inbox slot q of the previous generation's parity
+__global__ void ipc_collect_k(const char* inbox, int64_t parity_bytes, int64_t slot_bytes,
+                              const uint32_t* gen, char* out, int64_t bytes, int t) {
+  const int64_t par = (int64_t)((*gen - 1u) & 1u) * parity_bytes;
+  const int q = blockIdx.y;
+  const char* s = inbox + par + q * slot_bytes;
+  char* d = out + q * bytes;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (bytes % 16 == 0) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < bytes / 16; i += stride)
+      reinterpret_cast<uint4*>(d)[i] = reinterpret_cast<const uint4*>(s)[i];
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < bytes; i += stride) d[i] = s[i];
+  }
+}
+
+// out[i] = rank-ordered fp32 sum of the t inbox slots (as rs_local_k), rounded to T
+template <typename T>
+__global__ void ipc_sum_k(const char* inbox, int64_t parity_bytes, int64_t slot_bytes,
+                          const uint32_t* gen, int t, int64_t n, T* out) {
+  const int64_t par = (int64_t)((*gen - 1u) & 1u) * parity_bytes;
+  const T* base = reinterpret_cast<const T*>(inbox + par);
+  const int64_t se = slot_bytes / (int64_t)sizeof(T);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = to_f(base[i]);
+    for (int r = 1; r < t; ++r) acc += to_f(base[r * se + i]);
+    out[i] = from_f<T>(acc);
+  }
+}
+
 class LocalComm final : public Comm {
  public:
   explicit LocalComm(int t) {
@@ -173,6 +293,7 @@ class NcclComm final : public Comm {
       }
     if (slots_) cudaFree(slots_);
     if (flags_) cudaFree(flags_);
+    if (err_) cudaFree(err_);
     if (comm_) ncclCommDestroy(comm_);
   }
 
@@ -228,6 +349,16 @@ class NcclComm final : public Comm {
     (void)dst;
     return static_cast<uint32_t*>(flags_) + t_;
   }
+  void p2p_ready_wait(int src, cudaStream_t st) override {
+    PeerPtrs g{}, a{};
+    for (int q = 0; q < t_; ++q) {
+      g.p[q] = static_cast<uint32_t*>(peer_flags_[q]) + t_;
+      a.p[q] = static_cast<uint32_t*>(peer_flags_[q]) + src;
+    }
+    if (err_ == nullptr) SPL_CUDA(cudaMalloc(&err_, sizeof(int)));
+    p2p_ready_k<<<1, 32, 0, st>>>(g, a, t_, err_);
+    SPL_CHECK_LAUNCH();
+  }
   void all_gather(const void* const* shard, void* const* full, int64_t n, DType dt,
                   cudaStream_t st) override {
     SPL_NCCL(ncclAllGather(shard[0], full[0], (size_t)n, nccl_type(dt), comm_, st));
@@ -245,17 +376,184 @@ class NcclComm final : public Comm {
 
  private:
   ncclComm_t comm_ = nullptr;
+  int* err_ = nullptr;
   void* slots_ = nullptr;
   void* flags_ = nullptr;
   size_t slot_bytes_ = 0;
   std::vector<void*> peer_slots_, peer_flags_;
 };
 
+
+// ---------------------------------------------------------------- CUDA-IPC transport
+// Region of one rank (one cudaMalloc, exported with one IPC handle):
+//   [ctrl: 256 u32 — arrivals[64], generation, fused-RS counters[64], fused-RS generation, err]
+//   [inbox: 2 parities × t slots × slot_bytes]  (pushed collectives)
+//   [fused-RS landing slots: t × slot_bytes]
+class IpcRankImpl final : public IpcRank {
+ public:
+  IpcRankImpl(int device, int t, int rank, size_t slot_bytes)
+      : device_(device), t_(t), rank_(rank), slot_(round16(slot_bytes)) {
+    require(t >= 1 && t <= kMaxLocal, "IPC group must have 1..16 ranks");
+    require(rank >= 0 && rank < t, "IPC rank out of range");
+    SPL_CUDA(cudaSetDevice(device));
+    bytes_ = ctrl_bytes() + 2 * (size_t)t * slot_ + (size_t)t * slot_;
+    SPL_CUDA(cudaMalloc(&base_, bytes_));
+    SPL_CUDA(cudaMemset(base_, 0, ctrl_bytes()));
+    SPL_CUDA(cudaIpcGetMemHandle(&handle_, base_));
+  }
+  ~IpcRankImpl() override {
+    if (base_) {
+      cudaSetDevice(device_);
+      cudaFree(base_);
+    }
+  }
+  void export_handle(unsigned char out[kHandleBytes]) const override {
+    static_assert(sizeof(cudaIpcMemHandle_t) == kHandleBytes, "IPC handle size");
+    std::memcpy(out, &handle_, kHandleBytes);
+  }
+  static size_t round16(size_t b) { return (b + 15) / 16 * 16; }
+  static size_t ctrl_bytes() { return 4096; }
+
+  int device_, t_, rank_;
+  size_t slot_, bytes_ = 0;
+  void* base_ = nullptr;
+  cudaIpcMemHandle_t handle_{};
+};
+
+class IpcComm final : public Comm {
+ public:
+  IpcComm(std::unique_ptr<IpcRankImpl> mine, const unsigned char* handles) : r_(std::move(mine)) {
+    t_ = r_->t_;
+    local_ = 1;
+    rank0_ = r_->rank_;
+    dev_ = r_->device_;
+    SPL_CUDA(cudaSetDevice(dev_));
+    base_.assign(t_, nullptr);
+    for (int q = 0; q < t_; ++q) {
+      if (q == rank0_) {
+        base_[q] = static_cast<char*>(r_->base_);
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles + (size_t)q * IpcRank::kHandleBytes, IpcRank::kHandleBytes);
+      void* p = nullptr;
+      SPL_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      base_[q] = static_cast<char*>(p);
+    }
+  }
+  ~IpcComm() override {
+    cudaSetDevice(dev_);
+    cudaDeviceSynchronize();
+    for (int q = 0; q < t_; ++q)
+      if (q != rank0_ && base_[q]) cudaIpcCloseMemHandle(base_[q]);
+  }
+  bool serial_order() const override { return true; }
+  bool p2p_default() const override { return true; }
+
+  void all_gather(const void* const* shard, void* const* full, int64_t n, DType dt,
+                  cudaStream_t st) override {
+    const int64_t bytes = n * (int64_t)dsize(dt);
+    push(static_cast<const char*>(shard[0]), 0, bytes, st);
+    barrier(st);
+    ipc_collect_k<<<dim3(grid_for(bytes / 16 + 1), t_), 256, 0, st>>>(
+        inbox(rank0_), parity_bytes(), (int64_t)r_->slot_, gen(), static_cast<char*>(full[0]),
+        bytes, t_);
+    SPL_CHECK_LAUNCH();
+  }
+  void reduce_scatter(const void* const* part, void* const* shard, int64_t n, DType dt,
+                      cudaStream_t st) override {
+    const int64_t bytes = n * (int64_t)dsize(dt);
+    push(static_cast<const char*>(part[0]), bytes, bytes, st);  // piece q to rank q
+    barrier(st);
+    sum(shard[0], n, dt, st);
+  }
+  void all_reduce(void* const* buf, int64_t n, DType dt, cudaStream_t st) override {
+    const int64_t bytes = n * (int64_t)dsize(dt);
+    push(static_cast<const char*>(buf[0]), 0, bytes, st);
+    barrier(st);
+    sum(buf[0], n, dt, st);
+  }
+  void all_reduce_f32(float* const* buf, int64_t n, cudaStream_t st) override {
+    all_reduce(reinterpret_cast<void* const*>(buf), n, DType::F32, st);
+  }
+
+  // fused reduce-scatter landing slots (the region's last t slots) and their counters
+  bool p2p_setup(size_t slot_bytes) override { return slot_bytes <= r_->slot_; }
+  void* p2p_slot(int dst, int src) override {
+    return base_[dst] + rs_off() + (size_t)src * r_->slot_;
+  }
+  uint32_t* p2p_flag(int dst, int src) override { return ctrl(dst) + kRsFlags + src; }
+  const void* p2p_slot_local(int dst, int src) override {
+    (void)dst;
+    return base_[rank0_] + rs_off() + (size_t)src * r_->slot_;
+  }
+  uint32_t* p2p_flags_local(int dst) override { (void)dst; return ctrl(rank0_) + kRsFlags; }
+  uint32_t* p2p_gen(int dst) override { (void)dst; return ctrl(rank0_) + kRsGen; }
+  void p2p_ready_wait(int src, cudaStream_t st) override {
+    PeerPtrs g{}, a{};
+    for (int q = 0; q < t_; ++q) {
+      g.p[q] = ctrl(q) + kRsGen;
+      a.p[q] = ctrl(q) + kRsFlags + src;
+    }
+    p2p_ready_k<<<1, 32, 0, st>>>(g, a, t_, reinterpret_cast<int*>(ctrl(rank0_) + kErr));
+    SPL_CHECK_LAUNCH();
+  }
+
+ private:
+  uint32_t* ctrl(int q) const { return reinterpret_cast<uint32_t*>(base_[q]); }
+  const uint32_t* gen() const { return ctrl(rank0_) + kGen; }
+  char* inbox(int q) const { return base_[q] + IpcRankImpl::ctrl_bytes(); }
+  int64_t parity_bytes() const { return (int64_t)t_ * (int64_t)r_->slot_; }
+  size_t rs_off() const { return IpcRankImpl::ctrl_bytes() + 2 * (size_t)t_ * r_->slot_; }
+
+  // every rank q receives src + q*src_stride (bytes) in its inbox slot for this rank
+  void push(const char* src, int64_t src_stride, int64_t bytes, cudaStream_t st) {
+    require(bytes <= (int64_t)r_->slot_, "IPC collective larger than the exchange slot");
+    PushArgs a{};
+    a.src = src;
+    a.src_stride = src_stride;
+    for (int q = 0; q < t_; ++q) a.dst[q] = inbox(q);
+    a.dst_off = (int64_t)rank0_ * (int64_t)r_->slot_;
+    a.parity_bytes = parity_bytes();
+    a.gen = gen();
+    a.bytes = bytes;
+    a.t = t_;
+    ipc_push_k<<<dim3(grid_for(bytes / 16 + 1), t_), 256, 0, st>>>(a);
+    SPL_CHECK_LAUNCH();
+  }
+  void barrier(cudaStream_t st) {
+    PeerPtrs c{};
+    for (int q = 0; q < t_; ++q) c.p[q] = base_[q];
+    ipc_barrier_k<<<1, 32, 0, st>>>(c, t_, rank0_);
+    SPL_CHECK_LAUNCH();
+  }
+  void sum(void* out, int64_t n, DType dt, cudaStream_t st) {
+    if (dt == DType::F32)
+      ipc_sum_k<float><<<grid_for(n), 256, 0, st>>>(inbox(rank0_), parity_bytes(), (int64_t)r_->slot_,
+                                                    gen(), t_, n, static_cast<float*>(out));
+    else
+      ipc_sum_k<bf16><<<grid_for(n), 256, 0, st>>>(inbox(rank0_), parity_bytes(), (int64_t)r_->slot_,
+                                                   gen(), t_, n, static_cast<bf16*>(out));
+    SPL_CHECK_LAUNCH();
+  }
+
+  std::unique_ptr<IpcRankImpl> r_;
+  std::vector<char*> base_;
+  int dev_ = 0;
+};
 }  // namespace
 
 std::unique_ptr<Comm> make_local_comm(int t) { return std::make_unique<LocalComm>(t); }
 std::unique_ptr<Comm> make_nccl_comm(int t, int rank, const unsigned char id[128]) {
   return std::make_unique<NcclComm>(t, rank, id);
+}
+std::unique_ptr<IpcRank> ipc_open(int device, int t, int rank, size_t slot_bytes) {
+  return std::make_unique<IpcRankImpl>(device, t, rank, slot_bytes);
+}
+std::unique_ptr<Comm> ipc_connect(std::unique_ptr<IpcRank> r, const unsigned char* handles) {
+  require(r != nullptr && handles != nullptr, "null IPC rank or handles");
+  std::unique_ptr<IpcRankImpl> impl(static_cast<IpcRankImpl*>(r.release()));
+  return std::make_unique<IpcComm>(std::move(impl), handles);
 }
 
 }  // namespace spl

@@ -57,6 +57,15 @@ class Comm {
   virtual const void* p2p_slot_local(int dst, int src) { (void)dst; (void)src; return nullptr; }
   virtual uint32_t* p2p_flags_local(int dst) { (void)dst; return nullptr; }
   virtual uint32_t* p2p_gen(int dst) { (void)dst; return nullptr; }
+  // Back-pressure of the fused reduce-scatter: before source `src` overwrites its slots in the
+  // destination ranks, wait (on `st`) until every destination consumed the previous landing
+  // (its generation caught up with src's arrival count there).
+  virtual void p2p_ready_wait(int src, cudaStream_t st) { (void)src; (void)st; }
+  // Whether the fused reduce-scatter is on by default for this transport.
+  virtual bool p2p_default() const { return local_ == t_; }
+  // Whether collectives must be issued on one stream in one order on every rank (device-side
+  // sequence-numbered protocols); the layer then keeps them all on its compute stream.
+  virtual bool serial_order() const { return false; }
 
   void log(CommTag tag, int kind, int64_t logical_elems) {
     CommCounters& c = counters[tag];
@@ -73,5 +82,19 @@ class Comm {
 
 std::unique_ptr<Comm> make_local_comm(int t);
 std::unique_ptr<Comm> make_nccl_comm(int t, int rank, const unsigned char id[128]);
+
+// One rank of a t-way group whose collectives run over CUDA-IPC-mapped peer memory (NVLink P2P
+// loads/stores between GPUs; same-device IPC when several processes share one GPU), with no
+// NCCL: a device-side barrier of system-scope release/acquire flags sequences them. Two-phase
+// setup: open() allocates this rank's exported region and returns its IPC handle; after the
+// caller exchanged the t handles (rank order), connect() maps the peers.
+class IpcRank {
+ public:
+  static constexpr int kHandleBytes = 64;
+  virtual ~IpcRank() = default;
+  virtual void export_handle(unsigned char out[kHandleBytes]) const = 0;
+};
+std::unique_ptr<IpcRank> ipc_open(int device, int t, int rank, size_t slot_bytes);
+std::unique_ptr<Comm> ipc_connect(std::unique_ptr<IpcRank> r, const unsigned char* handles);
 
 }  // namespace spl

@@ -47,4 +47,31 @@ enum KClass : int { K_GEMM = 0, K_ATTN = 1, K_ELEM = 2, K_COMM = 3, K_OTHER = 4,
 
 constexpr int kNumSMs = 148;
 
+// Message of the last failing C-ABI call on this thread (spl_last_error); defined in api.cu.
+extern thread_local std::string g_last_error;
+
+// Runs an extern "C" entry point body, mapping exceptions to the status codes of spl.h:
+// spl::Error -> its code, std::invalid_argument -> SPL_EINVAL (1), std::domain_error ->
+// SPL_EDOMAIN (2), anything else -> SPL_ECUDA (3).
+template <typename F>
+int c_guard(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return 0;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return 1;
+  } catch (const std::domain_error& e) {
+    g_last_error = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return 3;
+  }
+}
+
 }  // namespace spl

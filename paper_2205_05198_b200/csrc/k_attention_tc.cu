@@ -901,8 +901,12 @@ void attn_keep_bits(const AttnArgs& a, cudaStream_t st) {
     return !(e != nullptr && e[0] == '0');
   }();
   auto kern = tie ? keep_bits_k<true> : keep_bits_k<false>;
+  // causal: words above the diagonal are skipped (their probabilities are 0), except when the
+  // interior is materialised — the stored mask carries the raw keep bit at every position,
+  // masked or not (mask_slice, block.cpp:392-394)
+  const int causal_skip = a.causal && a.sm == nullptr;
   kern<<<(unsigned)grid, 1024, 0, st>>>(a.drop, a.head_offset, (int)a.lh, (int)a.b, (int)a.s, W,
-                                        a.causal, a.keepbits, ShiftMuls{4u, 32u, 2u, 1u});
+                                        causal_skip, a.keepbits, ShiftMuls{4u, 32u, 2u, 1u});
   SPL_CHECK_LAUNCH();
 }
 

@@ -40,6 +40,7 @@ struct Graph {
   std::vector<const void*> in;
   std::vector<void*> out;
   int64_t launches = 0;
+  CommCounters comm[4];  // the CommLog increments the captured body makes, replayed per launch
 };
 
 template <typename T>
@@ -85,11 +86,10 @@ class Layer final : public LayerBase {
     }
     // The keep-bit RNG pass runs on the main stream by default: overlapping it with the GEMMs
     // on a side stream measured no faster (the GEMMs already hold the chip at its power cap).
-    {  // reduce-scatter fused into the row-parallel GEMMs: on for simulated ranks; NCCL ranks
-       // opt in with SPL_FUSED_RS=1 (CUDA IPC peer slots over NVLink) until measured on a node
+    {  // reduce-scatter fused into the row-parallel GEMMs: on for simulated ranks and the
+       // CUDA-IPC transport; NCCL ranks opt in with SPL_FUSED_RS=1 (IPC peer slots over NVLink)
       const char* f = std::getenv("SPL_FUSED_RS");
-      const bool local = comm_->local() == t_;
-      const bool want = f != nullptr ? f[0] == '1' : local;
+      const bool want = f != nullptr ? f[0] == '1' : comm_->p2p_default();
       if (want && std::is_same_v<T, bf16> && sp_ && t_ > 1 && t_ <= k::kMaxScatterRanks &&
           h_ % 8 == 0)
         fused_rs_ = comm_->p2p_setup((size_t)(RL_ * h_) * sizeof(T));
@@ -105,7 +105,8 @@ class Layer final : public LayerBase {
     const char* e = std::getenv("SPL_KEEPBITS_SIDE");
     bits_serial_ = !(e != nullptr && e[0] == '1');
     const char* c = std::getenv("SPL_SERIAL_COMM");
-    comm_serial_ = c != nullptr && c[0] == '1';
+    // transports whose collectives are sequenced on the device need one issue order per rank
+    comm_serial_ = (c != nullptr && c[0] == '1') || comm_->serial_order();
   }
 
   ~Layer() override {
@@ -158,33 +159,54 @@ class Layer final : public LayerBase {
       if (c.exec != nullptr && c.in == in && c.out == out) gp = &c;
     if (gp == nullptr) {
       if (set.size() >= kMaxGraphs) {
-        SPL_CUDA(cudaGraphExecDestroy(set.front().exec));
+        if (set.front().exec != nullptr) SPL_CUDA(cudaGraphExecDestroy(set.front().exec));
         set.erase(set.begin());
       }
-      set.emplace_back();
-      gp = &set.back();
-    }
-    Graph& g = *gp;
-    if (g.exec == nullptr) {
+      Graph g;
       const int64_t l0 = launches_;
-      cudaGraph_t graph;
+      CommCounters c0[4];
+      std::copy(comm_->counters, comm_->counters + 4, c0);
+      cudaGraph_t graph = nullptr;
       SPL_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
       try {
         body();
       } catch (...) {
-        cudaStreamEndCapture(st_, &graph);
+        cudaStreamEndCapture(st_, &graph);  // end the capture, drop the partial graph
+        if (graph != nullptr) cudaGraphDestroy(graph);
+        launches_ = l0;
+        std::copy(c0, c0 + 4, comm_->counters);
         throw;
       }
       SPL_CUDA(cudaStreamEndCapture(st_, &graph));
-      SPL_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
-      SPL_CUDA(cudaGraphDestroy(graph));
+      const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      SPL_CUDA(ie);
       g.in = in;
       g.out = out;
       g.launches = launches_ - l0;
       launches_ = l0;
+      for (int k = 0; k < 4; ++k) {  // the capture's CommLog increments, applied per launch
+        CommCounters& d = g.comm[k];
+        const CommCounters& a = comm_->counters[k];
+        d.all_gathers = a.all_gathers - c0[k].all_gathers;
+        d.reduce_scatters = a.reduce_scatters - c0[k].reduce_scatters;
+        d.all_reduces = a.all_reduces - c0[k].all_reduces;
+        d.ring_elements = a.ring_elements - c0[k].ring_elements;
+        comm_->counters[k] = c0[k];
+      }
+      set.push_back(std::move(g));
+      gp = &set.back();
     }
+    Graph& g = *gp;
     SPL_CUDA(cudaGraphLaunch(g.exec, st_));
     launches_ += g.launches;
+    for (int k = 0; k < 4; ++k) {
+      CommCounters& c = comm_->counters[k];
+      c.all_gathers += g.comm[k].all_gathers;
+      c.reduce_scatters += g.comm[k].reduce_scatters;
+      c.all_reduces += g.comm[k].all_reduces;
+      c.ring_elements += g.comm[k].ring_elements;
+    }
   }
 
   // fork: our stream waits for the caller's prior work; join: the caller waits for ours.
@@ -894,6 +916,10 @@ class Layer final : public LayerBase {
     g.bias = bias; g.C2 = C2; g.aux = aux; g.ldaux = ldaux;
     g.accumulate = epi == Epi::F32 && grad_acc_;
     if (scatter_rank >= 0) {  // the reduce-scatter fused into this row-parallel GEMM
+      // back-pressure: the destinations consumed this source's previous landing (peer ranks;
+      // simulated ranks are ordered by the one stream)
+      if (comm_->local() != t_)
+        launch(K_COMM, 1, 0, 0, [&] { comm_->p2p_ready_wait(rank0_ + scatter_rank, st_); });
       for (int q = 0; q < t_; ++q) g.scatter[q] = comm_->p2p_slot(q, rank0_ + scatter_rank);
       g.scatter_n = t_;
       g.scatter_rows = RL_;

@@ -79,7 +79,7 @@ class SeqparLayer:
     def __init__(self, cfg: BlockConfig, t: int, recompute: str = "none",
                  sequence_parallel: bool = True, dtype: str = "bf16", device: int = 0,
                  check_finite: bool = True, nccl: tuple[int, bytes] | None = None,
-                 _borrow=None):
+                 _borrow=None, ipc=None):
         self.cfg, self.t, self.recompute, self.sp, self.dtype = cfg, t, recompute, sequence_parallel, dtype
         self.device = device
         self._owned = True
@@ -90,13 +90,22 @@ class SeqparLayer:
             return
         d = _desc(cfg, recompute, sequence_parallel, dtype, check_finite)
         self._h = C.c_void_p()
-        if nccl is None:
+        if ipc is not None:
+            # one rank of a CUDA-IPC group: ipc = (rank, exchange) where exchange(handle_bytes)
+            # returns the t ranks' handles in rank order (any host transport, e.g. gloo)
+            rank, exchange = ipc
+            obj = C.c_void_p()
+            hb = C.create_string_buffer(64)
+            check(lib().spl_ipc_open(C.byref(d), device, t, rank, C.byref(obj), hb))
+            handles = b"".join(exchange(hb.raw[:64]))
+            check(lib().spl_create_ipc(C.byref(d), obj, handles, C.byref(self._h)))
+        elif nccl is None:
             check(lib().spl_create_local(C.byref(d), device, t, C.byref(self._h)))
         else:
             rank, uid = nccl
             check(lib().spl_create_nccl(C.byref(d), device, t, rank, uid, C.byref(self._h)))
         self.local = lib().spl_local_ranks(self._h)
-        self.rank0 = 0 if nccl is None else nccl[0]
+        self.rank0 = nccl[0] if nccl is not None else (ipc[0] if ipc is not None else 0)
 
     # ---- lifecycle
     def close(self):
@@ -271,6 +280,12 @@ class SeqparForward:
     ledgers: list
     comm: dict
     layer: SeqparLayer = field(repr=False)
+    params_digest: bytes = field(default=b"", repr=False)
+
+
+def _digest(params: np.ndarray) -> bytes:
+    import hashlib
+    return hashlib.blake2b(np.ascontiguousarray(params, np.float64).tobytes(), digest_size=16).digest()
 
 
 @dataclass
@@ -306,7 +321,8 @@ def seqpar_block_forward(x_shards: list, params: np.ndarray, t: int, cfg: BlockC
             raise ValueError("input shard must be {s/t, b, h}")
     y = layer.forward([_to_dev(xs, dtype, device) for xs in x_shards])
     ledgers = [layer.ledger(r) for r in range(t)]
-    return SeqparForward(t, cfg, [_to_host(v) for v in y], ledgers, layer.comm_log(), layer)
+    return SeqparForward(t, cfg, [_to_host(v) for v in y], ledgers, layer.comm_log(), layer,
+                         _digest(params))
 
 
 def seqpar_block_backward(dy_shards: list, fwd: SeqparForward, params: np.ndarray) -> SeqparBackward:
@@ -317,10 +333,235 @@ def seqpar_block_backward(dy_shards: list, fwd: SeqparForward, params: np.ndarra
     for d in dy_shards:
         if tuple(d.shape) != layer.shard_shape():
             raise ValueError("dy shard shape mismatch")
+    # the backward GEMMs use `params` (block.cpp:639-640): reload them when they are not the
+    # forward's; full recomputation would also re-run the forward with them, which the
+    # reference never does, so that combination is rejected
+    if fwd.params_digest and _digest(params) != fwd.params_digest:
+        if layer.recompute == "full":
+            raise ValueError("full recomputation re-runs the forward: backward params must be "
+                             "the forward's")
+        layer.load_params(params)
     layer.comm_log_reset()
     dx = layer.backward([_to_dev(d, layer.dtype, layer.device) for d in dy_shards])
     return SeqparBackward([_to_host(v) for v in dx], layer.grads(),
                           [layer.w1_grad_shard(r) for r in range(fwd.t)], layer.comm_log())
+
+
+def seqpar_block_forward_sharded(x: "RankShardedTensor", params: np.ndarray, cfg: BlockConfig,
+                                 **kw) -> SeqparForward:
+    """The RankShardedTensor overload (block.hpp:158-162, block.cpp:604-613)."""
+    if x.axis != "sequence":
+        raise ValueError("layer input must be sharded along the sequence axis")
+    x.check()
+    return seqpar_block_forward(x.shards, params, len(x.shards), cfg, **kw)
+
+
+@dataclass
+class ReferenceForward:
+    """Mirror of ReferenceForward (block.hpp:104-119): the single-rank layer. On the GPU it is
+    the t = 1 layer (the reference's t = 1 seqpar path is bit-identical to it,
+    test_seqpar.cpp:161-168)."""
+    y: np.ndarray
+    ledger: dict
+    cfg: BlockConfig
+    layer: SeqparLayer = field(repr=False)
+    params_digest: bytes = field(default=b"", repr=False)
+
+    def saved(self, name: str) -> np.ndarray:
+        n = self.ledger[name][0]
+        return self.layer.saved(0, name, (n,))
+
+
+@dataclass
+class BlockGrads:
+    """Mirror of BlockGrads (block.hpp:123-126): packed param grads + dx."""
+    params: np.ndarray
+    dx: np.ndarray
+
+
+def reference_block_forward(x: np.ndarray, params: np.ndarray, cfg: BlockConfig,
+                            recompute: str = "none", dtype: str = "f32",
+                            device: int = 0) -> ReferenceForward:
+    """reference_block_forward(x, params, cfg) (block.cpp:419-456) on the GPU."""
+    if tuple(x.shape) != (cfg.seq, cfg.batch, cfg.hidden):
+        raise ValueError("reference_block_forward: input must be {s, b, h}")
+    if cfg.heads <= 0 or cfg.hidden % cfg.heads:
+        raise ValueError("hidden not divisible by heads")
+    f = seqpar_block_forward([x], params, 1, cfg, recompute, True, dtype, device)
+    return ReferenceForward(f.y_shards[0], f.ledgers[0], cfg, f.layer, f.params_digest)
+
+
+def reference_block_backward(dy: np.ndarray, fwd: ReferenceForward, params: np.ndarray) -> BlockGrads:
+    """reference_block_backward(dy, fwd, params) (block.cpp:458-510) on the GPU."""
+    if tuple(dy.shape) != tuple(fwd.y.shape):
+        raise ValueError("dy shape mismatch")
+    f = SeqparForward(1, fwd.cfg, [fwd.y], [fwd.ledger], {}, fwd.layer, fwd.params_digest)
+    b = seqpar_block_backward([dy], f, params)
+    return BlockGrads(b.param_grads, b.dx_shards[0])
+
+
+class RankShardedTensor:
+    """Mirror of RankShardedTensor (tensor.hpp:80-89, tensor.cpp:227-259); axis is
+    "sequence", "hidden" or "replicated"."""
+
+    def __init__(self, shards: list, axis: str = "replicated", logical_shape=None):
+        self.shards, self.axis = list(shards), axis
+        self.logical_shape = tuple(logical_shape) if logical_shape is not None else None
+
+    @classmethod
+    def from_full(cls, full: np.ndarray, axis: str, axis_index: int, ranks: int):
+        if axis == "replicated":
+            return cls([full.copy() for _ in range(ranks)], axis, full.shape)
+        if full.shape[axis_index] % ranks:
+            raise ValueError("split axis not divisible by part count")
+        return cls([np.ascontiguousarray(p) for p in np.split(full, ranks, axis_index)], axis, full.shape)
+
+    def to_full(self, axis_index: int) -> np.ndarray:
+        if self.axis == "replicated":
+            return self.shards[0]
+        return np.concatenate(self.shards, axis_index)
+
+    def check(self):
+        if not self.shards:
+            raise ValueError("sharded tensor has no shards")
+        if any(s.shape != self.shards[0].shape for s in self.shards):
+            raise ValueError("shard shapes differ across ranks")
+        if self.axis == "replicated" and any(not np.array_equal(s, self.shards[0]) for s in self.shards):
+            raise ValueError("replicated tensor has diverging shards")
+
+
+def attention_interior(q: np.ndarray, k: np.ndarray, cfg: BlockConfig, head_offset: int,
+                       local_heads: int, dtype: str = "f32", device: int = 0) -> np.ndarray:
+    """attention_interior(q, k, cfg, head_offset, local_heads) (block.cpp:381-417) on the GPU
+    kernel (spl_attention_interior_qk). Returns {3, local_heads, b, s, s}: softmax_out,
+    dropout_mask (0/1), dropout_out, as fp64."""
+    torch = _torch()
+    s, b = cfg.seq, cfg.batch
+    if cfg.heads <= 0 or cfg.hidden % cfg.heads:
+        raise ValueError("hidden not divisible by heads")
+    lw = local_heads * (cfg.hidden // cfg.heads)
+    if tuple(q.shape) != (s, b, lw) or tuple(k.shape) != (s, b, lw):
+        raise ValueError("attention_interior: q and k must be {s, b, local_heads*hd}")
+    td = _tdtype(dtype)
+    dev = f"cuda:{device}"
+    qd, kd = _to_dev(q, dtype, device), _to_dev(k, dtype, device)
+    n = (local_heads, b, s, s)
+    sm = torch.empty(n, dtype=td, device=dev)
+    sd = torch.empty(n, dtype=td, device=dev)
+    mk = torch.empty(n, dtype=torch.uint8, device=dev)
+    d = _desc(cfg, "none", True, dtype, True)
+    stream = C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    check(lib().spl_attention_interior_qk(C.byref(d), device, C.c_void_p(qd.data_ptr()),
+                                          C.c_void_p(kd.data_ptr()), head_offset, local_heads,
+                                          C.c_void_p(sm.data_ptr()), C.c_void_p(mk.data_ptr()),
+                                          C.c_void_p(sd.data_ptr()), stream))
+    torch.cuda.synchronize(device)
+    return np.stack([_to_host(sm), mk.cpu().numpy().astype(np.float64), _to_host(sd)])
+
+
+# ---------------------------------------------------------------- collectives (collectives.hpp:57-62)
+COMM_TAGS = {"schedule": 0, "regather": 1, "grad_sync": 2}
+
+
+def _comm_dict(log) -> dict:
+    return {t: dict(all_gathers=log[4 * i], reduce_scatters=log[4 * i + 1],
+                    all_reduces=log[4 * i + 2], ring_elements=log[4 * i + 3])
+            for i, t in enumerate(COMM_TAGS)}
+
+
+def _group(tensors: list, op: str, device: int):
+    torch = _torch()
+    if not tensors:
+        raise ValueError(f"{op}: empty rank group")
+    shape = tuple(np.shape(tensors[0]))
+    if any(tuple(np.shape(x)) != shape for x in tensors):
+        raise ValueError(f"{op}: shard shapes differ across ranks")
+    dev = [torch.from_numpy(np.ascontiguousarray(x, np.float64)).to(f"cuda:{device}") for x in tensors]
+    ptrs = (C.c_void_p * len(dev))(*[d.data_ptr() for d in dev])
+    return dev, ptrs, shape, (C.c_int64 * max(len(shape), 1))(*shape)
+
+
+def all_gather(shards: list, axis: int, tag: str = "schedule", device: int = 0):
+    """all_gather(span<const Tensor>, axis, CommLog*, tag) (collectives.cpp:40-46) on device
+    buffers in fp64. Returns (full, comm log)."""
+    torch = _torch()
+    dev, ptrs, shape, cs = _group(shards, "all_gather", device)
+    if not 0 <= axis < len(shape):
+        raise ValueError("axis out of range")
+    out_shape = list(shape)
+    out_shape[axis] *= len(shards)
+    out = torch.empty(out_shape, dtype=torch.float64, device=f"cuda:{device}")
+    log = (C.c_int64 * 12)()
+    check(lib().spl_all_gather(ptrs, len(dev), cs, len(shape), axis, _lib.DTYPE_F64,
+                               C.c_void_p(out.data_ptr()), log, COMM_TAGS[tag],
+                               C.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
+    return out.cpu().numpy(), _comm_dict(log)
+
+
+def reduce_scatter(partials: list, axis: int, tag: str = "schedule", device: int = 0):
+    """reduce_scatter (collectives.cpp:48-57): rank-ordered fp64 sum, split along axis."""
+    torch = _torch()
+    dev, ptrs, shape, cs = _group(partials, "reduce_scatter", device)
+    t = len(dev)
+    if not 0 <= axis < len(shape):
+        raise ValueError("axis out of range")
+    if shape[axis] % t:
+        raise ValueError("split axis not divisible by part count")
+    piece = list(shape)
+    piece[axis] //= t
+    outs = [torch.empty(piece, dtype=torch.float64, device=f"cuda:{device}") for _ in range(t)]
+    optr = (C.c_void_p * t)(*[o.data_ptr() for o in outs])
+    log = (C.c_int64 * 12)()
+    check(lib().spl_reduce_scatter(ptrs, t, cs, len(shape), axis, _lib.DTYPE_F64, optr, log,
+                                   COMM_TAGS[tag],
+                                   C.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
+    return [o.cpu().numpy() for o in outs], _comm_dict(log)
+
+
+def all_reduce(partials: list, tag: str = "schedule", device: int = 0):
+    """all_reduce (collectives.cpp:59-65): rank-ordered fp64 sum."""
+    torch = _torch()
+    dev, ptrs, shape, cs = _group(partials, "all_reduce", device)
+    out = torch.empty(shape, dtype=torch.float64, device=f"cuda:{device}")
+    log = (C.c_int64 * 12)()
+    check(lib().spl_all_reduce(ptrs, len(dev), cs, len(shape), _lib.DTYPE_F64,
+                               C.c_void_p(out.data_ptr()), log, COMM_TAGS[tag],
+                               C.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
+    return out.cpu().numpy(), _comm_dict(log)
+
+
+@dataclass
+class RecomputeStrategy:
+    """RecomputeStrategy (config.hpp:53-67); parse/name restate config.cpp:36-84."""
+    kind: str = "none"
+    sequence_parallel: bool = False
+    microbatch_level: bool = False
+
+    @classmethod
+    def parse(cls, spec: str) -> "RecomputeStrategy":
+        out, have = cls(), False
+        for tok in spec.split("+") if spec else []:
+            if tok in ("none", "full", "selective"):
+                if have:
+                    raise ValueError(f"strategy '{spec}' names more than one recompute kind")
+                have, out.kind = True, tok
+            elif tok == "seq":
+                out.sequence_parallel = True
+            elif tok == "mblevel":
+                out.microbatch_level = True
+            else:
+                raise ValueError(f"unknown strategy token '{tok}' (expected none|full|selective "
+                                 "with optional +seq, +mblevel)")
+        if not have:
+            raise ValueError(f"strategy '{spec}' must name one of none|full|selective")
+        if out.microbatch_level and out.kind == "none":
+            raise ValueError("'none+mblevel' is not a strategy: the microbatch window needs a "
+                             "full or selective base to checkpoint with")
+        return out
+
+    def name(self) -> str:
+        return self.kind + ("+seq" if self.sequence_parallel else "") + \
+            ("+mblevel" if self.microbatch_level else "")
 
 
 def per_layer_bytes(a: int, h: int, s: int, b: int, t: int, kind: str, sequence_parallel: bool,

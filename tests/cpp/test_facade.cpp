@@ -62,10 +62,12 @@ static Tensor concat0(const std::vector<Tensor>& v) {
   }
   return out;
 }
-static double max_abs_diff(const Tensor& a, const Tensor& b) {
-  double m = 0;
-  for (int64_t i = 0; i < a.numel(); ++i) m = std::max(m, std::abs(a[i] - b[i]));
-  return m;
+using seqpar::max_abs_diff;
+static Tensor tensor_of(std::vector<int64_t> shape, std::initializer_list<double> values) {
+  Tensor out(std::move(shape));
+  int64_t i = 0;
+  for (double v : values) out[i++] = v;
+  return out;
 }
 static int64_t group_bytes(const seqpar::ActivationLedger& l, std::initializer_list<const char*> names) {
   int64_t t = 0;
@@ -76,6 +78,165 @@ static int64_t group_bytes(const seqpar::ActivationLedger& l, std::initializer_l
 }
 
 int main() {
+  {  // reduce-scatter sums rank partials then shards them (test_seqpar.cpp:61-69)
+    std::vector<Tensor> partials{tensor_of({2}, {1, 2}), tensor_of({2}, {3, 4})};
+    const auto shards = seqpar::reduce_scatter(partials, 0);
+    CHECK(shards.size() == 2 && shards[0][0] == 4 && shards[1][0] == 6);
+  }
+  {  // at t=1 every collective is the identity (71-79)
+    std::vector<Tensor> one{tensor_of({2, 2}, {1, 2, 3, 4})};
+    CHECK(seqpar::bit_equal(seqpar::all_gather(one, 0), one[0]));
+    CHECK(seqpar::bit_equal(seqpar::all_reduce(one), one[0]));
+    const auto sc = seqpar::reduce_scatter(one, 0);
+    CHECK(sc.size() == 1 && seqpar::bit_equal(sc[0], one[0]));
+  }
+  {  // all_reduce equals all_gather of reduce_scatter on integer tensors (81-97)
+    for (uint64_t trial = 0; trial < 50; ++trial) {
+      std::vector<Tensor> partials;
+      for (int64_t r = 0; r < 4; ++r) {
+        Tensor part({8, 3});
+        for (int64_t i = 0; i < part.numel(); ++i)
+          part[i] = std::floor(seqpar::uniform01(seqpar::hash_counter(trial, (uint64_t)r), (uint64_t)i) * 33.0) - 16.0;
+        partials.push_back(std::move(part));
+      }
+      CHECK(seqpar::bit_equal(seqpar::all_reduce(partials),
+                              seqpar::all_gather(seqpar::reduce_scatter(partials, 0), 0)));
+    }
+    // CommLog ring model (collectives.cpp:30-38) and tags
+    std::vector<Tensor> parts(4, Tensor({8, 3}));
+    seqpar::CommLog log;
+    seqpar::all_gather(parts, 1, &log, seqpar::CommTag::Regather);
+    seqpar::reduce_scatter(parts, 0, &log);
+    seqpar::all_reduce(parts, &log, seqpar::CommTag::GradSync);
+    CHECK(log.regather.all_gathers == 1 && log.regather.ring_elements == (96 / 4) * 3);
+    CHECK(log.schedule.reduce_scatters == 1 && log.schedule.ring_elements == (24 / 4) * 3);
+    CHECK(log.grad_sync.all_reduces == 1 && log.grad_sync.ring_elements == 2 * (24 / 4) * 3);
+    // axis 1 concatenation / scatter follow the reference's axis blocks (tensor.cpp:169-225)
+    std::vector<Tensor> cols{tensor_of({2, 1}, {1, 2}), tensor_of({2, 1}, {3, 4})};
+    CHECK(seqpar::bit_equal(seqpar::all_gather(cols, 1), tensor_of({2, 2}, {1, 3, 2, 4})));
+    const auto rs = seqpar::reduce_scatter(std::vector<Tensor>{tensor_of({2, 2}, {1, 2, 3, 4}),
+                                                               tensor_of({2, 2}, {10, 20, 30, 40})}, 1);
+    CHECK(seqpar::bit_equal(rs[0], tensor_of({2, 1}, {11, 33})) &&
+          seqpar::bit_equal(rs[1], tensor_of({2, 1}, {22, 44})));
+  }
+  {  // collectives reject ragged rank groups (99-107)
+    std::vector<Tensor> ragged{Tensor({2, 2}), Tensor({2, 3})};
+    check_throws<std::invalid_argument>([&] { seqpar::all_reduce(ragged); }, "ragged all_reduce");
+    check_throws<std::invalid_argument>([&] { seqpar::all_gather(ragged, 0); }, "ragged all_gather");
+    check_throws<std::invalid_argument>([&] { seqpar::reduce_scatter(ragged, 0); }, "ragged reduce_scatter");
+    std::vector<Tensor> three(3, Tensor({4}));
+    check_throws<std::invalid_argument>([&] { seqpar::reduce_scatter(three, 0); }, "indivisible scatter");
+  }
+  {  // sharded tensors reassemble and police their invariants (109-120)
+    const Tensor full = seqpar::random_uniform(1, {4, 2, 6}, -1, 1);
+    const auto sh = seqpar::RankShardedTensor::from_full(full, seqpar::ShardAxis::Sequence, 0, 2);
+    CHECK(sh.shards.size() == 2);
+    CHECK(seqpar::bit_equal(sh.to_full(0), full));
+    sh.check();
+    auto rep = seqpar::RankShardedTensor::from_full(full, seqpar::ShardAxis::Replicated, 0, 2);
+    rep.check();
+    rep.shards[1][0] += 1.0;
+    check_throws<std::invalid_argument>([&] { rep.check(); }, "diverging replicas");
+    // the RankShardedTensor overload of seqpar_block_forward (block.hpp:158-162)
+    const BlockConfig cfg = toy();
+    const LayerParams p = LayerParams::random(cfg, 31);
+    const Tensor x = seqpar::random_uniform(32, {4, 1, 8}, -1, 1);
+    auto a = seqpar::seqpar_block_forward(
+        seqpar::RankShardedTensor::from_full(x, seqpar::ShardAxis::Sequence, 0, 2), p, cfg);
+    auto b = seqpar::seqpar_block_forward(split0(x, 2), p, 2, cfg);
+    CHECK(a.t == 2 && seqpar::bit_equal(concat0(a.y_shards), concat0(b.y_shards)));
+    check_throws<std::invalid_argument>(
+        [&] {
+          seqpar::seqpar_block_forward(
+              seqpar::RankShardedTensor::from_full(x, seqpar::ShardAxis::Hidden, 2, 2), p, cfg);
+        },
+        "hidden-sharded input");
+  }
+  {  // reference forward: ledger, zero block, p=0 masks, t=1 bit identity (122-168)
+    BlockConfig cfg = toy();
+    const LayerParams p = LayerParams::random(cfg, 11);
+    const Tensor x = seqpar::random_uniform(3, {4, 1, 8}, -1, 1);
+    const auto fwd = seqpar::reference_block_forward(x, p, cfg);
+    CHECK(fwd.ledger.total_bytes() == 1248);
+    CHECK(fwd.ledger.total_bytes() == seqpar::layer_component_breakdown(2, 8, 4, 1).total);
+    const auto z = seqpar::reference_block_forward(Tensor({4, 1, 8}), LayerParams::zeros(cfg), cfg);
+    bool zero = true;
+    for (int64_t i = 0; i < z.y.numel(); ++i) zero &= z.y[i] == 0.0;
+    CHECK(zero);
+    cfg.dropout_p = 0.0;
+    const LayerParams p5 = LayerParams::random(cfg, 5);
+    const Tensor x9 = seqpar::random_uniform(9, {4, 1, 8}, -1, 1);
+    const auto dry = seqpar::reference_block_forward(x9, p5, cfg);
+    const Tensor m = dry.attn_dropout_mask();
+    bool ones = m.numel() == 32;
+    for (int64_t i = 0; i < m.numel(); ++i) ones &= m[i] == 1.0;
+    CHECK(ones);
+    cfg.dropout_p = 0.25;
+    CHECK(seqpar::reference_block_forward(x9, p5, cfg).ledger.total_bytes() == dry.ledger.total_bytes());
+    const BlockConfig c0 = toy();
+    const LayerParams p21 = LayerParams::random(c0, 21);
+    const Tensor x22 = seqpar::random_uniform(22, {4, 1, 8}, -1, 1);
+    CHECK(seqpar::bit_equal(seqpar::seqpar_block_forward({x22}, p21, 1, c0).y_shards[0],
+                            seqpar::reference_block_forward(x22, p21, c0).y));
+    // reference backward == seqpar t=1 backward
+    const Tensor dy = seqpar::random_uniform(23, {4, 1, 8}, -1, 1);
+    const auto rf = seqpar::reference_block_forward(x22, p21, c0);
+    const auto rg = seqpar::reference_block_backward(dy, rf, p21);
+    const auto sf = seqpar::seqpar_block_forward({x22}, p21, 1, c0);
+    const auto sg = seqpar::seqpar_block_backward({dy}, sf, p21);
+    CHECK(seqpar::bit_equal(rg.dx, sg.dx_shards[0]));
+    CHECK(seqpar::bit_equal(rg.params.w1, sg.param_grads.w1));
+    check_throws<std::invalid_argument>([&] { seqpar::reference_block_forward(Tensor({2, 1, 8}), p21, c0); },
+                                        "reference input shape");
+    // backward with other params: the GEMMs use them (block.cpp:639-640)
+    const LayerParams other = LayerParams::random(c0, 99);
+    const auto og = seqpar::reference_block_backward(dy, seqpar::reference_block_forward(x22, p21, c0), other);
+    CHECK(!seqpar::bit_equal(og.dx, rg.dx));
+  }
+  {  // attention_interior(q, k, cfg, head_offset, local_heads) (block.cpp:381-417)
+    BlockConfig cfg;
+    cfg.heads = 4; cfg.hidden = 32; cfg.seq = 16; cfg.batch = 2; cfg.dropout_p = 0.1; cfg.causal = true;
+    const Tensor q = seqpar::random_uniform(41, {16, 2, 32}, -1, 1);
+    const Tensor k = seqpar::random_uniform(42, {16, 2, 32}, -1, 1);
+    const auto full = seqpar::attention_interior(q, k, cfg, 0, 4);
+    // head slice 2..3 = the rank-1 view at t=2: columns 16..31 of q/k
+    Tensor q1({16, 2, 16}), k1({16, 2, 16});
+    for (int64_t r = 0; r < 32; ++r)
+      for (int64_t c = 0; c < 16; ++c) {
+        q1[r * 16 + c] = q[r * 32 + 16 + c];
+        k1[r * 16 + c] = k[r * 32 + 16 + c];
+      }
+    const auto half = seqpar::attention_interior(q1, k1, cfg, 2, 2);
+    const int64_t per = 2 * 2 * 16 * 16;
+    bool same_mask = true, same_sm = true, rows_ok = true, drop_ok = true;
+    for (int64_t i = 0; i < per; ++i) {
+      same_mask &= half.dropout_mask[i] == full.dropout_mask[per + i];
+      same_sm &= std::abs(half.softmax_out[i] - full.softmax_out[per + i]) <= 1e-6;
+      drop_ok &= std::abs(half.dropout_out[i] - half.softmax_out[i] * half.dropout_mask[i] / 0.9) <= 1e-6;
+    }
+    for (int64_t row = 0; row < 2 * 2 * 16; ++row) {
+      double sum = 0;
+      for (int64_t j = 0; j < 16; ++j) {
+        sum += half.softmax_out[row * 16 + j];
+        if (j > row % 16) rows_ok &= half.softmax_out[row * 16 + j] == 0.0;  // causal
+      }
+      rows_ok &= std::abs(sum - 1.0) <= 1e-5;
+    }
+    CHECK(same_mask && same_sm && rows_ok && drop_ok);
+    check_throws<std::invalid_argument>([&] { seqpar::attention_interior(q1, k1, cfg, 1, 2); },
+                                        "misaligned head offset");
+  }
+  {  // RecomputeStrategy::parse / name (test_config.cpp:92-106)
+    using S = seqpar::RecomputeStrategy;
+    for (const char* n : {"none", "full", "selective", "none+seq", "full+seq", "selective+seq",
+                          "full+mblevel", "selective+seq+mblevel"})
+      CHECK(S::parse(n).name() == n);
+    CHECK(S::parse("full+seq").sequence_parallel);
+    CHECK(S::parse("selective+mblevel").microbatch_level);
+    CHECK(S::parse("seq+selective") == S::parse("selective+seq"));
+    for (const char* bad : {"none+mblevel", "bogus", "full+bogus", "full+selective", "seq"})
+      check_throws<std::invalid_argument>([&] { S::parse(bad); }, bad);
+  }
   {  // ledger matches the itemised toy count (test_seqpar.cpp:120-137)
     const BlockConfig cfg = toy();
     const LayerParams p = LayerParams::random(cfg, 11);

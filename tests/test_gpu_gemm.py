@@ -93,3 +93,14 @@ def test_gemm_single_cta_variant(env):
                         "-k", "test_gemm_tc or large_k", "-p", "no:cacheprovider"],
                        env=dict(os.environ, SPL_GEMM_PAIR="0"), capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("orient,epi", [((False, True), 1), ((False, False), 3), ((True, True), 4)])
+def test_gemm_k24576(env, orient, epi):
+    """K = 4h = 24576: the 22B FC2 forward / FC1-input dgrad reduction depth (and the wgrad
+    orientation at the same depth)."""
+    spl, torch = env
+    be, out, _, ref = run_gemm(spl, torch, 512, 768, 24576, *orient, epi, seed=3)
+    assert be == 1
+    # fp32 accumulation over K = 24576: the rounding error grows ~sqrt(K) (2.7e-5 measured)
+    assert rel(out, ref) <= (5e-5 if epi == 4 else 5e-3), rel(out, ref)
