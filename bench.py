@@ -130,68 +130,114 @@ def gemm_traffic_from_profile(cfg_name):
     return b / n if n else None
 
 
-def cpu_baseline_sample(cfg_name, threads=0):
-    """The oracle (fp64 restatement of the reference seqpar layer, test infrastructure) timed
-    on the host cores on a bounded sample of the workload: the same layer width (h, a) with
-    one sequence of s_sample tokens; fwd+bwd, tokens/s."""
+def _layer_inputs(mod, cfg_name, s_sample, b_sample):
+    a, h, _, _ = CONFIGS[cfg_name]
     import oracle as orc
-    a, h, s, b = CONFIGS[cfg_name]
-    s_sample = min(s, 512) if cfg_name != "tiny" else s
-    b_sample = 1 if cfg_name != "tiny" else b
-    cores = orc.set_threads(threads)
     cfg = orc.BlockConfig(heads=a, hidden=h, seq=s_sample, batch=b_sample, dropout_p=0.1, seed=42)
     p = orc.params_random(h, 7)
     x = orc.random_uniform(1, (s_sample, b_sample, h), -1, 1)
     dy = orc.random_uniform(2, (s_sample, b_sample, h), -1, 1)
+    return cfg, p, x, dy
+
+
+def reference_cpu(cfg_name, s_sample, b_sample, budget_s, warmup=1, steps=1):
+    """The reference's OWN seqpar fwd+bwd (block.cpp/tensor.cpp/collectives.cpp compiled
+    unmodified into oracle/_ref/libref_seqpar.so — single-threaded, as the reference is) on a
+    bounded sample of the workload: the config's full width (h, a) with s_sample·b_sample tokens.
+    Falls back to the fp64 restatement (oracle port) on one thread when the library was not
+    built. Returns (tokens/s, seconds per step, steps, warmup, kind)."""
+    from oracle import ref as R
+    import oracle as orc
+    kind = "reference" if R.available() else "port"
+    cfg, p, x, dy = _layer_inputs(None, cfg_name, s_sample, b_sample)
+    if kind == "port":
+        orc.set_threads(1)
+        run = lambda: orc.seqpar_layer(cfg, 1, p, x, dy)  # noqa: E731
+    else:
+        run = lambda: R.seqpar_layer(cfg, 1, p, x, dy)  # noqa: E731
+    t0 = time.perf_counter()
+    run()  # first warm-up step, also sizes the run
+    one = time.perf_counter() - t0
+    fit = max(1, int(budget_s / max(one, 1e-3)) - 1)
+    warmup = max(0, min(warmup - 1, fit // 2))
+    steps = max(1, min(steps, fit - warmup))
+    for _ in range(warmup):
+        run()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        run()
+    dt = (time.perf_counter() - t0) / steps
+    return s_sample * b_sample / dt, dt, steps, warmup + 1, kind
+
+
+def cpu_baseline_sample(cfg_name):
+    """cpu_baseline of the ours-arm line (rank 0, N=1): the reference's own code on 1 core
+    (faithful: the reference is single-threaded) on a 128-token sample, plus the fp64 port on
+    all host cores on a 512-token sample (BASELINE.md §4 asks for both)."""
+    import oracle as orc
+    a, h, s, b = CONFIGS[cfg_name]
+    s1 = s if cfg_name == "tiny" else 128
+    b1 = b if cfg_name == "tiny" else 1
+    v1, dt1, _, _, kind = reference_cpu(cfg_name, s1, b1, budget_s=60.0)
+    s_all = s if cfg_name == "tiny" else 512
+    b_all = b if cfg_name == "tiny" else 1
+    cores = orc.set_threads(0)
+    cfg, p, x, dy = _layer_inputs(None, cfg_name, s_all, b_all)
     t0 = time.perf_counter()
     orc.seqpar_layer(cfg, 1, p, x, dy)
-    dt = time.perf_counter() - t0
-    return {"value": s_sample * b_sample / dt, "unit": "tokens/s", "cores": cores, "kind": "port",
-            "sample": f"oracle fp64 seqpar fwd+bwd, h={h} a={a} s={s_sample} b={b_sample}, t=1 "
-                      f"({dt:.2f} s)", "seconds": dt}
+    dta = time.perf_counter() - t0
+    return {"value": v1, "unit": "tokens/s", "cores": 1, "kind": kind,
+            "sample": f"the reference's own seqpar_block_forward+backward (fp64, oracle/_ref, "
+                      f"1 thread) at h={h} a={a} s={s1} b={b1} t=1 ({dt1:.1f} s/step)",
+            "all_cores": {"value": s_all * b_all / dta, "unit": "tokens/s", "cores": cores,
+                          "kind": "port",
+                          "sample": f"fp64 restatement (OpenMP) at h={h} a={a} s={s_all} "
+                                    f"b={b_all} t=1 ({dta:.1f} s)"}}
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path (the oracle port — the reference needs
-    Eigen/Boost, absent here) on all host threads, rank 0 only."""
+    """--impl reference: the reference's CPU path — its own block.cpp / tensor.cpp /
+    collectives.cpp compiled unmodified (oracle/_ref, single-threaded like the reference) —
+    rank 0 only, on a bounded sample of the config (full width, 256 tokens per step)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import oracle as orc
     a, h, s, b = CONFIGS[args.config]
-    s_sample = min(s, 512) if args.config != "tiny" else s
-    b_sample = 1 if args.config != "tiny" else b
-    cores = orc.set_threads(0)
-    cfg = orc.BlockConfig(heads=a, hidden=h, seq=s_sample, batch=b_sample, dropout_p=0.1, seed=42)
-    p = orc.params_random(h, 7)
-    x = orc.random_uniform(1, (s_sample, b_sample, h), -1, 1)
-    dy = orc.random_uniform(2, (s_sample, b_sample, h), -1, 1)
-    budget = 150.0  # seconds for the whole run (warm-up included)
-    t0 = time.perf_counter()
-    orc.seqpar_layer(cfg, 1, p, x, dy)  # first warm-up step, also sizes the run
-    one = time.perf_counter() - t0
-    fit = max(2, int(budget / max(one, 1e-3)))
-    warmup = max(1, min(args.warmup, fit // 2))
-    steps = max(1, min(args.steps, fit - warmup))
-    for _ in range(warmup - 1):
-        orc.seqpar_layer(cfg, 1, p, x, dy)
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        orc.seqpar_layer(cfg, 1, p, x, dy)
-    dt = (time.perf_counter() - t0) / steps
-    v = s_sample * b_sample / dt
-    sample = (f"oracle fp64 seqpar fwd+bwd (reference algorithm; reference build needs Eigen3/"
-              f"Boost, absent), h={h} a={a} s={s_sample} b={b_sample} t=1, {steps} steps")
+    s_sample = s if args.config == "tiny" else 256
+    b_sample = b if args.config == "tiny" else 1
+    v, dt, steps, warmup, kind = reference_cpu(args.config, s_sample, b_sample, budget_s=240.0,
+                                               warmup=args.warmup, steps=args.steps)
+    who = ("the reference's own seqpar_block_forward+backward (block.cpp/tensor.cpp/"
+           "collectives.cpp/rng.cpp compiled unmodified, oracle/_ref, Eigen/Boost shims)"
+           if kind == "reference" else "fp64 restatement of the reference (oracle port)")
+    sample = f"{who}, fp64, 1 thread, h={h} a={a} s={s_sample} b={b_sample} t=1, {steps} timed steps"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
             "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config} layer fwd+bwd (sampled)", "heads": a, "hidden": h,
-                       "seq": s, "batch": b},
-            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "config": {"workload": f"{args.config} layer fwd+bwd (sampled: {s_sample * b_sample} "
+                                   f"tokens per step)", "heads": a, "hidden": h, "seq": s, "batch": b},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": 1, "kind": kind,
                              "sample": sample},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def self_launch(args):
+    """`python bench.py --gpus N` (N > 1) without torchrun: re-exec under
+    torch.distributed.run with one process per GPU — never a silent single-GPU run."""
+    import socket
+    import torch
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} needs {args.gpus} visible GPUs, found {n}")
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -206,31 +252,45 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "ipc"],
+                    help="transport of the t>1 collectives: NCCL, or libspl's CUDA-IPC peer-memory "
+                         "transport (spl_create_ipc)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
     import torch
     import paper_2205_05198_b200 as spl
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: one process per GPU")
     t = world
-    assert t == args.gpus or world == 1, "launch one process per GPU (torchrun) for --gpus > 1"
     torch.cuda.set_device(local_rank)
     dist = None
     nccl = None
+    ipc = None
     if "WORLD_SIZE" in os.environ and "MASTER_ADDR" in os.environ:
-        # launched by torchrun (any N, including 1): one NCCL rank per GPU
+        # launched by torchrun (any N, including 1): one rank per GPU; NCCL for the plumbing
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
-        nccl = (rank, share_unique_id(spl.SeqparLayer.nccl_unique_id, rank))
+        if args.comm == "ipc" and t > 1:
+            def exchange(hb):
+                got = [None] * t
+                dist.all_gather_object(got, hb)
+                return got
+            ipc = (rank, exchange)
+        else:
+            nccl = (rank, share_unique_id(spl.SeqparLayer.nccl_unique_id, rank))
     a, h, s, b = CONFIGS[args.config]
     sp = not args.no_sp
     cfg = spl.BlockConfig(a, h, s, b, dropout_p=0.1, causal=False, seed=42)
     L = spl.SeqparLayer(cfg, t, args.recompute, sp, "bf16", device=local_rank,
-                        check_finite=False, nccl=nccl)
+                        check_finite=False, nccl=nccl, ipc=ipc)
     L.init_params(1234)
     L.set_graphs(not args.no_graphs)  # forward / backward replayed as CUDA graphs
     shp = L.shard_shape()
@@ -312,12 +372,28 @@ def main():
     pk, pk_kind = peaks()
     g = prof["gemm"]
     gemm_tflops = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
-    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    burst = pk.get("bf16_tflops")
+    sustained = pk.get("bf16_tflops_sustained", burst)
+    hbm = pk.get("hbm_gbs")
     total_prof_ms = sum(v["ms"] for v in prof.values())
     led, phys, unc = L.saved_bytes(0)
     mf = model_flops(a, h, s, b)
+
+    def cls_roof(name, bound):
+        v = prof[name]
+        if not v["ms"]:
+            return None
+        if bound == "tensor":
+            ach = v["flops"] / (v["ms"] / 1e3) / 1e12
+            return {"bound": "tensor", "achieved": ach, "peak": burst, "unit": "TFLOP/s",
+                    "frac": ach / burst if burst else None, "ms_per_step": v["ms"] / args.steps}
+        ach = v["bytes"] / (v["ms"] / 1e3) / 1e9
+        peak_b = hbm if bound == "hbm" else 900.0  # NVLink 5: 900 GB/s per direction
+        return {"bound": bound, "achieved": ach, "peak": peak_b, "unit": "GB/s",
+                "frac": ach / peak_b if peak_b else None, "ms_per_step": v["ms"] / args.steps}
+
     line = {
-        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded U(-1,1) inputs, LayerParams::random on device)",
@@ -325,22 +401,32 @@ def main():
                                f"{args.recompute} recompute",
                    "heads": a, "hidden": h, "seq": s, "batch": b, "t": t, "dropout_p": 0.1,
                    "causal": False, "parallelism": f"tp{t}+sp" if sp else f"tp{t}",
+                   "comm": (args.comm if t > 1 else "none"),
                    "l2": "working set > L2 (weights alone 0.9 GB/t); no flush"},
-        "mfu": mf / (ms_step / 1e3) / t / (peak * 1e12),
+        "mfu": mf / (ms_step / 1e3) / t / (burst * 1e12),
+        "mfu_vs_sustained_peak": mf / (ms_step / 1e3) / t / (sustained * 1e12),
         "mfu_vs_nominal_2250": mf / (ms_step / 1e3) / t / 2.25e15,
         "activation_bytes_per_gpu": {"ledger": led, "physical": phys, "uncounted_stats": unc,
                                      "formula_34sbh_over_t": 34 * s * b * h // t,
                                      "per_layer_bytes": spl.per_layer_bytes(a, h, s, b, t, args.recompute, sp)},
         "roofline": {"kernel": "tcgen05 GEMM (all layer GEMMs)", "bound": "tensor",
-                     "achieved": gemm_tflops, "peak": peak, "unit": "TFLOP/s",
-                     "frac": gemm_tflops / peak if peak else None,
+                     "achieved": gemm_tflops, "peak": burst, "unit": "TFLOP/s",
+                     "frac": gemm_tflops / burst if burst else None,
                      "traffic": gemm_traffic_from_profile(args.config) if t == 1 else None,
                      "traffic_unit": "DRAM bytes per GEMM launch (ncu, profiles/)",
                      "algorithmic_bytes_per_launch": g["bytes"] / max(g["launches"], 1),
-                     "peak_kind": f"{pk_kind} bf16_tflops_sustained (cuBLAS 8192^3 back to back; "
-                                  f"MEASURED_PEAKS records its clock median under load)",
-                     "frac_of_burst_peak": gemm_tflops / pk["bf16_tflops"] if pk.get("bf16_tflops") else None,
+                     "peak_kind": f"{pk_kind} bf16_tflops (burst: cuBLAS 8192^3 best of 10)",
+                     "frac_of_sustained_peak": gemm_tflops / sustained if sustained else None,
                      "share_of_step": g["ms"] / total_prof_ms if total_prof_ms else None},
+        "rooflines": {"gemm": cls_roof("gemm", "tensor"), "attention": cls_roof("attention", "tensor"),
+                      "elementwise": cls_roof("elementwise", "hbm"),
+                      "collective": cls_roof("collective", "nvlink") if t > 1 else None,
+                      "other": ({"what": "softmax-dropout keep-bit RNG (ALU-bound: 2 splitmix64 "
+                                         "per interior element)",
+                                 "ms_per_step": prof["other"]["ms"] / args.steps,
+                                 "keys_per_s": (a // t) * b * s * s * prof["other"]["launches"] / args.steps
+                                 / max(prof["other"]["ms"] / args.steps / 1e3, 1e-12)}
+                                if prof["other"]["ms"] else None)},
         "kernel_classes": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
                                "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] and v["flops"] else None,
                                "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] and v["bytes"] else None}
