@@ -141,7 +141,7 @@ def lib():
 
 def header_symbols() -> list[str]:
     """Every function the C ABI header declares."""
-    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/|//[^\n]*", "", open(HEADER).read(), flags=re.S)
     return sorted(set(re.findall(r"\b(spl_[a-z0-9_]+)\s*\(", text)))
 
 
