@@ -867,6 +867,10 @@ template <>
 void attn_bwd_tc<bf16>(const AttnArgs& a, const void* dout, void* dqkv, float* delta,
                        cudaStream_t st) {
   const bool stored = a.sm != nullptr;
+  if (umma_bwd_on(a) && attn_bwd_fused_supported(a)) {
+    attn_bwd_fused(a, dout, dqkv, st);
+    return;
+  }
   if (umma_bwd_on(a)) {  // recompute regimes and (stored interior) the no-recompute regime
     const int64_t rows = a.lh * a.b * a.s;
     SPL_HD_SWITCH(a.hd, fa_delta<HD><<<(unsigned)((rows * 4 + 255) / 256), 256, 0, st>>>(

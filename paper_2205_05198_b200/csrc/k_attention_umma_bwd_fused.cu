@@ -1,0 +1,484 @@
+// Attention backward in ONE kernel per (key block, head, batch) for the recompute regimes
+// (selective / full), tcgen05 + TMEM + TMA, bf16, head_dim 64 / 96: dK, dV and dQ from a single
+// recomputation of Sᵀ, dPᵀ and the softmax-backward elements (block.cpp:159-193), where the
+// split kernels (k_attention_umma_bwd.cu) recompute them twice (7 GEMM-equivalents and two
+// exponentials per element instead of 5 and one).
+//
+// CTA = 128 keys of one (head, batch), loops over 64-query tiles (the dK/dV kernel's loop):
+//   MMA   Sᵀ = K·Qᵀ, dPᵀ = V·dOᵀ (M=128 keys, N=64 queries, SS)          -> TMEM (2 buffers)
+//   warps Pᵀ = exp2(Sᵀc - lse), keep from the keep bits (transposed per warp),
+//         P̃ᵀ = Pᵀ·keep/(1-p) -> TMEM over the consumed Sᵀ columns (A of a TS-form MMA),
+//         dSᵀ = Pᵀ∘(dPᵀ·keep/(1-p) - rowdot) -> smem, bf16 [128 keys][64 queries] SW128
+//   MMA   dV += P̃ᵀ·dO (TS), dK += dSᵀ·Q (SS, dSᵀ K-major),
+//         dQᵀ = Kᵀ·dSᵀ (SS: M = head_dim rows padded to 128 read MN-major from the K tile,
+//         B = the same dSᵀ tile read MN-major) -> TMEM (its own 64 columns)
+//   warps dQ readers (one per 32 head_dim rows) add the dQᵀ tile into an fp32 accumulator
+//         dq_acc[(head, batch)][query][head_dim] with red.global.add.f32 (coalesced: lanes =
+//         consecutive head_dim), so the dQ sum over key blocks happens in L2 (order between
+//         key blocks is not fixed: dQ is reproducible to fp32 rounding, dK / dV bit-exactly;
+//         SPL_ATTN_DETERMINISTIC=1 selects the split kernels).
+// fa_bwd_prep (before): rowdot -> -rowdot, -lse·log2(e) per query row (loaded per tile by
+// the producer with bulk copies) and zeroes dq_acc; fa_bwd_dq_store (after): dq_acc·scale ->
+// bf16 into the Q columns of dqkv.
+//
+// Warp roles (512 threads, 128 registers each):
+//   warps 0-7   softmax-backward elements (TMEM lane quadrant = warp & 3, query half = warp >> 2)
+//   warps 8-11  dQ readers (TMEM lane quadrant = warp & 3; idle when 32·quadrant >= head_dim)
+//   warp 12     TMA producer; warp 13 TMEM allocator + MMA issuer; warps 14-15 idle
+#include <cstring>
+
+#include "kernels.hpp"
+#include "tc_common.cuh"
+
+namespace spl::k {
+
+CUtensorMap attn_seq_map(const void* ptr, int64_t width, int64_t b, int64_t s, int64_t ld, int rows);
+
+namespace {
+
+using namespace tc;
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+  uint32_t m = 0x0000ffffu;
+#pragma unroll
+  for (int j = 16; j != 0; j >>= 1, m ^= m << j) {
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+    x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y & m) << j));
+  }
+  return x;
+}
+
+template <int HD>
+struct FusedCfg {
+  static_assert(HD == 64 || HD == 96, "fused attention backward: head_dim 64 or 96");
+  static constexpr int ATOMS = (HD + 63) / 64;
+  static constexpr int A128 = 128 * 128;        // atom stride of a 128-row tile
+  static constexpr int A64 = 64 * 128;          // atom stride of a 64-row tile
+  static constexpr int T128 = ATOMS * A128;
+  static constexpr int T64 = ATOMS * A64;
+  static constexpr int NS = HD > 64 ? 3 : 4;    // (Q, dO, stats) ring depth
+  static constexpr int K_OFF = 0, V_OFF = T128, QD_OFF = 2 * T128;
+  static constexpr int ST_OFF = QD_OFF + NS * 2 * T64;          // [NS][-lse·log2e x64][-rowdot x64]
+  static constexpr int DS_OFF = (ST_OFF + NS * 512 + 1023) / 1024 * 1024;  // [2][128 x 64 bf16]
+  static constexpr int DS_BYTES = 128 * 128;
+  static constexpr int BAR_OFF = DS_OFF + 2 * DS_BYTES;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  // TMEM: Sᵀ [0,128) (2 x 64), dPᵀ [128,256), dV, dK (HD each), dQᵀ (64)
+  static constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + HD;
+  static constexpr uint32_t DQ_COL = 256 + 2 * HD;
+  static_assert(DQ_COL + 64 <= 512, "TMEM budget");
+  static constexpr int NQW = (HD + 31) / 32;  // dQ reader warps
+};
+
+template <int HD, bool CAUSAL>
+__global__ void __launch_bounds__(512, 1)
+    fa_bwd_fused_umma(const __grid_constant__ CUtensorMap map_kv,  // qkv, 128-row boxes
+                      const __grid_constant__ CUtensorMap map_q,   // qkv, 64-row boxes
+                      const __grid_constant__ CUtensorMap map_do,  // dO, 64-row boxes
+                      AttnArgs a, bf16* __restrict__ dqkv) {
+  using C = FusedCfg<HD>;
+  constexpr int NS = C::NS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* qd_full = bar + 1;           // [NS]
+  uint64_t* qd_empty = bar + 1 + NS;     // [NS]
+  uint64_t* sd_full = bar + 1 + 2 * NS;  // [2] Sᵀ, dPᵀ in TMEM
+  uint64_t* sd_free = sd_full + 2;       // [2] read by the softmax warps
+  uint64_t* w_full = sd_full + 4;        // [2] P̃ᵀ (TMEM) + dSᵀ (smem) written
+  uint64_t* w_free = sd_full + 6;        // [2] consumed by the dV / dK / dQᵀ MMAs
+  uint64_t* dq_full = sd_full + 8;       // dQᵀ of the current tile in TMEM
+  uint64_t* dq_free = sd_full + 9;       // read out by the dQ readers
+  uint64_t* acc_full = sd_full + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sd_full + 11);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k0 = blockIdx.x * 128;
+  const int hb = blockIdx.y;
+  const int hl = hb / (int)a.b, bj = hb % (int)a.b;
+  const int S = (int)a.s;
+  const int q_start = CAUSAL ? (k0 / 64) * 64 : 0;
+  const int nq = (S - q_start) / 64;
+  const int kcol = (int)(a.koff + (int64_t)hl * HD), vcol = (int)(a.voff + (int64_t)hl * HD),
+            qcol = (int)(a.qoff + (int64_t)hl * HD), dcol = hl * HD;
+  const int64_t brow = (int64_t)hb * a.s;
+  const float* nlse = a.bstat;                  // -lse·log2(e)  [lh*b*s]
+  const float* ndel = a.bstat + a.lh * a.b * a.s;  // -rowdot
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&qd_full[i], 1);
+      mbar_init(&qd_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sd_full[i], 1);
+      mbar_init(&sd_free[i], 8);
+      mbar_init(&w_full[i], 8);
+      mbar_init(&w_free[i], 1);
+    }
+    mbar_init(dq_full, 1);
+    mbar_init(dq_free, C::NQW);
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 13) tmem_alloc_warp(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp >= 12) {
+    if (warp == 12 && lane == 0) {
+      // ------------------------------------------------ TMA producer
+      mbar_expect_tx(kv_full, 2 * C::T128);
+#pragma unroll
+      for (int at = 0; at < C::ATOMS; ++at) {
+        tma_load_3d(smem + C::K_OFF + at * C::A128, &map_kv, kv_full, kcol + 64 * at, bj, k0);
+        tma_load_3d(smem + C::V_OFF + at * C::A128, &map_kv, kv_full, vcol + 64 * at, bj, k0);
+      }
+      for (int it = 0; it < nq; ++it) {
+        const int st = it % NS;
+        mbar_wait(&qd_empty[st], ((it / NS) & 1) ^ 1);
+        uint8_t* Qt = smem + C::QD_OFF + st * 2 * C::T64;
+        uint8_t* Dt = Qt + C::T64;
+        float* stt = reinterpret_cast<float*>(smem + C::ST_OFF + st * 512);
+        const int qb = q_start + it * 64;
+        mbar_expect_tx(&qd_full[st], 2 * C::T64 + 512);
+#pragma unroll
+        for (int at = 0; at < C::ATOMS; ++at) {
+          tma_load_3d(Qt + at * C::A64, &map_q, &qd_full[st], qcol + 64 * at, bj, qb);
+          tma_load_3d(Dt + at * C::A64, &map_do, &qd_full[st], dcol + 64 * at, bj, qb);
+        }
+        bulk_load(stt, nlse + brow + qb, 256, &qd_full[st]);
+        bulk_load(stt + 64, ndel + brow + qb, 256, &qd_full[st]);
+      }
+    } else if (warp == 13 && lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc_sd = make_idesc(128, 64, false, false);
+      constexpr uint32_t idesc_acc = make_idesc(128, HD, false, true);
+      constexpr uint32_t idesc_dq = make_idesc(128, 64, true, true);
+      const uint32_t ka = smem_u32(smem + C::K_OFF), va = smem_u32(smem + C::V_OFF);
+      mbar_wait(kv_full, 0);
+      auto issue_sd = [&](int it) {
+        const int sb = it & 1, qs = it % NS;
+        mbar_wait(&qd_full[qs], (it / NS) & 1);
+        mbar_wait(&sd_free[sb], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t qb = smem_u32(smem + C::QD_OFF + qs * 2 * C::T64), db = qb + C::T64;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * C::A128 + (kk & 3) * 32;
+          const uint32_t ob = (kk >> 2) * C::A64 + (kk & 3) * 32;
+          umma_bf16(tmem + C::S_COL + sb * 64, smem_desc(ka + oa, 16, 1024),
+                    smem_desc(qb + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
+          umma_bf16(tmem + C::DP_COL + sb * 64, smem_desc(va + oa, 16, 1024),
+                    smem_desc(db + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&sd_full[sb]);
+      };
+      if (nq > 0) issue_sd(0);
+      for (int it = 0; it < nq; ++it) {
+        if (it + 1 < nq) issue_sd(it + 1);
+        const int st = it & 1, qs = it % NS;
+        mbar_wait(&w_full[st], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t dsw = smem_u32(smem + C::DS_OFF + st * C::DS_BYTES);
+        const uint32_t qb = smem_u32(smem + C::QD_OFF + qs * 2 * C::T64), db = qb + C::T64;
+#pragma unroll
+        for (int kk = 0; kk < 64 / 16; ++kk) {
+          // dV += P̃ᵀ·dO (A: P̃ᵀ in TMEM, queries 32h.. of half h at columns 32h..+16);
+          // dK += dSᵀ·Q (A: dSᵀ smem, K-major)
+          const uint64_t bdo = smem_desc(db + kk * 2048, C::A64, 1024);
+          const uint64_t bq = smem_desc(qb + kk * 2048, C::A64, 1024);
+          const uint32_t col = (uint32_t)(st * 64 + (kk >> 1) * 32 + (kk & 1) * 8);
+          umma_bf16_ts(tmem + C::DV_COL, tmem + C::S_COL + col, bdo, idesc_acc, (it | kk) != 0 ? 1u : 0u);
+          umma_bf16(tmem + C::DK_COL, smem_desc(dsw + kk * 32, 16, 1024), bq, idesc_acc,
+                    (it | kk) != 0 ? 1u : 0u);
+        }
+        // dQᵀ = Kᵀ·dSᵀ: K = the CTA's 128 keys in 8 steps of 16 rows; A = K tile MN-major
+        // (head_dim rows, padded to M = 128), B = dSᵀ MN-major (queries contiguous)
+        mbar_wait(dq_free, ((it & 1) ^ 1));
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 128 / 16; ++kk)
+          umma_bf16(tmem + C::DQ_COL, smem_desc(ka + kk * 2048, C::A128, 1024),
+                    smem_desc(dsw + kk * 2048, 8192, 1024), idesc_dq, kk > 0 ? 1u : 0u);
+        umma_commit(&w_free[st]);
+        umma_commit(&qd_empty[qs]);
+        umma_commit(dq_full);
+      }
+      umma_commit(acc_full);
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------ dQ readers
+    const int qd = warp & 3;
+    if (qd < C::NQW) {
+      const int row = qd * 32 + lane;  // head_dim index
+      const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16) + C::DQ_COL;
+      float* accp = a.dq_acc + (brow + q_start) * HD + row;
+      for (int it = 0; it < nq; ++it) {
+        mbar_wait(dq_full, it & 1);
+        tc_fence_after();
+        uint32_t v0[32], v1[32];
+        tmem_ld32_nw(tl, v0);
+        tmem_ld32_nw(tl + 32, v1);
+        tmem_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dq_free);
+        if (row < HD) {
+          float* p = accp + (int64_t)it * 64 * HD;
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p + c * HD), "f"(__uint_as_float(v0[c])) : "memory");
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p + (32 + c) * HD), "f"(__uint_as_float(v1[c])) : "memory");
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ softmax-backward warps
+    const int qd = warp & 3;
+    const int half = warp >> 2;       // query columns 32*half .. +31 of each 64-query tile
+    const int row = qd * 32 + lane;   // key row
+    const int key = k0 + row;
+    const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16);
+    const float sl2 = a.scale * kLog2e;
+    const float inv_keep = a.drop.inv_keep;
+    const bool drop_on = a.drop.thresh != 0;
+    const int W = S / 32;
+    const uint32_t* kbits = a.keepbits;
+    // keep-bit word (query qb + 32*half + lane, this warp's 32 keys), one tile ahead
+    auto kword = [&](int it) -> uint32_t {
+      if (!drop_on) return 0xffffffffu;
+      if (it >= nq) return 0u;
+      const int q = q_start + it * 64 + 32 * half + lane;
+      return kbits[(brow + q) * W + (k0 >> 5) + qd];
+    };
+    uint32_t kw_n = kword(0);
+    for (int it = 0; it < nq; ++it) {
+      const int st = it & 1, qs = it % NS;
+      const int qb = q_start + it * 64;
+      const uint32_t kt = drop_on ? warp_transpose32(kw_n, lane) : 0xffffffffu;
+      kw_n = kword(it + 1);
+      // this tile's -lse·log2e / -rowdot of the half's 32 queries (smem broadcasts)
+      const float* stt = reinterpret_cast<const float*>(smem + C::ST_OFF + qs * 512) + 32 * half;
+      mbar_wait(&qd_full[qs], (it / NS) & 1);  // the stage's stats landed
+      mbar_wait(&sd_full[st], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t rs[32], rp[32];
+      tmem_ld32_nw(tl + C::S_COL + st * 64 + half * 32, rs);
+      tmem_ld32_nw(tl + C::DP_COL + st * 64 + half * 32, rp);
+      tmem_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sd_free[st]);
+      mbar_wait(&w_free[st], ((it >> 1) & 1) ^ 1);
+      const int q0h = qb + 32 * half;
+      const bool full = !(CAUSAL && k0 + 127 > qb);
+      uint32_t pw[16], dw[16];
+      auto pd_loop = [&](auto masked) {
+        constexpr bool kMasked = decltype(masked)::value;
+        const uint64_t sl2x2 = f32x2(sl2, sl2);
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const uint64_t nl2 = *reinterpret_cast<const uint64_t*>(stt + i);
+          const uint64_t nd2 = *reinterpret_cast<const uint64_t*>(stt + 64 + i);
+          float s0, s1;
+          f32x2_split(ffma2(f32x2(__uint_as_float(rs[i]), __uint_as_float(rs[i + 1])), sl2x2, nl2),
+                      s0, s1);
+          float p0 = ex2(s0), p1 = ex2(s1);
+          bool k0b = (kt >> i) & 1u, k1b = (kt >> (i + 1)) & 1u;
+          if constexpr (kMasked) {
+            const bool v0 = !(CAUSAL && key > q0h + i);
+            const bool v1 = !(CAUSAL && key > q0h + i + 1);
+            p0 = v0 ? p0 : 0.f;
+            p1 = v1 ? p1 : 0.f;
+            k0b = k0b && v0;
+            k1b = k1b && v1;
+          }
+          const uint64_t kf2 = f32x2(k0b ? inv_keep : 0.f, k1b ? inv_keep : 0.f);
+          const uint64_t p2 = f32x2(p0, p1);
+          float a0, a1, b0, b1;
+          f32x2_split(fmul2(p2, kf2), a0, a1);
+          f32x2_split(
+              fmul2(p2, ffma2(f32x2(__uint_as_float(rp[i]), __uint_as_float(rp[i + 1])), kf2, nd2)),
+              b0, b1);
+          pw[i >> 1] = pack_bf16(a0, a1);
+          dw[i >> 1] = pack_bf16(b0, b1);
+        }
+      };
+      if (full) pd_loop(std::false_type{});
+      else pd_loop(std::true_type{});
+      // P̃ᵀ as bf16 pairs over the first 16 of this half's (consumed) 32 Sᵀ columns
+      tmem_st16u(tl + C::S_COL + st * 64 + half * 32, pw);
+      // dSᵀ -> smem [128 keys x 64 queries] K-major SW128: this half's queries = chunks 4h..4h+3
+      uint8_t* drow = smem + C::DS_OFF + st * C::DS_BYTES + row * 128;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int phys = (4 * half + u) ^ (row & 7);
+        *reinterpret_cast<uint4*>(drow + phys * 16) =
+            make_uint4(dw[4 * u], dw[4 * u + 1], dw[4 * u + 2], dw[4 * u + 3]);
+      }
+      fence_proxy_async();
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&w_full[st]);
+    }
+    // epilogue: dK·scale, dV -> bf16 (halves take alternate 32-column chunks)
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    bf16* rowp = dqkv + ((int64_t)key * a.b + bj) * a.ld;
+#pragma unroll 1
+    for (int c = half; c < HD / 32; c += 2) {
+      float v[32], w[32];
+      tmem_ld32(tl + C::DK_COL + c * 32, v);
+      tmem_ld32(tl + C::DV_COL + c * 32, w);
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        *reinterpret_cast<uint4*>(rowp + kcol + c * 32 + i) = make_uint4(
+            pack_bf16(v[i] * a.scale, v[i + 1] * a.scale), pack_bf16(v[i + 2] * a.scale, v[i + 3] * a.scale),
+            pack_bf16(v[i + 4] * a.scale, v[i + 5] * a.scale), pack_bf16(v[i + 6] * a.scale, v[i + 7] * a.scale));
+        *reinterpret_cast<uint4*>(rowp + vcol + c * 32 + i) =
+            make_uint4(pack_bf16(w[i], w[i + 1]), pack_bf16(w[i + 2], w[i + 3]),
+                       pack_bf16(w[i + 4], w[i + 5]), pack_bf16(w[i + 6], w[i + 7]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 13) {
+    tc_fence_after();
+    tmem_dealloc_warp(tmem, 512);
+  }
+}
+
+// -lse·log2(e) and -rowdot(dO, O) per (head, batch, query) row, and the dQ accumulator rows
+// zeroed. Rows in memory order of dO / O (token-major), 4 lanes per row (as fa_delta).
+template <int HD>
+__global__ void fa_bwd_prep(AttnArgs a, const bf16* __restrict__ dout) {
+  constexpr int VPL = HD / 32;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = t >> 2;
+  const int sub = (int)(t & 3);
+  const int64_t nrows = a.lh * a.b * a.s;
+  const int64_t hl = r % a.lh, tok = r / a.lh;  // tok = i*b + bj
+  const bf16* o = static_cast<const bf16*>(a.o);
+  float acc = 0.f;
+  const int64_t bj = tok % a.b, i = tok / a.b;
+  const int64_t row = (hl * a.b + bj) * a.s + i;
+  if (r < nrows) {
+    const int64_t off = tok * a.ldo + hl * HD;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const int c = (sub + 4 * v) * 8;
+      const uint4 x = *reinterpret_cast<const uint4*>(dout + off + c);
+      const uint4 y = *reinterpret_cast<const uint4*>(o + off + c);
+      const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        acc += __uint_as_float(xs[k] << 16) * __uint_as_float(ys[k] << 16) +
+               __uint_as_float(xs[k] & 0xffff0000u) * __uint_as_float(ys[k] & 0xffff0000u);
+      float4* z = reinterpret_cast<float4*>(a.dq_acc + row * HD + c);
+      z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  if (sub == 0 && r < nrows) {
+    a.bstat[row] = -a.lse[row] * kLog2e;
+    a.bstat[nrows + row] = -acc;
+  }
+}
+
+// dq_acc·scale -> bf16 into the Q columns of dqkv; rows in dqkv memory order, 8 head_dim
+// elements (two float4 loads, one 16-byte store) per thread.
+template <int HD>
+__global__ void fa_bwd_dq_store(AttnArgs a, bf16* __restrict__ dqkv) {
+  constexpr int VPR = HD / 8;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = t / VPR;
+  const int v = (int)(t % VPR);
+  const int64_t nrows = a.lh * a.b * a.s;
+  if (r >= nrows) return;
+  const int64_t hl = r % a.lh, tok = r / a.lh;
+  const int64_t bj = tok % a.b, i = tok / a.b;
+  const float4* src = reinterpret_cast<const float4*>(a.dq_acc + ((hl * a.b + bj) * a.s + i) * HD + v * 8);
+  const float4 x = src[0], y = src[1];
+  const float sc = a.scale;
+  *reinterpret_cast<uint4*>(dqkv + tok * a.ld + a.qoff + hl * HD + v * 8) =
+      make_uint4(pack_bf16(x.x * sc, x.y * sc), pack_bf16(x.z * sc, x.w * sc),
+                 pack_bf16(y.x * sc, y.y * sc), pack_bf16(y.z * sc, y.w * sc));
+}
+
+template <int HD, bool CAUSAL>
+void launch_fused(const AttnArgs& a, const bf16* dout, bf16* dqkv, cudaStream_t st) {
+  using C = FusedCfg<HD>;
+  static_assert(C::SMEM <= 232448, "fused attention backward: smem over the limit");
+  static bool once = [] {
+    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_fused_umma<HD, CAUSAL>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    return true;
+  }();
+  (void)once;
+  const int64_t rows = a.lh * a.b * a.s;
+  fa_bwd_prep<HD><<<(unsigned)((rows * 4 + 255) / 256), 256, 0, st>>>(a, dout);
+  SPL_CHECK_LAUNCH();
+  const CUtensorMap m128 = attn_seq_map(a.qkv, a.ld, a.b, a.s, a.ld, 128);
+  const CUtensorMap m64 = attn_seq_map(a.qkv, a.ld, a.b, a.s, a.ld, 64);
+  const CUtensorMap d64 = attn_seq_map(dout, a.ldo, a.b, a.s, a.ldo, 64);
+  dim3 grid((unsigned)(a.s / 128), (unsigned)(a.lh * a.b));
+  fa_bwd_fused_umma<HD, CAUSAL><<<grid, 512, C::SMEM, st>>>(m128, m64, d64, a, dqkv);
+  SPL_CHECK_LAUNCH();
+  fa_bwd_dq_store<HD><<<(unsigned)((rows * (HD / 8) + 255) / 256), 256, 0, st>>>(a, dqkv);
+  SPL_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+bool attn_bwd_fused_supported(const AttnArgs& a) {
+  static const bool off = [] {
+    const char* e = std::getenv("SPL_ATTN_DETERMINISTIC");
+    return e != nullptr && e[0] == '1';
+  }();
+  return !off && a.sm == nullptr && a.dq_acc != nullptr && a.bstat != nullptr &&
+         (a.hd == 64 || a.hd == 96) && a.s % 128 == 0 && a.s >= 128 && a.lse != nullptr &&
+         (a.keepbits != nullptr || a.drop.thresh == 0) && a.ld % 8 == 0 && a.ldo % 8 == 0 &&
+         a.qoff % 8 == 0 && ((uintptr_t)a.qkv & 15) == 0 && ((uintptr_t)a.o & 15) == 0 &&
+         ((uintptr_t)a.dq_acc & 15) == 0 && ((uintptr_t)a.bstat & 15) == 0 && a.s < (1 << 30);
+}
+
+void attn_bwd_fused(const AttnArgs& a, const void* dout, void* dqkv, cudaStream_t st) {
+  const bf16* d = static_cast<const bf16*>(dout);
+  bf16* g = static_cast<bf16*>(dqkv);
+  if (a.hd == 64) {
+    if (a.causal) launch_fused<64, true>(a, d, g, st); else launch_fused<64, false>(a, d, g, st);
+  } else {
+    if (a.causal) launch_fused<96, true>(a, d, g, st); else launch_fused<96, false>(a, d, g, st);
+  }
+}
+
+}  // namespace spl::k

@@ -190,6 +190,10 @@ struct AttnArgs {
   uint32_t* keepbits = nullptr;
   int masked_only = 0;  // backward: 1 = every tile through the per-element validity path (A/B)
   int stats_shfl = 0;   // dK/dV: 1 = per-element shuffles for row stats / keep bits (A/B)
+  // fused backward (attn_bwd_fused): fp32 dQ accumulator [lh*b][s][hd] and the per-row
+  // statistics [2][lh*b*s] (-lse·log2 e, -rowdot); transient workspaces
+  float* dq_acc = nullptr;
+  float* bstat = nullptr;
 };
 inline int64_t keepbits_words(int64_t lh, int64_t b, int64_t s) { return lh * b * s * ((s + 31) / 32); }
 // Forward. If a.sm != nullptr the interior is materialised (softmax_out, mask, dropout_out).
@@ -211,5 +215,10 @@ void attn_fwd_umma(const AttnArgs& a, cudaStream_t st);
 bool attn_bwd_umma_supported(const AttnArgs& a);
 void attn_bwd_umma(const AttnArgs& a, const void* dout, void* dqkv, const float* delta,
                    cudaStream_t st);
+// One-kernel backward (dK, dV and dQ from one recomputation; dQ summed over key blocks in an
+// fp32 L2 accumulator): recompute regimes, bf16, head_dim 64/96, s % 128 == 0, workspaces set.
+// SPL_ATTN_DETERMINISTIC=1 turns it off (split kernels, bit-reproducible dQ).
+bool attn_bwd_fused_supported(const AttnArgs& a);
+void attn_bwd_fused(const AttnArgs& a, const void* dout, void* dqkv, cudaStream_t st);
 
 }  // namespace spl::k

@@ -667,6 +667,7 @@ class Layer final : public LayerBase {
       *dqkv = nullptr, *dproj = nullptr, *d_s = nullptr, *dr1 = nullptr, *y_re = nullptr;
     float *delta = nullptr, *partials = nullptr;
     uint32_t* keepbits = nullptr;
+    float *dq_acc = nullptr, *bstat = nullptr;  // fused attention backward workspaces
   };
 
   void validate() {
@@ -736,7 +737,7 @@ class Layer final : public LayerBase {
     const int nch_l = k::num_chunks(RL_, kChunkRows), nch_f = k::num_chunks(RF_, kChunkRows);
     const int64_t npart = std::max<int64_t>(2 * (int64_t)nch_l * h_, nch_f * std::max<int64_t>(3 * lw_, fw_));
     T *yfull = nullptr, *dfull = nullptr, *dgin = nullptr, *dqkv = nullptr, *dproj = nullptr;
-    float *delta = nullptr, *partials = nullptr;
+    float *delta = nullptr, *partials = nullptr, *dq_acc = nullptr, *bstat = nullptr;
     for (int r = 0; r < L_; ++r) {
       Rank& R = R_[r];
       R.wqkv = alloc<T>(h_ * 3 * lw_, kParam, r);
@@ -800,6 +801,17 @@ class Layer final : public LayerBase {
       // side stream at the start of every forward and backward call
       if (std::is_same_v<T, bf16> && d_.dropout_p > 0.0)
         R.keepbits = alloc<uint32_t>(k::keepbits_words(lh_, b_, s_), kWork, r);
+      // fused attention backward (recompute regimes, bf16, head_dim 64/96): fp32 dQ
+      // accumulator and per-row statistics
+      if (std::is_same_v<T, bf16> && kind_ != SPL_RECOMPUTE_NONE && (hd_ == 64 || hd_ == 96) &&
+          s_ % 128 == 0) {
+        if (!dq_acc) {
+          dq_acc = alloc<float>(lh_ * b_ * s_ * hd_, kWork, r);
+          bstat = alloc<float>(2 * lh_ * b_ * s_, kWork, r);
+        }
+        R.dq_acc = dq_acc;
+        R.bstat = bstat;
+      }
       R.dgin = dgin;
       R.dqkv = dqkv;
       R.dproj = dproj;
@@ -944,6 +956,8 @@ class Layer final : public LayerBase {
     a.lse = R.lse;
     a.sm = R.sm; a.mask = R.mask_i; a.sd = R.sd;
     a.keepbits = R.keepbits;
+    a.dq_acc = R.dq_acc;
+    a.bstat = R.bstat;
     return a;
   }
 
