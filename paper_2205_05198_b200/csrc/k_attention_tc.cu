@@ -112,6 +112,54 @@ struct Rng {
 // fmaheavy ran at 89% (ncu) and the all-funnel-shift form is 7% faster (tools/micro/
 // bench_rng2.cu), so keep_fast uses funnel shifts throughout.
 
+// The 32-key word (row base, keys kbeg..kbeg+31; bits at or past s cleared) of one query row.
+template <bool TIE>
+__device__ __forceinline__ uint32_t keep_word(const Rng& rng, uint64_t base, int kbeg, int s,
+                                              uint32_t mixed_lo, uint32_t mixed_hi, uint32_t t_lo,
+                                              uint32_t t_hi, const ShiftMuls& sm) {
+  uint32_t word = 0;
+  const uint64_t bw = base + (uint64_t)kbeg;
+  const uint32_t blo = (uint32_t)bw, bhi = (uint32_t)(bw >> 32);
+  const int kend = kbeg + 32 <= s ? 32 : s - kbeg;
+  if (blo <= 0xffffffffu - 31u) {  // no carry into the high half inside this word
+    const uint32_t hx = bhi ^ (bhi >> 30);
+    const uint32_t hc = hx * 0x1ce4e5b9u;
+    if ((blo >> 30) == ((blo + 31u) >> 30)) {
+      const uint32_t c30 = __funnelshift_r(blo, bhi, 30);
+      if constexpr (TIE) {
+        bool tie = false;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const uint32_t hf = hash_hi<true>(blo + j, bhi, hc, mixed_lo, mixed_hi, sm, c30);
+          if (hf > t_hi) word |= 1u << j;
+          tie |= hf == t_hi;
+        }
+        if (tie) {  // a key's high word equals the threshold's: decide on the low word
+          word = 0;
+#pragma unroll 1
+          for (int j = 0; j < 32; ++j)
+            if (keep_fast<true>(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm, c30))
+              word |= 1u << j;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (keep_fast<true>(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm, c30))
+            word |= 1u << j;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (keep_fast(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm)) word |= 1u << j;
+    }
+  } else {
+#pragma unroll 1
+    for (int j = 0; j < 32; ++j) word |= (rng.keep(base, (uint32_t)(kbeg + j)) ? 1u : 0u) << j;
+  }
+  if (kend < 32) word &= (1u << kend) - 1u;
+  return word;
+}
+
 template <bool TIE>
 __global__ void __launch_bounds__(1024, 1) keep_bits_k(DropKey key, int64_t head_offset, int lh,
                                                    int b, int s, int W, int causal,
@@ -130,52 +178,51 @@ __global__ void __launch_bounds__(1024, 1) keep_bits_k(DropKey key, int64_t head
     uint32_t* out = bits + (int64_t)row * W;
     for (int w = lane; w < W; w += 32) {
       const int kbeg = 32 * w;
-      uint32_t word = 0;
-      if (!(causal && kbeg > q)) {
-        const uint64_t bw = base + (uint64_t)kbeg;
-        const uint32_t blo = (uint32_t)bw, bhi = (uint32_t)(bw >> 32);
-        const int kend = kbeg + 32 <= s ? 32 : s - kbeg;
-        if (blo <= 0xffffffffu - 31u) {  // no carry into the high half inside this word
-          const uint32_t hx = bhi ^ (bhi >> 30);
-          const uint32_t hc = hx * 0x1ce4e5b9u;
-          if ((blo >> 30) == ((blo + 31u) >> 30)) {
-            const uint32_t c30 = __funnelshift_r(blo, bhi, 30);
-            if constexpr (TIE) {
-              bool tie = false;
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const uint32_t hf = hash_hi<true>(blo + j, bhi, hc, mixed_lo, mixed_hi, sm, c30);
-                if (hf > t_hi) word |= 1u << j;
-                tie |= hf == t_hi;
-              }
-              if (tie) {  // a key's high word equals the threshold's: decide on the low word
-                word = 0;
-#pragma unroll 1
-                for (int j = 0; j < 32; ++j)
-                  if (keep_fast<true>(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm,
-                                      c30))
-                    word |= 1u << j;
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (keep_fast<true>(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm, c30))
-                  word |= 1u << j;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (keep_fast(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm)) word |= 1u << j;
-          }
-        } else {
-#pragma unroll 1
-          for (int j = 0; j < 32; ++j)
-            word |= (rng.keep(base, (uint32_t)(kbeg + j)) ? 1u : 0u) << j;
-        }
-        if (kend < 32) word &= (1u << kend) - 1u;
-      }
-      out[w] = word;
+      out[w] = (causal && kbeg > q)
+                   ? 0u
+                   : keep_word<TIE>(rng, base, kbeg, s, mixed_lo, mixed_hi, t_lo, t_hi, sm);
     }
+  }
+}
+
+// Transposed layout for the fused backward (thread = key): bits[((hl*b + bj)*(s/32) + qb)*s + k]
+// bit j = keep(32*qb + j, k). One warp per 32 query rows (lane = row, so every lane hashes its
+// own row's words exactly as keep_bits_k does), each 32 x 32 block transposed across the warp
+// and stored coalesced (lanes = consecutive keys). s % 32 == 0.
+__device__ __forceinline__ uint32_t warp_transpose32_k(uint32_t x, int lane) {
+  uint32_t m = 0x0000ffffu;
+#pragma unroll
+  for (int j = 16; j != 0; j >>= 1, m ^= m << j) {
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+    x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y & m) << j));
+  }
+  return x;
+}
+template <bool TIE>
+__global__ void __launch_bounds__(1024, 1) keep_bits_t_k(DropKey key, int64_t head_offset, int lh,
+                                                     int b, int s, int causal,
+                                                     uint32_t* __restrict__ bits, ShiftMuls sm) {
+  const Rng rng(key);
+  const uint32_t mixed_lo = (uint32_t)rng.mixed, mixed_hi = (uint32_t)(rng.mixed >> 32);
+  const uint32_t t_lo = (uint32_t)rng.tsh, t_hi = (uint32_t)(rng.tsh >> 32);
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int nqb = s / 32, W = s / 32;
+  const int nunits = lh * b * nqb * W;  // (32-row block, key word): fine-grained for balance
+  for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nunits; u += warps) {
+    const int w = u % W;
+    const int blk = u / W;
+    const int qb = blk % nqb;
+    const int t = blk / nqb;
+    const int bj = t % b, hl = t / b;
+    uint32_t word = 0;
+    if (!causal || w <= qb) {  // key words past the block's last query: all masked
+      const int q = 32 * qb + lane;
+      const uint64_t base = rng.row_base(((uint64_t)(head_offset + hl) * b + bj) * s + q, s);
+      word = keep_word<TIE>(rng, base, 32 * w, s, mixed_lo, mixed_hi, t_lo, t_hi, sm);
+      word = warp_transpose32_k(word, lane);
+    }
+    bits[(int64_t)blk * s + 32 * w + lane] = word;
   }
 }
 
@@ -863,14 +910,17 @@ static bool umma_bwd_on(const AttnArgs& a) {
   return !off && attn_bwd_umma_supported(a);
 }
 
+bool attn_bwd_uses_fused(const AttnArgs& a) { return umma_bwd_on(a) && attn_bwd_fused_supported(a); }
+
 template <>
 void attn_bwd_tc<bf16>(const AttnArgs& a, const void* dout, void* dqkv, float* delta,
                        cudaStream_t st) {
   const bool stored = a.sm != nullptr;
-  if (umma_bwd_on(a) && attn_bwd_fused_supported(a)) {
+  if (attn_bwd_uses_fused(a)) {
     attn_bwd_fused(a, dout, dqkv, st);
     return;
   }
+  require(!a.keep_t, "attention backward: transposed keep bits need the fused path");
   if (umma_bwd_on(a)) {  // recompute regimes and (stored interior) the no-recompute regime
     const int64_t rows = a.lh * a.b * a.s;
     SPL_HD_SWITCH(a.hd, fa_delta<HD><<<(unsigned)((rows * 4 + 255) / 256), 256, 0, st>>>(
@@ -909,6 +959,17 @@ void attn_keep_bits(const AttnArgs& a, cudaStream_t st) {
   // interior is materialised — the stored mask carries the raw keep bit at every position,
   // masked or not (mask_slice, block.cpp:392-394)
   const int causal_skip = a.causal && a.sm == nullptr;
+  if (a.keep_t) {  // the fused backward's (key, 32 queries) words
+    require(a.s % 32 == 0, "keep bits (transposed): s % 32 != 0");
+    require(rows / 32 * W < (1ll << 31), "keep bits (transposed): too many words");
+    int64_t gt = (rows / 32 * W + 31) / 32;
+    if (gt > kNumSMs) gt = kNumSMs;
+    auto kt = tie ? keep_bits_t_k<true> : keep_bits_t_k<false>;
+    kt<<<(unsigned)gt, 1024, 0, st>>>(a.drop, a.head_offset, (int)a.lh, (int)a.b, (int)a.s,
+                                      causal_skip, a.keepbits, ShiftMuls{4u, 32u, 2u, 1u});
+    SPL_CHECK_LAUNCH();
+    return;
+  }
   kern<<<(unsigned)grid, 1024, 0, st>>>(a.drop, a.head_offset, (int)a.lh, (int)a.b, (int)a.s, W,
                                         causal_skip, a.keepbits, ShiftMuls{4u, 32u, 2u, 1u});
   SPL_CHECK_LAUNCH();

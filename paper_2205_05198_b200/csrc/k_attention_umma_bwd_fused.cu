@@ -9,7 +9,7 @@
 //   warps Pᵀ = exp2(Sᵀc - lse), keep from the keep bits (transposed per warp),
 //         P̃ᵀ = Pᵀ·keep/(1-p) -> TMEM over the consumed Sᵀ columns (A of a TS-form MMA),
 //         dSᵀ = Pᵀ∘(dPᵀ·keep/(1-p) - rowdot) -> smem, bf16 [128 keys][64 queries] SW128
-//   MMA   dV += P̃ᵀ·dO (TS), dK += dSᵀ·Q (SS, dSᵀ K-major),
+//   MMA   dV += P̃ᵀ·dO, dK += dSᵀ·Q (TS: dSᵀ also written to TMEM over the consumed dPᵀ),
 //         dQᵀ = Kᵀ·dSᵀ (SS: M = head_dim rows padded to 128 read MN-major from the K tile,
 //         B = the same dSᵀ tile read MN-major) -> TMEM (its own 64 columns)
 //   warps dQ readers (one per 32 head_dim rows) add the dQᵀ tile into an fp32 accumulator
@@ -22,9 +22,12 @@
 // bf16 into the Q columns of dqkv.
 //
 // Warp roles (512 threads, 128 registers each):
-//   warps 0-7   softmax-backward elements (TMEM lane quadrant = warp & 3, query half = warp >> 2)
+//   warps 0-7   softmax-backward elements (TMEM lane quadrant = warp & 3; warps 0-3 the even,
+//               4-7 the odd query tiles, in ping-pong)
 //   warps 8-11  dQ readers (TMEM lane quadrant = warp & 3; idle when 32·quadrant >= head_dim)
 //   warp 12     TMA producer; warp 13 TMEM allocator + MMA issuer; warps 14-15 idle
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.hpp"
@@ -66,6 +69,15 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
   return x;
 }
 
+// SPL_ATTN_TRACE=1 (dev A/B): clock64() stamps of one CTA's pipeline events, printed after
+// the first launch — [event][tile]
+__device__ unsigned long long* g_trace = nullptr;
+constexpr int kTraceX = 3, kTraceY = 100;
+#define TRACE(e, it)                                                                         \
+  do {                                                                                       \
+    if (tr != nullptr && (it) < 64) tr[(e) * 64 + (it)] = (unsigned long long)clock64();     \
+  } while (0)
+
 template <int HD>
 struct FusedCfg {
   static_assert(HD == 64 || HD == 96, "fused attention backward: head_dim 64 or 96");
@@ -74,10 +86,12 @@ struct FusedCfg {
   static constexpr int A64 = 64 * 128;          // atom stride of a 64-row tile
   static constexpr int T128 = ATOMS * A128;
   static constexpr int T64 = ATOMS * A64;
-  static constexpr int NS = HD > 64 ? 3 : 4;    // (Q, dO, stats) ring depth
+  // (Q, dO, stats) ring depth (a stage is released when the dV/dK MMAs of its tile complete)
+  static constexpr int NS = HD > 64 ? 3 : 5;
   static constexpr int K_OFF = 0, V_OFF = T128, QD_OFF = 2 * T128;
   static constexpr int ST_OFF = QD_OFF + NS * 2 * T64;          // [NS][-lse·log2e x64][-rowdot x64]
-  static constexpr int DS_OFF = (ST_OFF + NS * 512 + 1023) / 1024 * 1024;  // [2][128 x 64 bf16]
+  // dSᵀ [2 tile parities][128 x 64 bf16]
+  static constexpr int DS_OFF = (ST_OFF + NS * 512 + 1023) / 1024 * 1024;
   static constexpr int DS_BYTES = 128 * 128;
   static constexpr int BAR_OFF = DS_OFF + 2 * DS_BYTES;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
@@ -88,7 +102,7 @@ struct FusedCfg {
   static constexpr int NQW = (HD + 31) / 32;  // dQ reader warps
 };
 
-template <int HD, bool CAUSAL>
+template <int HD, bool CAUSAL, bool KT>
 __global__ void __launch_bounds__(512, 1)
     fa_bwd_fused_umma(const __grid_constant__ CUtensorMap map_kv,  // qkv, 128-row boxes
                       const __grid_constant__ CUtensorMap map_q,   // qkv, 64-row boxes
@@ -132,8 +146,8 @@ __global__ void __launch_bounds__(512, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sd_full[i], 1);
-      mbar_init(&sd_free[i], 8);
-      mbar_init(&w_full[i], 8);
+      mbar_init(&sd_free[i], 4);
+      mbar_init(&w_full[i], 4);
       mbar_init(&w_free[i], 1);
     }
     mbar_init(dq_full, 1);
@@ -146,6 +160,9 @@ __global__ void __launch_bounds__(512, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  unsigned long long* tr =
+      (g_trace != nullptr && blockIdx.x == kTraceX && blockIdx.y == kTraceY) ? g_trace : nullptr;
+  if (threadIdx.x == 0) TRACE(15, 0);
 
   if (warp >= 12) {
     if (warp == 12 && lane == 0) {
@@ -159,6 +176,7 @@ __global__ void __launch_bounds__(512, 1)
       for (int it = 0; it < nq; ++it) {
         const int st = it % NS;
         mbar_wait(&qd_empty[st], ((it / NS) & 1) ^ 1);
+        TRACE(13, it);
         uint8_t* Qt = smem + C::QD_OFF + st * 2 * C::T64;
         uint8_t* Dt = Qt + C::T64;
         float* stt = reinterpret_cast<float*>(smem + C::ST_OFF + st * 512);
@@ -172,8 +190,8 @@ __global__ void __launch_bounds__(512, 1)
         bulk_load(stt, nlse + brow + qb, 256, &qd_full[st]);
         bulk_load(stt + 64, ndel + brow + qb, 256, &qd_full[st]);
       }
-    } else if (warp == 13 && lane == 0) {
-      // ------------------------------------------------ MMA issuer
+    } else if (warp == 13) {
+      // ------------------------------------------------ MMA issuer (whole warp, elected lane)
       constexpr uint32_t idesc_sd = make_idesc(128, 64, false, false);
       constexpr uint32_t idesc_acc = make_idesc(128, HD, false, true);
       constexpr uint32_t idesc_dq = make_idesc(128, 64, true, true);
@@ -181,53 +199,57 @@ __global__ void __launch_bounds__(512, 1)
       mbar_wait(kv_full, 0);
       auto issue_sd = [&](int it) {
         const int sb = it & 1, qs = it % NS;
+        if (lane == 0) TRACE(0, it);
         mbar_wait(&qd_full[qs], (it / NS) & 1);
         mbar_wait(&sd_free[sb], ((it >> 1) & 1) ^ 1);
+        if (lane == 0) TRACE(1, it);
         tc_fence_after();
         const uint32_t qb = smem_u32(smem + C::QD_OFF + qs * 2 * C::T64), db = qb + C::T64;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t oa = (kk >> 2) * C::A128 + (kk & 3) * 32;
           const uint32_t ob = (kk >> 2) * C::A64 + (kk & 3) * 32;
-          umma_bf16(tmem + C::S_COL + sb * 64, smem_desc(ka + oa, 16, 1024),
+          umma_bf16_w(tmem + C::S_COL + sb * 64, smem_desc(ka + oa, 16, 1024),
                     smem_desc(qb + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
-          umma_bf16(tmem + C::DP_COL + sb * 64, smem_desc(va + oa, 16, 1024),
+          umma_bf16_w(tmem + C::DP_COL + sb * 64, smem_desc(va + oa, 16, 1024),
                     smem_desc(db + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
         }
-        umma_commit(&sd_full[sb]);
+        umma_commit_w(&sd_full[sb]);
       };
       if (nq > 0) issue_sd(0);
       for (int it = 0; it < nq; ++it) {
         if (it + 1 < nq) issue_sd(it + 1);
         const int st = it & 1, qs = it % NS;
         mbar_wait(&w_full[st], (it >> 1) & 1);
+        if (lane == 0) TRACE(2, it);
         tc_fence_after();
         const uint32_t dsw = smem_u32(smem + C::DS_OFF + st * C::DS_BYTES);
         const uint32_t qb = smem_u32(smem + C::QD_OFF + qs * 2 * C::T64), db = qb + C::T64;
 #pragma unroll
         for (int kk = 0; kk < 64 / 16; ++kk) {
-          // dV += P̃ᵀ·dO (A: P̃ᵀ in TMEM, queries 32h.. of half h at columns 32h..+16);
-          // dK += dSᵀ·Q (A: dSᵀ smem, K-major)
+          // dV += P̃ᵀ·dO, dK += dSᵀ·Q (A: P̃ᵀ / dSᵀ in TMEM, queries 32h.. of half h at
+          // columns 32h..+16)
           const uint64_t bdo = smem_desc(db + kk * 2048, C::A64, 1024);
           const uint64_t bq = smem_desc(qb + kk * 2048, C::A64, 1024);
           const uint32_t col = (uint32_t)(st * 64 + (kk >> 1) * 32 + (kk & 1) * 8);
-          umma_bf16_ts(tmem + C::DV_COL, tmem + C::S_COL + col, bdo, idesc_acc, (it | kk) != 0 ? 1u : 0u);
-          umma_bf16(tmem + C::DK_COL, smem_desc(dsw + kk * 32, 16, 1024), bq, idesc_acc,
-                    (it | kk) != 0 ? 1u : 0u);
+          umma_bf16_ts_w(tmem + C::DV_COL, tmem + C::S_COL + col, bdo, idesc_acc, (it | kk) != 0 ? 1u : 0u);
+          umma_bf16_ts_w(tmem + C::DK_COL, tmem + C::DP_COL + col, bq, idesc_acc, (it | kk) != 0 ? 1u : 0u);
         }
+        umma_commit_w(&qd_empty[qs]);  // the stage's Q / dO are read by now
         // dQᵀ = Kᵀ·dSᵀ: K = the CTA's 128 keys in 8 steps of 16 rows; A = K tile MN-major
         // (head_dim rows, padded to M = 128), B = dSᵀ MN-major (queries contiguous)
         mbar_wait(dq_free, ((it & 1) ^ 1));
+        if (lane == 0) TRACE(3, it);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk)
-          umma_bf16(tmem + C::DQ_COL, smem_desc(ka + kk * 2048, C::A128, 1024),
+          umma_bf16_w(tmem + C::DQ_COL, smem_desc(ka + kk * 2048, C::A128, 1024),
                     smem_desc(dsw + kk * 2048, 8192, 1024), idesc_dq, kk > 0 ? 1u : 0u);
-        umma_commit(&w_free[st]);
-        umma_commit(&qd_empty[qs]);
-        umma_commit(dq_full);
+        umma_commit_w(&w_free[st]);
+        umma_commit_w(dq_full);
+        if (lane == 0) TRACE(4, it);
       }
-      umma_commit(acc_full);
+      umma_commit_w(acc_full);
     }
   } else if (warp >= 8) {
     // ------------------------------------------------ dQ readers
@@ -238,11 +260,13 @@ __global__ void __launch_bounds__(512, 1)
       float* accp = a.dq_acc + (brow + q_start) * HD + row;
       for (int it = 0; it < nq; ++it) {
         mbar_wait(dq_full, it & 1);
+        if (lane == 0 && qd == 0) TRACE(10, it);
         tc_fence_after();
         uint32_t v0[32], v1[32];
         tmem_ld32_nw(tl, v0);
         tmem_ld32_nw(tl + 32, v1);
         tmem_wait();
+        if (lane == 0 && qd == 0) TRACE(11, it);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(dq_free);
@@ -255,12 +279,17 @@ __global__ void __launch_bounds__(512, 1)
           for (int c = 0; c < 32; ++c)
             asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p + (32 + c) * HD), "f"(__uint_as_float(v1[c])) : "memory");
         }
+        if (lane == 0 && qd == 0) TRACE(12, it);
       }
     }
   } else {
     // ------------------------------------------------ softmax-backward warps
+    // Two warpgroups in ping-pong: warps 0-3 take the even query tiles (Sᵀ/dPᵀ buffer 0),
+    // warps 4-7 the odd ones (buffer 1), each warp all 64 queries of its key row in two
+    // 32-query halves — so one group's TMEM loads (64 KB of fp32 Sᵀ/dPᵀ per tile, the TMEM
+    // read port is the narrowest resource) overlap the other group's element work.
     const int qd = warp & 3;
-    const int half = warp >> 2;       // query columns 32*half .. +31 of each 64-query tile
+    const int wg = warp >> 2;         // tile parity
     const int row = qd * 32 + lane;   // key row
     const int key = k0 + row;
     const uint32_t tl = tmem + ((uint32_t)(qd * 32) << 16);
@@ -269,90 +298,117 @@ __global__ void __launch_bounds__(512, 1)
     const bool drop_on = a.drop.thresh != 0;
     const int W = S / 32;
     const uint32_t* kbits = a.keepbits;
-    // keep-bit word (query qb + 32*half + lane, this warp's 32 keys), one tile ahead
-    auto kword = [&](int it) -> uint32_t {
+    // keep bits of (this key, the 32 queries of half h of tile it): KT reads the transposed
+    // layout directly; otherwise each lane loads (its query, the warp's 32 keys) and the warp
+    // transposes the 32 x 32 block. Loaded one own tile ahead.
+    auto kword = [&](int it, int h) -> uint32_t {
       if (!drop_on) return 0xffffffffu;
       if (it >= nq) return 0u;
-      const int q = q_start + it * 64 + 32 * half + lane;
-      return kbits[(brow + q) * W + (k0 >> 5) + qd];
+      const int qw = (q_start + it * 64 + 32 * h) >> 5;
+      if constexpr (KT) return kbits[((int64_t)hb * (S >> 5) + qw) * S + key];
+      return kbits[(brow + 32 * qw + lane) * W + (k0 >> 5) + qd];
     };
-    uint32_t kw_n = kword(0);
-    for (int it = 0; it < nq; ++it) {
-      const int st = it & 1, qs = it % NS;
+    uint32_t kw0 = kword(wg, 0), kw1 = kword(wg, 1);
+    for (int it = wg; it < nq; it += 2) {
+      const int sb = wg, qs = it % NS;
       const int qb = q_start + it * 64;
-      const uint32_t kt = drop_on ? warp_transpose32(kw_n, lane) : 0xffffffffu;
-      kw_n = kword(it + 1);
-      // this tile's -lse·log2e / -rowdot of the half's 32 queries (smem broadcasts)
-      const float* stt = reinterpret_cast<const float*>(smem + C::ST_OFF + qs * 512) + 32 * half;
+      const uint32_t kt0 = (KT || !drop_on) ? kw0 : warp_transpose32(kw0, lane);
+      const uint32_t kt1 = (KT || !drop_on) ? kw1 : warp_transpose32(kw1, lane);
+      kw0 = kword(it + 2, 0);
+      kw1 = kword(it + 2, 1);
+      const float* stt = reinterpret_cast<const float*>(smem + C::ST_OFF + qs * 512);
       mbar_wait(&qd_full[qs], (it / NS) & 1);  // the stage's stats landed
-      mbar_wait(&sd_full[st], (it >> 1) & 1);
+      mbar_wait(&sd_full[sb], (it >> 1) & 1);
+      // tile it-2's MMAs complete: this parity's dSᵀ buffer and the P̃ᵀ columns of its Sᵀ
+      // buffer are free
+      mbar_wait(&w_free[sb], ((it >> 1) & 1) ^ 1);
+      const bool trw = lane == 0 && qd == 0;
+      if (trw) TRACE(5, it);
       tc_fence_after();
-      uint32_t rs[32], rp[32];
-      tmem_ld32_nw(tl + C::S_COL + st * 64 + half * 32, rs);
-      tmem_ld32_nw(tl + C::DP_COL + st * 64 + half * 32, rp);
-      tmem_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sd_free[st]);
-      mbar_wait(&w_free[st], ((it >> 1) & 1) ^ 1);
-      const int q0h = qb + 32 * half;
       const bool full = !(CAUSAL && k0 + 127 > qb);
-      uint32_t pw[16], dw[16];
-      auto pd_loop = [&](auto masked) {
-        constexpr bool kMasked = decltype(masked)::value;
-        const uint64_t sl2x2 = f32x2(sl2, sl2);
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const uint64_t nl2 = *reinterpret_cast<const uint64_t*>(stt + i);
-          const uint64_t nd2 = *reinterpret_cast<const uint64_t*>(stt + 64 + i);
-          float s0, s1;
-          f32x2_split(ffma2(f32x2(__uint_as_float(rs[i]), __uint_as_float(rs[i + 1])), sl2x2, nl2),
-                      s0, s1);
-          float p0 = ex2(s0), p1 = ex2(s1);
-          bool k0b = (kt >> i) & 1u, k1b = (kt >> (i + 1)) & 1u;
-          if constexpr (kMasked) {
-            const bool v0 = !(CAUSAL && key > q0h + i);
-            const bool v1 = !(CAUSAL && key > q0h + i + 1);
-            p0 = v0 ? p0 : 0.f;
-            p1 = v1 ? p1 : 0.f;
-            k0b = k0b && v0;
-            k1b = k1b && v1;
-          }
-          const uint64_t kf2 = f32x2(k0b ? inv_keep : 0.f, k1b ? inv_keep : 0.f);
-          const uint64_t p2 = f32x2(p0, p1);
-          float a0, a1, b0, b1;
-          f32x2_split(fmul2(p2, kf2), a0, a1);
-          f32x2_split(
-              fmul2(p2, ffma2(f32x2(__uint_as_float(rp[i]), __uint_as_float(rp[i + 1])), kf2, nd2)),
-              b0, b1);
-          pw[i >> 1] = pack_bf16(a0, a1);
-          dw[i >> 1] = pack_bf16(b0, b1);
+      uint8_t* drow = smem + C::DS_OFF + sb * C::DS_BYTES + row * 128;
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        uint32_t rs[32], rp[32];
+        tmem_ld32_nw(tl + C::S_COL + sb * 64 + h * 32, rs);
+        tmem_ld32_nw(tl + C::DP_COL + sb * 64 + h * 32, rp);
+        tmem_wait();
+        if (trw) TRACE(h ? 8 : 6, it);
+        if (h == 1) {  // both halves of Sᵀ/dPᵀ are in registers (P̃ᵀ still goes to TMEM below)
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sd_free[sb]);
         }
-      };
-      if (full) pd_loop(std::false_type{});
-      else pd_loop(std::true_type{});
-      // P̃ᵀ as bf16 pairs over the first 16 of this half's (consumed) 32 Sᵀ columns
-      tmem_st16u(tl + C::S_COL + st * 64 + half * 32, pw);
-      // dSᵀ -> smem [128 keys x 64 queries] K-major SW128: this half's queries = chunks 4h..4h+3
-      uint8_t* drow = smem + C::DS_OFF + st * C::DS_BYTES + row * 128;
+        const uint32_t kt = h ? kt1 : kt0;
+        const uint32_t sth_s = smem_u32(stt + 32 * h);
+        const int q0h = qb + 32 * h;
+        uint32_t pw[16], dw[16];
+        auto pd_loop = [&](auto masked) {
+          constexpr bool kMasked = decltype(masked)::value;
+          const uint64_t sl2x2 = f32x2(sl2, sl2);
+          uint32_t l4[4], d4[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int phys = (4 * half + u) ^ (row & 7);
-        *reinterpret_cast<uint4*>(drow + phys * 16) =
-            make_uint4(dw[4 * u], dw[4 * u + 1], dw[4 * u + 2], dw[4 * u + 3]);
+          for (int i = 0; i < 32; i += 2) {
+            if ((i & 3) == 0) {  // 4 queries' statistics per 16-byte shared load (broadcast)
+              asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(l4[0]), "=r"(l4[1]), "=r"(l4[2]), "=r"(l4[3]) : "r"(sth_s + 4 * i));
+              asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(d4[0]), "=r"(d4[1]), "=r"(d4[2]), "=r"(d4[3]) : "r"(sth_s + 256 + 4 * i));
+            }
+            const uint64_t nl2 = ((uint64_t)l4[(i & 3) + 1] << 32) | l4[i & 3];
+            const uint64_t nd2 = ((uint64_t)d4[(i & 3) + 1] << 32) | d4[i & 3];
+            float s0, s1;
+            f32x2_split(ffma2(f32x2(__uint_as_float(rs[i]), __uint_as_float(rs[i + 1])), sl2x2, nl2),
+                        s0, s1);
+            float p0 = ex2(s0), p1 = ex2(s1);
+            bool k0b = (kt >> i) & 1u, k1b = (kt >> (i + 1)) & 1u;
+            if constexpr (kMasked) {
+              const bool v0 = !(CAUSAL && key > q0h + i);
+              const bool v1 = !(CAUSAL && key > q0h + i + 1);
+              p0 = v0 ? p0 : 0.f;
+              p1 = v1 ? p1 : 0.f;
+              k0b = k0b && v0;
+              k1b = k1b && v1;
+            }
+            const uint64_t kf2 = f32x2(k0b ? inv_keep : 0.f, k1b ? inv_keep : 0.f);
+            const uint64_t p2 = f32x2(p0, p1);
+            float a0, a1, b0, b1;
+            f32x2_split(fmul2(p2, kf2), a0, a1);
+            f32x2_split(
+                fmul2(p2, ffma2(f32x2(__uint_as_float(rp[i]), __uint_as_float(rp[i + 1])), kf2, nd2)),
+                b0, b1);
+            pw[i >> 1] = pack_bf16(a0, a1);
+            dw[i >> 1] = pack_bf16(b0, b1);
+          }
+        };
+        if (full) pd_loop(std::false_type{});
+        else pd_loop(std::true_type{});
+        if (trw && h == 0) TRACE(7, it);
+        // P̃ᵀ / dSᵀ as bf16 pairs over the first 16 of this half's (consumed) 32 Sᵀ / dPᵀ
+        // columns (A operands of the TS-form dV / dK MMAs)
+        tmem_st16u(tl + C::S_COL + sb * 64 + h * 32, pw);
+        tmem_st16u(tl + C::DP_COL + sb * 64 + h * 32, dw);
+        // dSᵀ -> smem [128 keys x 64 queries] K-major SW128: half h's queries = chunks 4h..4h+3
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int phys = (4 * h + u) ^ (row & 7);
+          *reinterpret_cast<uint4*>(drow + phys * 16) =
+              make_uint4(dw[4 * u], dw[4 * u + 1], dw[4 * u + 2], dw[4 * u + 3]);
+        }
       }
       fence_proxy_async();
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&w_full[st]);
+      if (lane == 0) mbar_arrive(&w_full[sb]);
+      if (trw) TRACE(9, it);
     }
-    // epilogue: dK·scale, dV -> bf16 (halves take alternate 32-column chunks)
+    // epilogue: dK·scale, dV -> bf16 (the warpgroups take alternate 32-column chunks)
     mbar_wait(acc_full, 0);
     tc_fence_after();
     bf16* rowp = dqkv + ((int64_t)key * a.b + bj) * a.ld;
 #pragma unroll 1
-    for (int c = half; c < HD / 32; c += 2) {
+    for (int c = wg; c < HD / 32; c += 2) {
       float v[32], w[32];
       tmem_ld32(tl + C::DK_COL + c * 32, v);
       tmem_ld32(tl + C::DV_COL + c * 32, w);
@@ -434,12 +490,12 @@ __global__ void fa_bwd_dq_store(AttnArgs a, bf16* __restrict__ dqkv) {
                  pack_bf16(y.x * sc, y.y * sc), pack_bf16(y.z * sc, y.w * sc));
 }
 
-template <int HD, bool CAUSAL>
+template <int HD, bool CAUSAL, bool KT>
 void launch_fused(const AttnArgs& a, const bf16* dout, bf16* dqkv, cudaStream_t st) {
   using C = FusedCfg<HD>;
   static_assert(C::SMEM <= 232448, "fused attention backward: smem over the limit");
   static bool once = [] {
-    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_fused_umma<HD, CAUSAL>,
+    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_fused_umma<HD, CAUSAL, KT>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     return true;
   }();
@@ -451,8 +507,34 @@ void launch_fused(const AttnArgs& a, const bf16* dout, bf16* dqkv, cudaStream_t 
   const CUtensorMap m64 = attn_seq_map(a.qkv, a.ld, a.b, a.s, a.ld, 64);
   const CUtensorMap d64 = attn_seq_map(dout, a.ldo, a.b, a.s, a.ldo, 64);
   dim3 grid((unsigned)(a.s / 128), (unsigned)(a.lh * a.b));
-  fa_bwd_fused_umma<HD, CAUSAL><<<grid, 512, C::SMEM, st>>>(m128, m64, d64, a, dqkv);
+  static unsigned long long* trace = [] {
+    const char* e = std::getenv("SPL_ATTN_TRACE");
+    unsigned long long* p = nullptr;
+    if (e != nullptr && e[0] == '1') {
+      SPL_CUDA(cudaMalloc(&p, 16 * 64 * 8));
+      SPL_CUDA(cudaMemset(p, 0, 16 * 64 * 8));
+      SPL_CUDA(cudaMemcpyToSymbol(g_trace, &p, sizeof p));
+    }
+    return p;
+  }();
+  fa_bwd_fused_umma<HD, CAUSAL, KT><<<grid, 512, C::SMEM, st>>>(m128, m64, d64, a, dqkv);
   SPL_CHECK_LAUNCH();
+  static int traced = 0;
+  if (trace != nullptr && traced++ == 2 && grid.x > kTraceX && grid.y > kTraceY) {
+    unsigned long long h[16 * 64];
+    SPL_CUDA(cudaStreamSynchronize(st));
+    SPL_CUDA(cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost));
+    const unsigned long long t0 = h[15 * 64];
+    fprintf(stderr, "fused bwd trace (cycles from CTA start), columns: tile, mma[issue_sd wait-start, "
+                    "sd issued, w_full seen, dq_free seen, end], sm[ready, ld0, cmp0, ld1, w_full], "
+                    "rd[dq_full, ld, reds], tma[empty]\n");
+    for (int it = 0; it < 32; ++it) {
+      fprintf(stderr, "%2d", it);
+      for (int e : {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13})
+        fprintf(stderr, " %7lld", h[e * 64 + it] ? (long long)(h[e * 64 + it] - t0) : -1ll);
+      fprintf(stderr, "\n");
+    }
+  }
   fa_bwd_dq_store<HD><<<(unsigned)((rows * (HD / 8) + 255) / 256), 256, 0, st>>>(a, dqkv);
   SPL_CHECK_LAUNCH();
 }
@@ -474,11 +556,20 @@ bool attn_bwd_fused_supported(const AttnArgs& a) {
 void attn_bwd_fused(const AttnArgs& a, const void* dout, void* dqkv, cudaStream_t st) {
   const bf16* d = static_cast<const bf16*>(dout);
   bf16* g = static_cast<bf16*>(dqkv);
-  if (a.hd == 64) {
-    if (a.causal) launch_fused<64, true>(a, d, g, st); else launch_fused<64, false>(a, d, g, st);
-  } else {
-    if (a.causal) launch_fused<96, true>(a, d, g, st); else launch_fused<96, false>(a, d, g, st);
+#define SPL_FUSED_CASE(HDX)                                                              \
+  if (a.keep_t) {                                                                        \
+    if (a.causal) launch_fused<HDX, true, true>(a, d, g, st);                            \
+    else launch_fused<HDX, false, true>(a, d, g, st);                                    \
+  } else {                                                                               \
+    if (a.causal) launch_fused<HDX, true, false>(a, d, g, st);                           \
+    else launch_fused<HDX, false, false>(a, d, g, st);                                   \
   }
+  if (a.hd == 64) {
+    SPL_FUSED_CASE(64)
+  } else {
+    SPL_FUSED_CASE(96)
+  }
+#undef SPL_FUSED_CASE
 }
 
 }  // namespace spl::k

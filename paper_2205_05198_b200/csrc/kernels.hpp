@@ -194,6 +194,9 @@ struct AttnArgs {
   // statistics [2][lh*b*s] (-lse·log2 e, -rowdot); transient workspaces
   float* dq_acc = nullptr;
   float* bstat = nullptr;
+  // keep bits in the transposed layout [lh*b][s/32][s] (word = one key x 32 queries), filled by
+  // attn_keep_bits for and read by the fused backward; else [lh*b*s][ceil(s/32)]
+  int keep_t = 0;
 };
 inline int64_t keepbits_words(int64_t lh, int64_t b, int64_t s) { return lh * b * s * ((s + 31) / 32); }
 // Forward. If a.sm != nullptr the interior is materialised (softmax_out, mask, dropout_out).
@@ -219,6 +222,9 @@ void attn_bwd_umma(const AttnArgs& a, const void* dout, void* dqkv, const float*
 // fp32 L2 accumulator): recompute regimes, bf16, head_dim 64/96, s % 128 == 0, workspaces set.
 // SPL_ATTN_DETERMINISTIC=1 turns it off (split kernels, bit-reproducible dQ).
 bool attn_bwd_fused_supported(const AttnArgs& a);
+// Whether attn_bwd<bf16> takes the fused path for these arguments (the layer fills the
+// backward's keep bits in the transposed layout exactly when it does).
+bool attn_bwd_uses_fused(const AttnArgs& a);
 void attn_bwd_fused(const AttnArgs& a, const void* dout, void* dqkv, cudaStream_t st);
 
 }  // namespace spl::k

@@ -669,6 +669,16 @@ class Layer final : public LayerBase {
     uint32_t* keepbits = nullptr;
     float *dq_acc = nullptr, *bstat = nullptr;  // fused attention backward workspaces
   };
+  bool bits_t_ = false;  // keep bits currently in the transposed (fused backward) layout
+  // SPL_KEEPBITS_T=1: the selective backward's keep bits in the transposed layout (the RNG
+  // pass stores (key, 32 queries) words; the fused kernel skips its per-tile warp transposes)
+  static bool keep_bits_t_env() {
+    static const bool on = [] {
+      const char* e = std::getenv("SPL_KEEPBITS_T");
+      return e != nullptr && e[0] == '1';
+    }();
+    return on;
+  }
 
   void validate() {
     require(t_ >= 1, "t must be >= 1");
@@ -958,6 +968,7 @@ class Layer final : public LayerBase {
     a.keepbits = R.keepbits;
     a.dq_acc = R.dq_acc;
     a.bstat = R.bstat;
+    a.keep_t = bits_t_ ? 1 : 0;
     return a;
   }
 
@@ -1096,8 +1107,15 @@ class Layer final : public LayerBase {
 
   // Fork the data-independent dropout-mask RNG onto the side stream (it overlaps the GEMMs
   // that precede attention); join() makes the main stream wait for it.
-  void fork_keep_bits() {
+  // transposed: the backward's bits for the fused attention backward (k::attn_bwd_uses_fused)
+  void fork_keep_bits(bool transposed = false) {
     if (R_.empty() || R_[0].keepbits == nullptr) return;
+    bits_t_ = false;
+    if (transposed) {
+      k::AttnArgs a0 = attn_args(0);
+      a0.keep_t = 1;
+      bits_t_ = k::attn_bwd_uses_fused(a0);
+    }
     if (bits_serial_) {  // on the main stream, right before its consumer
       for (int r = 0; r < L_; ++r) {
         k::AttnArgs a = attn_args(r);
@@ -1212,7 +1230,7 @@ class Layer final : public LayerBase {
     const int64_t h = h_;
     // recompute regimes regenerate the keep bits (full recomputation just re-ran the forward,
     // whose bits are still in the buffer); the no-recompute regime reads the stored mask
-    if (kind_ == SPL_RECOMPUTE_SELECTIVE) fork_keep_bits();
+    if (kind_ == SPL_RECOMPUTE_SELECTIVE) fork_keep_bits(keep_bits_t_env());
     const double eb = sizeof(T);
     const int nch_l = k::num_chunks(RL_, kChunkRows), nch_f = k::num_chunks(RF_, kChunkRows);
     const float inv_keep = k_mlp_.inv_keep;
