@@ -635,6 +635,7 @@ bool attn_fwd_umma_supported(const AttnArgs& a) {
 }
 
 void attn_fwd_umma(const AttnArgs& a, cudaStream_t st) {
+  if (attn_fwd_pp_supported(a)) return attn_fwd_pp(a, st);
   switch (a.hd) {
     case 64: return launch_fwd_umma_hd<64>(a, st);
     case 96: return launch_fwd_umma_hd<96>(a, st);

@@ -213,6 +213,10 @@ void attn_keep_bits(const AttnArgs& a, cudaStream_t st);
 // no-recompute regime writes the stored interior); used by attn_fwd<bf16>.
 bool attn_fwd_umma_supported(const AttnArgs& a);
 void attn_fwd_umma(const AttnArgs& a, cudaStream_t st);
+// Recompute-regime forward with two query tiles per CTA in ping-pong (k_attention_fwd_pp.cu);
+// attn_fwd_umma dispatches to it when supported (SPL_ATTN_FWD_PP=0: off).
+bool attn_fwd_pp_supported(const AttnArgs& a);
+void attn_fwd_pp(const AttnArgs& a, cudaStream_t st);
 // tcgen05/TMEM backward (recompute regimes: keep bits from attn_keep_bits; no-recompute: the
 // stored interior). delta = rowdot(dO, O) must be computed first.
 bool attn_bwd_umma_supported(const AttnArgs& a);

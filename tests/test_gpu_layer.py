@@ -305,6 +305,10 @@ def test_facade_reference_api(spl, orc):
     (dict(heads=8, hidden=1024, seq=192, batch=1), 2, True),    # head_dim 128 (175B), s tail
     (dict(heads=8, hidden=1280, seq=256, batch=1), 2, False),   # head_dim 160 (530B / 1T)
     (dict(heads=4, hidden=256, seq=160, batch=3), 1, True),     # head_dim 64, s tail
+    # s % 128 == 0: the two-tile ping-pong forward (k_attention_fwd_pp.cu), causal diagonal
+    # tiles in both query tiles and a CTA whose second tile is empty (s = 384)
+    (dict(heads=4, hidden=512, seq=384, batch=1), 1, True),     # head_dim 128
+    (dict(heads=8, hidden=512, seq=256, batch=2), 2, True),     # head_dim 64
 ])
 @pytest.mark.parametrize("recompute", ["selective", "none"])
 def test_bf16_head_dims(spl, orc, shape, t, causal, recompute):
