@@ -264,6 +264,12 @@ int spl_profile_read(spl_handle* h, double ms[5], int64_t launches[5], double fl
                      double bytes[5]);
 /* Number of kernel launches of this library recorded since the last reset. */
 int spl_launch_count(spl_handle* h, int64_t* count, int reset);
+/* Which collective paths the handle runs: out[0] = 1 when the reduce-scatters
+ * are fused into the row-parallel GEMMs (peer landing slots); out[1] = 1 when the all-gathers
+ * are fused into the consuming GEMMs reading the simulated ranks' shards, 2 when those GEMMs
+ * pull the shards from the peer ranks' memory (CUDA IPC / NVLink), 0 when gathered copies
+ * are materialised. */
+int spl_comm_paths(const spl_handle* h, int out[2]);
 
 /* Kernel-level entry (tests / microbenchmarks): C[M,N] = A[M,K]·B[K,N] in bf16 with fp32
  * accumulation on the layer's GEMM kernels. A(m,k) = A[m*lda+k] (a_mn=0) or A[k*lda+m]

@@ -98,6 +98,7 @@ def lib():
         "spl_profile_enable": (I32, [H, I32]),
         "spl_profile_read": (I32, [H, P(D), P(I64), P(D), P(D)]),
         "spl_launch_count": (I32, [H, P(I64), I32]),
+        "spl_comm_paths": (I32, [H, P(I32)]),
         "spl_set_graphs": (I32, [H, I32]),
         "spl_layer_component_breakdown": (I32, [I64, I64, I64, I64, I64, I64, P(I64)]),
         "spl_percent_of_baseline": (I32, [I64, I64, I64, I64, I64, I32, I32, I64, I64, P(I64), P(I64)]),

@@ -657,6 +657,14 @@ int spl_launch_count(spl_handle* h, int64_t* count, int reset) {
   });
 }
 
+int spl_comm_paths(const spl_handle* h, int out[2]) {
+  return guard([&] {
+    check_handle(h);
+    if (out == nullptr) throw std::invalid_argument("null output");
+    h->layer->comm_paths(out);
+  });
+}
+
 int spl_set_graphs(spl_handle* h, int on) {
   return guard([&] {
     check_handle(h);

@@ -1,4 +1,8 @@
+#include <cuda.h>
+
 #include <cstring>
+#include <map>
+#include <utility>
 
 #include "comm.hpp"
 #include "kernels.hpp"
@@ -27,6 +31,53 @@ inline int grid_for(int64_t n) {
   if (g > kNumSMs * 16) g = kNumSMs * 16;
   return (int)(g < 1 ? 1 : g);
 }
+
+// ---------------------------------------------------------------- peer address exchange
+// A buffer is named to the peers by (IPC handle of its allocation, offset): layer buffers may
+// live inside a pooled allocation (stack workspaces), and CUDA IPC exports whole allocations.
+struct PeerEntry {
+  cudaIpcMemHandle_t handle;
+  uint64_t offset;
+};
+PeerEntry peer_entry(const void* p) {
+  using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static RangeFn range = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SPL_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+    if (f == nullptr || q != cudaDriverEntryPointSuccess) raise(3, "cuMemGetAddressRange unavailable");
+    return reinterpret_cast<RangeFn>(f);
+  }();
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)p) != CUDA_SUCCESS) raise(3, "cuMemGetAddressRange failed");
+  PeerEntry e;
+  SPL_CUDA(cudaIpcGetMemHandle(&e.handle, (void*)base));
+  e.offset = (uint64_t)((CUdeviceptr)p - base);
+  return e;
+}
+// Opened peer allocations, one mapping per (peer, allocation) for the process's lifetime
+// (closed when the transport is destroyed).
+class PeerMaps {
+ public:
+  const void* open(int q, const PeerEntry& e) {
+    std::string key(reinterpret_cast<const char*>(&e.handle), sizeof e.handle);
+    key += std::to_string(q);
+    auto it = maps_.find(key);
+    if (it == maps_.end()) {
+      void* p = nullptr;
+      SPL_CUDA(cudaIpcOpenMemHandle(&p, e.handle, cudaIpcMemLazyEnablePeerAccess));
+      it = maps_.emplace(std::move(key), p).first;
+    }
+    return static_cast<const char*>(it->second) + e.offset;
+  }
+  ~PeerMaps() {
+    for (auto& kv : maps_) cudaIpcCloseMemHandle(kv.second);
+  }
+
+ private:
+  std::map<std::string, void*> maps_;
+};
 
 // ---------------------------------------------------------------- peer-memory protocol kernels
 __device__ __forceinline__ uint32_t ld_acq_sys(const uint32_t* p) {
@@ -294,6 +345,7 @@ class NcclComm final : public Comm {
     if (slots_) cudaFree(slots_);
     if (flags_) cudaFree(flags_);
     if (err_) cudaFree(err_);
+    if (bar_) cudaFree(bar_);
     if (comm_) ncclCommDestroy(comm_);
   }
 
@@ -359,6 +411,28 @@ class NcclComm final : public Comm {
     p2p_ready_k<<<1, 32, 0, st>>>(g, a, t_, err_);
     SPL_CHECK_LAUNCH();
   }
+  bool p2p_map(const void* mine, std::vector<const void*>& all) override {
+    const PeerEntry e = peer_entry(mine);
+    char* dev = nullptr;
+    SPL_CUDA(cudaMalloc(&dev, sizeof(PeerEntry) * (t_ + 1)));
+    SPL_CUDA(cudaMemcpy(dev + sizeof(PeerEntry) * t_, &e, sizeof e, cudaMemcpyHostToDevice));
+    SPL_NCCL(ncclAllGather(dev + sizeof(PeerEntry) * t_, dev, sizeof(PeerEntry), ncclUint8, comm_, 0));
+    SPL_CUDA(cudaStreamSynchronize(0));
+    std::vector<PeerEntry> ents(t_);
+    SPL_CUDA(cudaMemcpy(ents.data(), dev, sizeof(PeerEntry) * t_, cudaMemcpyDeviceToHost));
+    SPL_CUDA(cudaFree(dev));
+    all.assign(t_, nullptr);
+    for (int q = 0; q < t_; ++q) all[q] = q == rank0_ ? mine : maps_.open(q, ents[q]);
+    return true;
+  }
+  // NCCL has no barrier; a one-element all-reduce completes only once every rank reached it
+  void p2p_barrier(cudaStream_t st) override {
+    if (bar_ == nullptr) {
+      SPL_CUDA(cudaMalloc(&bar_, sizeof(float)));
+      SPL_CUDA(cudaMemset(bar_, 0, sizeof(float)));
+    }
+    SPL_NCCL(ncclAllReduce(bar_, bar_, 1, ncclFloat32, ncclSum, comm_, st));
+  }
   void all_gather(const void* const* shard, void* const* full, int64_t n, DType dt,
                   cudaStream_t st) override {
     SPL_NCCL(ncclAllGather(shard[0], full[0], (size_t)n, nccl_type(dt), comm_, st));
@@ -376,6 +450,8 @@ class NcclComm final : public Comm {
 
  private:
   ncclComm_t comm_ = nullptr;
+  PeerMaps maps_;
+  float* bar_ = nullptr;
   int* err_ = nullptr;
   void* slots_ = nullptr;
   void* flags_ = nullptr;
@@ -449,6 +525,31 @@ class IpcComm final : public Comm {
   }
   bool serial_order() const override { return true; }
   bool p2p_default() const override { return true; }
+  bool pull_default() const override { return true; }
+
+  // The (handle, offset) entries travel through each rank's exported control region: write
+  // mine, barrier, read the peers' (mapped) regions, barrier (nobody rewrites its entry before
+  // every rank read it).
+  bool p2p_map(const void* mine, std::vector<const void*>& all) override {
+    const PeerEntry e = peer_entry(mine);
+    SPL_CUDA(cudaMemcpy(base_[rank0_] + kXchOff, &e, sizeof e, cudaMemcpyHostToDevice));
+    barrier(0);
+    SPL_CUDA(cudaStreamSynchronize(0));
+    all.assign(t_, nullptr);
+    for (int q = 0; q < t_; ++q) {
+      if (q == rank0_) {
+        all[q] = mine;
+        continue;
+      }
+      PeerEntry pe;
+      SPL_CUDA(cudaMemcpy(&pe, base_[q] + kXchOff, sizeof pe, cudaMemcpyDeviceToHost));
+      all[q] = maps_.open(q, pe);
+    }
+    barrier(0);
+    SPL_CUDA(cudaStreamSynchronize(0));
+    return true;
+  }
+  void p2p_barrier(cudaStream_t st) override { barrier(st); }
 
   void all_gather(const void* const* shard, void* const* full, int64_t n, DType dt,
                   cudaStream_t st) override {
@@ -537,8 +638,11 @@ class IpcComm final : public Comm {
     SPL_CHECK_LAUNCH();
   }
 
+  static constexpr size_t kXchOff = 2048;  // address-exchange entry in the control region
+  static_assert(kXchOff >= kCtrlWords * 4 && kXchOff + sizeof(PeerEntry) <= 4096, "ctrl layout");
   std::unique_ptr<IpcRankImpl> r_;
   std::vector<char*> base_;
+  PeerMaps maps_;  // destroyed before the peers' regions are closed (declared after base_)
   int dev_ = 0;
 };
 }  // namespace

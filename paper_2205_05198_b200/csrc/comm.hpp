@@ -63,6 +63,21 @@ class Comm {
   virtual void p2p_ready_wait(int src, cudaStream_t st) { (void)src; (void)st; }
   // Whether the fused reduce-scatter is on by default for this transport.
   virtual bool p2p_default() const { return local_ == t_; }
+
+  // ---- all-gather fused into the consuming GEMM by pulling (peer ranks): the GEMM's TMA
+  // reads every rank's shard where it lies (peer memory over NVLink), so the transfer is spread
+  // over the GEMM's tiles. p2p_map exchanges the address of a buffer every rank holds in the
+  // same role (collective: every rank calls it in the same order) and returns the t ranks'
+  // addresses valid in this process; p2p_barrier (on `st`) orders every rank's writes issued
+  // before it ahead of every rank's reads issued after it.
+  virtual bool p2p_map(const void* mine, std::vector<const void*>& all) {
+    (void)mine;
+    (void)all;
+    return false;
+  }
+  virtual void p2p_barrier(cudaStream_t st) { (void)st; }
+  // Whether the pulled all-gather is on by default for this transport.
+  virtual bool pull_default() const { return false; }
   // Whether collectives must be issued on one stream in one order on every rank (device-side
   // sequence-numbered protocols); the layer then keeps them all on its compute stream.
   virtual bool serial_order() const { return false; }

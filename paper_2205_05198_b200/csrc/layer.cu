@@ -94,13 +94,32 @@ class Layer final : public LayerBase {
           h_ % 8 == 0)
         fused_rs_ = comm_->p2p_setup((size_t)(RL_ * h_) * sizeof(T));
     }
-    {  // all-gather fused into the consuming GEMMs (their TMA reads every rank's shard): on for
-       // simulated ranks when every consumer runs on the CTA-pair kernel (SPL_FUSED_AG=0: off)
+    {  // all-gather fused into the consuming GEMMs (their TMA reads every rank's shard) when
+       // every consumer runs on the CTA-pair kernel: simulated ranks read each other's device
+       // buffers; peer ranks pull the shards from the peers' memory (mapped once here), on by
+       // default for the CUDA-IPC transport, opt-in for NCCL ranks (SPL_FUSED_AG=1 / 0)
       const char* f = std::getenv("SPL_FUSED_AG");
-      const bool want = f != nullptr ? f[0] == '1' : true;
+      const bool local = comm_->local() == t_;
+      const bool want = f != nullptr ? f[0] == '1' : (local || comm_->pull_default());
       if (want && std::is_same_v<T, bf16> && sp_ && t_ > 1 && t_ <= GemmArgs::kMaxShards &&
-          comm_->local() == t_ && RL_ % 128 == 0)
-        fused_ag_ = fused_ag_eligible();
+          RL_ % 128 == 0) {
+        if (local) {
+          fused_ag_ = fused_ag_eligible();
+        } else {
+          pull_ = true;  // shard_of() reads peer_ (the probe only needs shapes: own buffers)
+          for (int w = 1; w < 4; ++w)
+            for (int q = 0; q < t_; ++q) peer_[w][q] = own_shard((Gath)w);
+          if (fused_ag_eligible()) {
+            std::vector<const void*> all;
+            for (int w = 1; w < 4; ++w) {
+              if (!comm_->p2p_map(own_shard((Gath)w), all)) break;
+              for (int q = 0; q < t_; ++q) peer_[w][q] = all[q];
+              fused_ag_ = w == 3;
+            }
+          }
+          pull_ = fused_ag_;
+        }
+      }
     }
     const char* e = std::getenv("SPL_KEEPBITS_SIDE");
     bits_serial_ = !(e != nullptr && e[0] == '1');
@@ -139,6 +158,10 @@ class Layer final : public LayerBase {
   }
 
   int local_ranks() const override { return L_; }
+  void comm_paths(int out[2]) const override {
+    out[0] = fused_rs_ ? 1 : 0;
+    out[1] = fused_ag_ ? (pull_ ? 2 : 1) : 0;
+  }
   void set_caller_stream(cudaStream_t s) override { caller_ = s; }
 
   // Run `body` (which issues work on st_, possibly forking to the side streams and joining
@@ -873,8 +896,13 @@ class Layer final : public LayerBase {
   // from every rank's shard instead of the gathered copy.
   enum Gath : int { kNoGath = 0, kGY1, kGY2, kGD };
   const void* shard_of(Gath w, int q) const {
+    if (pull_) return peer_[w][q];  // peer ranks: the shard in rank q's memory
     return w == kGY1 ? (const void*)R_[q].y1_s : w == kGY2 ? (const void*)R_[q].y2
                                                            : (const void*)R_[q].d_s;
+  }
+  const void* own_shard(Gath w) const {
+    return w == kGY1 ? (const void*)R_[0].y1_s : w == kGY2 ? (const void*)R_[0].y2
+                                                           : (const void*)R_[0].d_s;
   }
   GemmArgs gemm_args(int64_t M, int64_t N, int64_t K, const T* A, int64_t lda, Major am,
                      const T* B, int64_t ldb, Major bm, void* C, int64_t ldc, Epi epi,
@@ -996,7 +1024,16 @@ class Layer final : public LayerBase {
   void gather(std::function<const void*(int)> shard, std::function<void*(int)> full, CommTag tag) {
     comm_->log(tag, 0, RF_ * h_);
     if (t_ == 1) return;  // identity; callers read the shard itself (see gathered())
-    if (fused_ag_) return;  // the consuming GEMMs read the shards (GemmArgs::a_shard/b_shard)
+    if (fused_ag_) {  // the consuming GEMMs read the shards (GemmArgs::a_shard/b_shard)
+      // peer ranks: every rank's shard written before any rank's consumer reads it. The
+      // re-gathers (stored Y1 / Y2, gather_async) need none: written in the forward, many
+      // barriers ago. Write-after-read is ordered by the schedule: a rank rewrites Y1 / Y2 in
+      // its next forward, after the gradient all-reduce every rank enters after its last
+      // reader; dY shards (d_s) are rewritten after the reduce-scatter that follows every
+      // rank's readers of them.
+      if (pull_) launch(K_COMM, 1, 0, 0, [&] { comm_->p2p_barrier(st_); });
+      return;
+    }
     auto s = cptrs(shard);
     auto f = mptrs(full);
     launch(K_COMM, 1, 0, (double)RF_ * h_ * sizeof(T) * (t_ - 1) / t_,
@@ -1399,7 +1436,9 @@ class Layer final : public LayerBase {
   bool bits_pending_ = false;
   bool bits_serial_ = true;
   bool comm_serial_ = false;  // SPL_SERIAL_COMM=1: backward collectives on the main stream
-  bool fused_ag_ = false;     // all-gather fused into the consuming GEMMs (simulated ranks)
+  bool fused_ag_ = false;     // all-gather fused into the consuming GEMMs
+  bool pull_ = false;         // ... reading the peer ranks' shards in their memory
+  const void* peer_[4][GemmArgs::kMaxShards] = {};  // [Gath][rank] shard addresses (pull_)
   bool fused_rs_ = false;  // reduce-scatters fused into the row-parallel GEMMs  // SPL_KEEPBITS_SIDE=1: RNG pass on the side stream
   bool graphs_ = false;
   std::vector<Graph> gfwd_, gbwd_;

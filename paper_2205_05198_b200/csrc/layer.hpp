@@ -51,6 +51,7 @@ class LayerBase {
   virtual void read_profile(double ms[K_NCLASS], int64_t launches[K_NCLASS],
                             double flops[K_NCLASS], double bytes[K_NCLASS]) = 0;
   virtual int64_t launch_count(bool reset) = 0;
+  virtual void comm_paths(int out[2]) const = 0;
   virtual void set_graphs(bool on) = 0;
   virtual int local_ranks() const = 0;
   virtual void set_caller_stream(cudaStream_t s) = 0;

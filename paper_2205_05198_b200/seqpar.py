@@ -265,6 +265,14 @@ class SeqparLayer:
         check(lib().spl_launch_count(self._h, C.byref(v), int(reset)))
         return v.value
 
+    def comm_paths(self) -> dict:
+        """Collective paths in use: fused reduce-scatter, and the all-gather as "copy" (gathered
+        copies), "local" (consumers read the simulated ranks' shards) or "pull" (consumers read
+        the peer ranks' shards in their memory)."""
+        v = (C.c_int32 * 2)()
+        check(lib().spl_comm_paths(self._h, v))
+        return {"fused_rs": bool(v[0]), "all_gather": ("copy", "local", "pull")[v[1]]}
+
     def set_graphs(self, on: bool):
         check(lib().spl_set_graphs(self._h, int(on)))
 

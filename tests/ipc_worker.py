@@ -55,8 +55,10 @@ def main():
         dx = L.backward(dd)
     torch.cuda.synchronize()
     log = L.comm_log()
+    paths = L.comm_paths()
     np.savez(out, y=y[0].double().cpu().numpy(), dx=dx[0].double().cpu().numpy(), grads=L.grads(),
-             w1=L.w1_grad_shard(0),
+             w1=L.w1_grad_shard(0), paths=np.array([int(paths["fused_rs"]),
+                                                   ("copy", "local", "pull").index(paths["all_gather"])]),
              comm=np.array([[v["all_gathers"], v["reduce_scatters"], v["all_reduces"], v["ring_elements"]]
                             for v in log.values()]))
     dist.barrier()

@@ -23,9 +23,15 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 SMALL = dict(heads=8, hidden=256, seq=128, batch=2)       # head_dim 32
 UMMA = dict(heads=4, hidden=256, seq=256, batch=2)        # head_dim 64, RL % 128 == 0
+WIDE = dict(heads=4, hidden=512, seq=256, batch=2)        # h/t = 256: the pulled all-gather
 CASES = [
     dict(shape=UMMA, recompute="selective", dtype="bf16"),                 # fused RS (default)
     dict(shape=UMMA, recompute="none", dtype="bf16", env={"SPL_FUSED_RS": "0"}),  # pushed RS
+    # all-gathers fused into the consuming GEMMs, which pull the peer's shards from its memory
+    # (default at this width), with the fused reduce-scatter; then the pushed all-gather
+    dict(shape=WIDE, recompute="selective", dtype="bf16"),
+    dict(shape=WIDE, recompute="none", dtype="bf16", graphs=True, steps=3),
+    dict(shape=WIDE, recompute="selective", dtype="bf16", env={"SPL_FUSED_AG": "0"}),
     dict(shape=SMALL, recompute="full", dtype="f32", causal=True),
     dict(shape=SMALL, recompute="selective", dtype="bf16", sp=False),      # f̄ all-reduce
     dict(shape=UMMA, recompute="selective", dtype="bf16", graphs=True, steps=3),  # graph replays
@@ -60,7 +66,8 @@ def run_local(spl, orc, case):
     dx = L.backward(dd)
     torch.cuda.synchronize()
     out = dict(y=[v.double().cpu().numpy() for v in y], dx=[v.double().cpu().numpy() for v in dx],
-               grads=L.grads(), w1=[L.w1_grad_shard(r) for r in range(2)], comm=L.comm_log())
+               grads=L.grads(), w1=[L.w1_grad_shard(r) for r in range(2)], comm=L.comm_log(),
+               paths=L.comm_paths())
     L.close()
     return out
 
@@ -93,6 +100,15 @@ def test_two_processes_bit_identical_to_local(spl, orc, tmp_path, case):
         for k in case.get("env", {}):
             os.environ.pop(k, None)
     sp = case.get("sp", True)
+    # the paths the peer ranks ran: the pulled all-gather wherever the simulated group fuses it
+    # (same eligibility), unless switched off
+    for r in range(2):
+        fused_rs, ag = got[r]["paths"]
+        assert bool(fused_rs) == want["paths"]["fused_rs"], (r, got[r]["paths"], want["paths"])
+        assert ("copy", "local", "pull")[ag] == ("pull" if want["paths"]["all_gather"] == "local"
+                                                 else "copy"), (r, got[r]["paths"], want["paths"])
+    if case["shape"] is WIDE and "SPL_FUSED_AG" not in case.get("env", {}):
+        assert want["paths"]["all_gather"] == "local" and got[0]["paths"][1] == 2
     for r in range(2):
         assert np.array_equal(got[r]["y"], want["y"][r]), f"y rank {r}"
         assert np.array_equal(got[r]["dx"], want["dx"][r]), f"dx rank {r}"
