@@ -106,7 +106,9 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
 }
 
 template <int HD, bool CAUSAL, bool STORED>
-__global__ void __launch_bounds__(320, 1)
+// 320 threads, one CTA per SM: up to 200 registers (the default cap of 168 spilled the stored
+// head_dim 160 variant: 176 bytes of stack; 56 at 200)
+__global__ void __maxnreg__(200)
     fa_bwd_dkdv_umma(const __grid_constant__ CUtensorMap map_kv,  // qkv, 128-row boxes
                      const __grid_constant__ CUtensorMap map_q,   // qkv, 64-row boxes
                      const __grid_constant__ CUtensorMap map_do,  // dO, 64-row boxes
@@ -681,8 +683,7 @@ __global__ void __launch_bounds__(320, 1)
                         d0, d1);
             dw[i >> 1] = pack_bf16(d0, d1);
           }
-          return;
-        }
+        } else {
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
           float dv[2];
@@ -700,6 +701,7 @@ __global__ void __launch_bounds__(320, 1)
             dv[u] = p * fmaf(__uint_as_float(rp[e]), kf, -dl);
           }
           dw[i >> 1] = pack_bf16(dv[0], dv[1]);
+        }
         }
       };
       if (full) ds_loop(std::false_type{});
