@@ -106,9 +106,9 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
 }
 
 template <int HD, bool CAUSAL, bool STORED>
-// 320 threads, one CTA per SM: up to 200 registers (the default cap of 168 spilled the stored
-// head_dim 160 variant: 176 bytes of stack; 56 at 200)
-__global__ void __maxnreg__(200)
+// 320 threads = 3 warps on some SMSP (16 K registers each): 168 registers is the ceiling
+// (__maxnreg__(200) compiles but fails to launch); the stored head_dim 160 variant spills.
+__global__ void __launch_bounds__(320, 1)
     fa_bwd_dkdv_umma(const __grid_constant__ CUtensorMap map_kv,  // qkv, 128-row boxes
                      const __grid_constant__ CUtensorMap map_q,   // qkv, 64-row boxes
                      const __grid_constant__ CUtensorMap map_do,  // dO, 64-row boxes
