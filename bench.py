@@ -115,12 +115,17 @@ def max_over_ranks(value, device="cuda"):
 
 def gemm_traffic_from_profile(cfg_name):
     """DRAM bytes per GEMM launch (read + write), averaged over the tcgen05 GEMM launches of
-    one step, from the committed ncu capture (profiles/r01_ncu_dram_<cfg>_t1_selective.json;
+    one step, from the newest committed ncu capture (profiles/r0N_ncu_dram_<cfg>_t1_selective.json;
     ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum). None when absent."""
-    path = os.path.join(ROOT, "profiles", f"r01_ncu_dram_{cfg_name}_t1_selective.json")
-    try:
-        prof = json.load(open(path))
-    except Exception:
+    prof = None
+    for rnd in ("r02", "r01"):
+        path = os.path.join(ROOT, "profiles", f"{rnd}_ncu_dram_{cfg_name}_t1_selective.json")
+        try:
+            prof = json.load(open(path))
+            break
+        except Exception:
+            continue
+    if prof is None:
         return None
     n = b = 0.0
     for k, v in prof.items():
@@ -402,6 +407,7 @@ def main():
                    "heads": a, "hidden": h, "seq": s, "batch": b, "t": t, "dropout_p": 0.1,
                    "causal": False, "parallelism": f"tp{t}+sp" if sp else f"tp{t}",
                    "comm": (args.comm if t > 1 else "none"),
+                   "collectives": L.comm_paths() if t > 1 else None,
                    "l2": "working set > L2 (weights alone 0.9 GB/t); no flush"},
         "mfu": mf / (ms_step / 1e3) / t / (burst * 1e12),
         "mfu_vs_sustained_peak": mf / (ms_step / 1e3) / t / (sustained * 1e12),
