@@ -257,6 +257,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--dtype", default=None, choices=["bf16", "f32"],
+                    help="compute dtype (default: f32 for the tiny config — BASELINE configs[0] "
+                         "is quoted in fp32 — bf16 otherwise)")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "ipc"],
                     help="transport of the t>1 collectives: NCCL, or libspl's CUDA-IPC peer-memory "
                          "transport (spl_create_ipc)")
@@ -294,14 +297,16 @@ def main():
     a, h, s, b = CONFIGS[args.config]
     sp = not args.no_sp
     cfg = spl.BlockConfig(a, h, s, b, dropout_p=0.1, causal=False, seed=42)
-    L = spl.SeqparLayer(cfg, t, args.recompute, sp, "bf16", device=local_rank,
+    dtype = args.dtype or ("f32" if args.config == "tiny" else "bf16")
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    L = spl.SeqparLayer(cfg, t, args.recompute, sp, dtype, device=local_rank,
                         check_finite=False, nccl=nccl, ipc=ipc)
     L.init_params(1234)
     L.set_graphs(not args.no_graphs)  # forward / backward replayed as CUDA graphs
     shp = L.shard_shape()
     gen = torch.Generator(device=f"cuda:{local_rank}").manual_seed(100 + rank)
-    x = [(torch.rand(shp, generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)]
-    dy = [(torch.rand(shp, generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)]
+    x = [(torch.rand(shp, generator=gen, device="cuda") * 2 - 1).to(tdt)]
+    dy = [(torch.rand(shp, generator=gen, device="cuda") * 2 - 1).to(tdt)]
     y = [torch.empty_like(x[0])]
     dx = [torch.empty_like(x[0])]
 
@@ -350,7 +355,7 @@ def main():
     # copies of one step overlapping the compute of its neighbours, one wait at the end.
     e2e = None
     if not args.no_e2e:
-        nbytes = x[0].numel() * 2
+        nbytes = x[0].numel() * x[0].element_size()
         hx = [x[0].cpu().pin_memory() for _ in range(2)]
         hdy = [dy[0].cpu().pin_memory() for _ in range(2)]
         hy = [torch.empty_like(hx[0]).pin_memory() for _ in range(2)]
@@ -400,7 +405,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": dtype,
         "data": "synthetic (seeded U(-1,1) inputs, LayerParams::random on device)",
         "config": {"workload": f"{args.config}-shape layer fwd+bwd, t={t}, SP={'on' if sp else 'off'}, "
                                f"{args.recompute} recompute",
