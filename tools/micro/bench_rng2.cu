@@ -5,6 +5,14 @@
 #include "rng_fast.cuh"
 using namespace spl::rngk;
 
+// x ^= x >> k with the high word's shift as IMAD.HI (FMA pipe) and the low word's as a funnel
+// shift (ALU pipe): 3 ALU + 1 FMA instead of 4 ALU (xs_alu) or 2 ALU + 3 FMA (xs_fma)
+__device__ __forceinline__ void xs_mix(uint32_t& lo, uint32_t& hi, int k, uint32_t m) {
+  const uint32_t f = __funnelshift_r(lo, hi, k), g = __umulhi(hi, m);
+  lo ^= f;
+  hi ^= g;
+}
+
 template <int VAR>
 __device__ __forceinline__ bool keep_var(uint32_t lo, uint32_t hi0, uint32_t hc, uint32_t mixed_lo,
                                          uint32_t mixed_hi, uint32_t t_lo, uint32_t t_hi,
@@ -16,14 +24,14 @@ __device__ __forceinline__ bool keep_var(uint32_t lo, uint32_t hi0, uint32_t hc,
     hi = (uint32_t)(w >> 32) + lo * 0xbf58476du;
     lo = (uint32_t)w;
   }
-  if (VAR & 1) xs_alu(lo, hi, 27); else xs_fma(lo, hi, sm.m27);
+  if (VAR & 256) xs_mix(lo, hi, 27, sm.m27); else if (VAR & 1) xs_alu(lo, hi, 27); else xs_fma(lo, hi, sm.m27);
   mul_c<0x133111ebu, 0x94d049bbu>(lo, hi);
   if (VAR & 32) {  // xor-shift 31 fused with ^ mix64(key) into 3-input LOP3s
     const uint32_t f = __funnelshift_r(lo, hi, 31), g = hi >> 31;
     lo = lo ^ f ^ mixed_lo;
     hi = hi ^ g ^ mixed_hi;
   } else {
-    if (VAR & 2) xs_alu(lo, hi, 31); else xs_fma(lo, hi, sm.m31);
+    if (VAR & 256) xs_mix(lo, hi, 31, sm.m31); else if (VAR & 2) xs_alu(lo, hi, 31); else xs_fma(lo, hi, sm.m31);
     lo ^= mixed_lo;
     hi ^= mixed_hi;
   }
@@ -36,12 +44,12 @@ __device__ __forceinline__ bool keep_var(uint32_t lo, uint32_t hi0, uint32_t hc,
     hi = (uint32_t)(w >> 32);
     lo = (uint32_t)w;
   }
-  if (VAR & 4) xs_fma(lo, hi, sm.m30); else xs_alu(lo, hi, 30);
+  if (VAR & 256) xs_mix(lo, hi, 30, sm.m30); else if (VAR & 4) xs_fma(lo, hi, sm.m30); else xs_alu(lo, hi, 30);
   mul_c<0x1ce4e5b9u, 0xbf58476du>(lo, hi);
-  if (VAR & 8) xs_alu(lo, hi, 27); else xs_fma(lo, hi, sm.m27);
+  if (VAR & 256) xs_mix(lo, hi, 27, sm.m27); else if (VAR & 8) xs_alu(lo, hi, 27); else xs_fma(lo, hi, sm.m27);
   mul_c<0x133111ebu, 0x94d049bbu>(lo, hi);
   if (VAR & 16) {  // high word decides unless equal to the threshold's
-    const uint32_t h2 = hi ^ (hi >> 31);
+    const uint32_t h2 = hi ^ ((VAR & 512) ? __umulhi(hi, sm.m31) : (hi >> 31));
     if (__builtin_expect(h2 != t_hi, 1)) return h2 > t_hi;
     const uint32_t l2 = lo ^ __funnelshift_r(lo, hi, 31);
     return l2 >= t_lo;
@@ -122,10 +130,14 @@ int main() {
   int* bad;
   cudaMalloc(&bits, (size_t)nrows * W * 4);
   cudaMalloc(&bad, 4);
-  run<75, 1024, 1>(bits, bad, nrows, W, s, 1);
-  run<75 | 128, 1024, 1>(bits, bad, nrows, W, s, 1);
-  run<75, 1024, 1>(bits, bad, nrows, W, s, 1);
-  run<75 | 128, 1024, 1>(bits, bad, nrows, W, s, 1);
+  for (int rep = 0; rep < 2; ++rep) {
+    run<75 | 128 | 16, 1024, 1>(bits, bad, nrows, W, s, 1);          // production form
+    run<75 | 128 | 16 | 256, 1024, 1>(bits, bad, nrows, W, s, 1);    // hi shifts as IMAD.HI
+    run<75 | 128 | 16 | 256 | 512, 1024, 1>(bits, bad, nrows, W, s, 1);
+    run<75 | 128 | 16 | 32 | 256, 1024, 1>(bits, bad, nrows, W, s, 1);
+    run<75 | 128 | 16 | 32 | 256 | 512, 1024, 1>(bits, bad, nrows, W, s, 1);
+    run<75 | 128 | 16 | 32, 1024, 1>(bits, bad, nrows, W, s, 1);
+  }
   printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
