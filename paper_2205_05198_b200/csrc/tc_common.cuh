@@ -28,6 +28,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+// Register reallocation between warpgroups (all four warps of a warpgroup execute it): the
+// producer / MMA warps give registers to the warps that hold whole rows of S.
+template <uint32_t N>
+__device__ __forceinline__ void regs_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void regs_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
 // Non-blocking probe: true once the phase with parity `phase` has completed.
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
   uint32_t ok;
