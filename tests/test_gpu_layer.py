@@ -481,3 +481,17 @@ def test_spl_create_survey_form(spl, orc):
     h2 = C.c_void_p()
     rc = _lib.lib().spl_create(C.byref(d), (C.c_int * 2)(0, 1), 2, C.byref(h2))
     assert rc == _lib.SPL_EINVAL
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_bf16_no_dropout_tcgen05_attention(spl, orc, causal):
+    """p = 0: the attention kernels run without keep bits (no keep-bit buffer is read); the
+    two-tile ping-pong forward and the fused backward at head_dim 64, s % 128 == 0."""
+    cfg, x, dy, p = make_case(orc, dict(heads=4, hidden=256, seq=256, batch=2), dropout=0.0,
+                              causal=causal, key=11)
+    ref = orc.seqpar_layer(cfg, 1, p, x, dy)
+    L, y, dx, g = run(spl, cfg, 1, p, x, dy, "selective", dtype="bf16")
+    assert rel_l2(y, ref.y) <= 1e-2
+    assert rel_l2(dx, ref.dx) <= 1e-2
+    grads_close(orc, cfg.hidden, g, ref.grads, 2e-2)
+    L.close()
