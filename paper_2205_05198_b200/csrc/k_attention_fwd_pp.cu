@@ -59,6 +59,8 @@ struct PpCfg {
   static constexpr int ATOMS = (HD + 63) / 64;
   static constexpr int TILE = ATOMS * kAtomBytes;
   static constexpr int KVS = HD <= 64 ? 4 : 2;  // (K, V) ring depth, 128 keys per stage
+  static constexpr int ORS = HD <= 64 ? 128 : 256;  // epilogue staging row stride (bytes)
+  static_assert(TILE >= 128 * ORS && HD * 2 <= ORS, "epilogue staging: 128 rows per Q tile");
   static constexpr int KV_OFF = 2 * TILE;
   static constexpr int BAR_OFF = KV_OFF + KVS * 2 * TILE;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
@@ -272,18 +274,34 @@ __global__ void __launch_bounds__(384, 1)
       const float oscale = a.drop.inv_keep / l;
       mbar_wait(&o_full[t], 0);
       tc_fence_after();
-      bf16* out = static_cast<bf16*>(a.o) + ((int64_t)(qr < S ? qr : 0) * a.b + bj) * a.ldo + (int64_t)hl * HD;
+      // O rows are HD·2 bytes apart from the next query's by b·ldo elements: one thread per row
+      // would issue 32 scattered 16-byte stores per instruction. Stage the warp's 32 rows in
+      // Q_t's shared memory (free: its last Q·Kᵀ completed before o_full) — 128 / 256-byte rows,
+      // 16-byte chunks XOR-swizzled by row — then store them row-contiguously.
+      constexpr int CH = HD / 8;  // 16-byte chunks per row
+      uint8_t* stage = Qs + t * Cfg::TILE + qd * 32 * Cfg::ORS;
+      uint8_t* srow = stage + lane * Cfg::ORS;
 #pragma unroll 1
       for (int c = 0; c < HD / 32; ++c) {
         float v[32];
         tmem_ld32(tl + ocol + c * 32, v);
-        if (qr < S) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 8)
-            *reinterpret_cast<uint4*>(out + c * 32 + i) =
-                make_uint4(pack_bf16x2(v[i] * oscale, v[i + 1] * oscale), pack_bf16x2(v[i + 2] * oscale, v[i + 3] * oscale),
-                           pack_bf16x2(v[i + 4] * oscale, v[i + 5] * oscale), pack_bf16x2(v[i + 6] * oscale, v[i + 7] * oscale));
+        for (int i = 0; i < 32; i += 8) {
+          const int ch = (c * 32 + i) / 8;
+          *reinterpret_cast<uint4*>(srow + ((ch ^ (lane & 7)) * 16)) =
+              make_uint4(pack_bf16x2(v[i] * oscale, v[i + 1] * oscale), pack_bf16x2(v[i + 2] * oscale, v[i + 3] * oscale),
+                         pack_bf16x2(v[i + 4] * oscale, v[i + 5] * oscale), pack_bf16x2(v[i + 6] * oscale, v[i + 7] * oscale));
         }
+      }
+      __syncwarp();
+      bf16* obase = static_cast<bf16*>(a.o) + (int64_t)bj * a.ldo + (int64_t)hl * HD;
+#pragma unroll 1
+      for (int idx = lane; idx < 32 * CH; idx += 32) {
+        const int r = idx / CH, ch = idx % CH;
+        const int q = q0t + qd * 32 + r;
+        if (q < S)
+          *reinterpret_cast<uint4*>(obase + (int64_t)q * a.b * a.ldo + ch * 8) =
+              *reinterpret_cast<const uint4*>(stage + r * Cfg::ORS + ((ch ^ (r & 7)) * 16));
       }
       if (qr < S && a.lse) a.lse[brow + qr] = (m_used + log2f(l)) * kLn2;
     }
