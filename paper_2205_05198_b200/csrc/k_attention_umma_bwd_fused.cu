@@ -403,10 +403,17 @@ __global__ void __launch_bounds__(512, 1)
       if (lane == 0) mbar_arrive(&w_full[sb]);
       if (trw) TRACE(9, it);
     }
-    // epilogue: dK·scale, dV -> bf16 (the warpgroups take alternate 32-column chunks)
+    // epilogue: dK·scale, dV -> bf16 (the warpgroups take alternate 32-column chunks). Rows of
+    // consecutive keys are b·ld elements apart, so each warp stages its 32 rows in the K / V
+    // tiles' shared memory (free: every MMA completed before acc_full; 16-byte chunks XOR-
+    // swizzled by row) and stores them as row-contiguous runs instead of one 16-byte piece
+    // per lane and instruction.
     mbar_wait(acc_full, 0);
     tc_fence_after();
-    bf16* rowp = dqkv + ((int64_t)key * a.b + bj) * a.ld;
+    constexpr int ORS = HD <= 64 ? 128 : 256;  // staging row stride (bytes)
+    static_assert(C::T128 >= 128 * ORS, "epilogue staging");
+    uint8_t* kst = smem + C::K_OFF + qd * 32 * ORS;
+    uint8_t* vst = smem + C::V_OFF + qd * 32 * ORS;
 #pragma unroll 1
     for (int c = wg; c < HD / 32; c += 2) {
       float v[32], w[32];
@@ -414,13 +421,26 @@ __global__ void __launch_bounds__(512, 1)
       tmem_ld32(tl + C::DV_COL + c * 32, w);
 #pragma unroll
       for (int i = 0; i < 32; i += 8) {
-        *reinterpret_cast<uint4*>(rowp + kcol + c * 32 + i) = make_uint4(
+        const int off = lane * ORS + (((c * 32 + i) / 8) ^ (lane & 7)) * 16;
+        *reinterpret_cast<uint4*>(kst + off) = make_uint4(
             pack_bf16(v[i] * a.scale, v[i + 1] * a.scale), pack_bf16(v[i + 2] * a.scale, v[i + 3] * a.scale),
             pack_bf16(v[i + 4] * a.scale, v[i + 5] * a.scale), pack_bf16(v[i + 6] * a.scale, v[i + 7] * a.scale));
-        *reinterpret_cast<uint4*>(rowp + vcol + c * 32 + i) =
+        *reinterpret_cast<uint4*>(vst + off) =
             make_uint4(pack_bf16(w[i], w[i + 1]), pack_bf16(w[i + 2], w[i + 3]),
                        pack_bf16(w[i + 4], w[i + 5]), pack_bf16(w[i + 6], w[i + 7]));
       }
+    }
+    __syncwarp();
+    const int nck = ((HD / 32 - wg + 1) / 2) * 4;  // this warpgroup's 16-byte chunks per row
+    bf16* kbase = dqkv + ((int64_t)(k0 + qd * 32) * a.b + bj) * a.ld;
+#pragma unroll 1
+    for (int idx = lane; idx < 32 * nck; idx += 32) {
+      const int r = idx / nck, k = idx % nck;
+      const int ch = 4 * (wg + 2 * (k >> 2)) + (k & 3);
+      const int so = r * ORS + ((ch ^ (r & 7)) * 16);
+      bf16* rp = kbase + (int64_t)r * a.b * a.ld + ch * 8;
+      *reinterpret_cast<uint4*>(rp + kcol) = *reinterpret_cast<const uint4*>(kst + so);
+      *reinterpret_cast<uint4*>(rp + vcol) = *reinterpret_cast<const uint4*>(vst + so);
     }
   }
   tc_fence_before();
