@@ -419,26 +419,45 @@ __global__ void __launch_bounds__(320, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&w_full[st]);
     }
-    // epilogue: dK·scale, dV -> bf16 (halves take alternate 32-column chunks)
+    // epilogue: dK·scale, dV -> bf16 (halves take alternate 32-column chunks). Consecutive keys'
+    // rows are b·ld elements apart: each warp stages its 32 rows of dK, then of dV, in the V
+    // tile's shared memory (free: every MMA completed before acc_full; 16-byte chunks with the
+    // low 3 chunk-index bits XOR-swizzled by row) and stores row-contiguous runs.
     mbar_wait(acc_full, 0);
     tc_fence_after();
-    bf16* rowp = dqkv + ((int64_t)(key < S ? key : 0) * a.b + bj) * a.ld;
+    constexpr int CH = HD / 8;                       // 16-byte chunks per row
+    constexpr int ORS = ((CH + 7) / 8) * 8 * 16;     // staging row stride (bytes)
+    static_assert(C::T128 >= 128 * ORS, "epilogue staging");
+    uint8_t* stg = smem + V_OFF + (row & ~31) * ORS;  // this warp's 32 rows
+    const int nck = ((HD / 32 - half + 1) / 2) * 4;  // this half's chunks per row
+    bf16* kbase = dqkv + ((int64_t)(k0 + (row & ~31)) * a.b + bj) * a.ld;
 #pragma unroll 1
-    for (int c = half; c < HD / 32; c += 2) {
-      float v[32], w[32];
-      tmem_ld32(tl + DK_COL + c * 32, v);
-      tmem_ld32(tl + DV_COL + c * 32, w);
-      if (key < S) {
+    for (int pass = 0; pass < 2; ++pass) {  // dK, then dV
+      const int col = pass == 0 ? DK_COL : DV_COL;
+      const float sc = pass == 0 ? a.scale : 1.f;
+#pragma unroll 1
+      for (int c = half; c < HD / 32; c += 2) {
+        float v[32];
+        tmem_ld32(tl + col + c * 32, v);
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
-          *reinterpret_cast<uint4*>(rowp + kcol + c * 32 + i) = make_uint4(
-              pack_bf16(v[i] * a.scale, v[i + 1] * a.scale), pack_bf16(v[i + 2] * a.scale, v[i + 3] * a.scale),
-              pack_bf16(v[i + 4] * a.scale, v[i + 5] * a.scale), pack_bf16(v[i + 6] * a.scale, v[i + 7] * a.scale));
-          *reinterpret_cast<uint4*>(rowp + vcol + c * 32 + i) =
-              make_uint4(pack_bf16(w[i], w[i + 1]), pack_bf16(w[i + 2], w[i + 3]),
-                         pack_bf16(w[i + 4], w[i + 5]), pack_bf16(w[i + 6], w[i + 7]));
+          const int ch = (c * 32 + i) / 8;
+          *reinterpret_cast<uint4*>(stg + lane * ORS + (((ch & ~7) | ((ch & 7) ^ (lane & 7))) * 16)) =
+              make_uint4(pack_bf16(v[i] * sc, v[i + 1] * sc), pack_bf16(v[i + 2] * sc, v[i + 3] * sc),
+                         pack_bf16(v[i + 4] * sc, v[i + 5] * sc), pack_bf16(v[i + 6] * sc, v[i + 7] * sc));
         }
       }
+      __syncwarp();
+      const int dcol = pass == 0 ? kcol : vcol;
+#pragma unroll 1
+      for (int idx = lane; idx < 32 * nck; idx += 32) {
+        const int r = idx / nck, k = idx % nck;
+        const int ch = 4 * (half + 2 * (k >> 2)) + (k & 3);
+        if (k0 + (row & ~31) + r < S)
+          *reinterpret_cast<uint4*>(kbase + (int64_t)r * a.b * a.ld + dcol + ch * 8) =
+              *reinterpret_cast<const uint4*>(stg + r * ORS + (((ch & ~7) | ((ch & 7) ^ (r & 7))) * 16));
+      }
+      __syncwarp();  // the staging rows are rewritten by the next pass
     }
   }
   tc_fence_before();
