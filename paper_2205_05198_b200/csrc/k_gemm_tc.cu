@@ -328,10 +328,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Barriers: full[s] lives in the leader and counts both CTAs' TMA bytes; empty[s] and
 // tfull[acc] exist in both CTAs and are arrived by the leader's multicast commits; tempty[acc]
 // lives in the leader and collects the 4+4 epilogue warps of the pair.
+// TN (pair tile width) 256, or 128 for GEMMs whose 256-wide tiles fill the 74 CTA pairs' last
+// wave badly (t > 1 shards: N = 3h/t, 4h/t, h/t); each CTA stages TN/2 columns of B.
 constexpr int P_STAGES = 6;
-constexpr int P_A_BYTES = 128 * BK * 2, P_B_BYTES = 128 * BK * 2;
-constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
-constexpr int P_SMEM = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+constexpr int P_A_BYTES = 128 * BK * 2;
+template <int TN>
+constexpr int p_stage_bytes() { return P_A_BYTES + (TN / 2) * BK * 2; }
+template <int TN>
+constexpr int p_smem() { return P_STAGES * p_stage_bytes<TN>() + 1024 + 256; }
 
 // Tensor maps of the pair kernel: one per operand, or one per row block of a sharded operand.
 struct PairMaps {
@@ -347,11 +351,12 @@ __device__ __forceinline__ const CUtensorMap* shard_map(const CUtensorMap* maps,
   return maps + q;
 }
 
-template <bool A_MN, bool B_MN, int EPI>
+template <bool A_MN, bool B_MN, int EPI, int TN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tc_pair_kernel(const __grid_constant__ PairMaps maps, const GemmArgs g, int tiles_m,
                         int tiles_n, int group, int l2_hint) {
-  constexpr int TN = 256;
+  static_assert(TN == 256 || TN == 128, "pair tile width");
+  constexpr int P_STAGE_BYTES = p_stage_bytes<TN>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* tiles = smem;
@@ -405,7 +410,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int tile = pair; tile < ntiles; tile += npairs) {
         int mb, nb;
         tile_coords(tile, tiles_m, tiles_n, group, mb, nb);
-        const int m0 = mb * 256 + 128 * (int)rank, n0 = nb * TN + 128 * (int)rank;
+        const int m0 = mb * 256 + 128 * (int)rank, n0 = nb * TN + (TN / 2) * (int)rank;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % P_STAGES;
           const uint32_t ph = (uint32_t)(it / P_STAGES) & 1u;
@@ -434,7 +439,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int kb0 = k0;
             const CUtensorMap* mbp = shard_map(maps.b, g.b_shards, sr, kb0);
             tma_load_2d_pair(sb, mbp, fb, n0, kb0);
-            tma_load_2d_pair(sb + 8192, mbp, fb, n0 + 64, kb0);
+            if (TN == 256) tma_load_2d_pair(sb + 8192, mbp, fb, n0 + 64, kb0);
           } else {
             tma_load_2d_pair(sb, &maps.b[0], fb, k0, n0);
           }
@@ -614,9 +619,10 @@ void launch_tc(const GemmArgs& g, cudaStream_t st) {
   SPL_CHECK_LAUNCH();
 }
 
-template <bool A_MN, bool B_MN, int EPI>
+template <bool A_MN, bool B_MN, int EPI, int TN>
 void launch_pair(const GemmArgs& g, cudaStream_t st) {
-  auto kern = gemm_tc_pair_kernel<A_MN, B_MN, EPI>;
+  auto kern = gemm_tc_pair_kernel<A_MN, B_MN, EPI, TN>;
+  constexpr int P_SMEM = p_smem<TN>();
   static bool attr = [&] {
     SPL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM));
     return true;
@@ -644,12 +650,12 @@ void launch_pair(const GemmArgs& g, cudaStream_t st) {
       maps.b[q] = make_map(g.b_shard[q], g.N, g.shard_rows, g.ldb, 64, BK);
   } else {
     maps.b[0] = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64, BK)
-                     : make_map(g.B, g.K, g.N, g.ldb, BK, 128);
+                     : make_map(g.B, g.K, g.N, g.ldb, BK, TN / 2);
   }
-  const int tiles_m = (int)((g.M + 255) / 256), tiles_n = (int)((g.N + 255) / 256);
+  const int tiles_m = (int)((g.M + 255) / 256), tiles_n = (int)((g.N + TN - 1) / TN);
   const int ntiles = tiles_m * tiles_n;
   const int pairs = ntiles < kNumSMs / 2 ? ntiles : kNumSMs / 2;
-  const int group = pick_group(g.K, 256, 256, tiles_m, tiles_n, pairs);
+  const int group = pick_group(g.K, 256, TN, tiles_m, tiles_n, pairs);
   static const int l2_hint = [] {
     const char* e = std::getenv("SPL_GEMM_L2HINT");
     return (e != nullptr && e[0] == '0') ? 0 : 1;
@@ -658,10 +664,11 @@ void launch_pair(const GemmArgs& g, cudaStream_t st) {
   SPL_CHECK_LAUNCH();
 }
 
-// BN == 0 selects the CTA-pair kernel (256 x 256 tiles).
+// BN == 0 / 1 select the CTA-pair kernel with 256 x 256 / 256 x 128 tiles.
 template <int BN, bool A_MN, bool B_MN, int EPI>
 void run(const GemmArgs& g, cudaStream_t st) {
-  if constexpr (BN == 0) launch_pair<A_MN, B_MN, EPI>(g, st);
+  if constexpr (BN == 0) launch_pair<A_MN, B_MN, EPI, 256>(g, st);
+  else if constexpr (BN == 1) launch_pair<A_MN, B_MN, EPI, 128>(g, st);
   else launch_tc<BN, A_MN, B_MN, EPI>(g, st);
 }
 
@@ -725,6 +732,26 @@ static bool pair_enabled() {
   return on;
 }
 
+// Fraction of the CTA pairs' wave slots a tile grid fills (persistent kernel, 74 pairs).
+static double wave_fill(int64_t tiles) {
+  const int64_t pairs = kNumSMs / 2;
+  const int64_t waves = (tiles + pairs - 1) / pairs;
+  return (double)tiles / (double)(waves * pairs);
+}
+// SPL_GEMM_PAIR128=1 (A/B only): 256 x 128 pair tiles when they fill the last wave clearly
+// better than 256 x 256 (the t > 1 shard widths: N = 768 at 22B t = 8 fills 65 % with
+// 256-wide tiles, 86 % with 128). Measured slower: 22B t = 8 selective + SP per-GPU compute
+// 2.79-2.87 -> 2.99-3.08 ms (the narrower tile's operand traffic outweighs the fuller wave).
+static bool pair_narrow(const GemmArgs& g) {
+  static const bool on = [] {
+    const char* e = std::getenv("SPL_GEMM_PAIR128");
+    return e != nullptr && e[0] == '1';
+  }();
+  if (!on) return false;
+  const int64_t tm = (g.M + 255) / 256;
+  return wave_fill(tm * ((g.N + 127) / 128)) > wave_fill(tm * ((g.N + 255) / 256)) + 0.05;
+}
+
 bool gemm_tc_pair_path(const GemmArgs& g) {
   return g.N >= 256 && g.M >= 256 && pair_enabled() && gemm_tc_supported(g);
 }
@@ -732,7 +759,10 @@ bool gemm_tc_pair_path(const GemmArgs& g) {
 void gemm_tc(const GemmArgs& g, cudaStream_t st) {
   if (g.a_shards > 1 || g.b_shards > 1)
     require(g.N >= 256 && g.M >= 256 && pair_enabled(), "sharded GEMM operands need the pair kernel");
-  if (g.N >= 256 && g.M >= 256 && pair_enabled()) dispatch_bn<0>(g, st);
+  if (g.N >= 256 && g.M >= 256 && pair_enabled()) {
+    if (pair_narrow(g)) dispatch_bn<1>(g, st);
+    else dispatch_bn<0>(g, st);
+  }
   else if (g.N >= 256) dispatch_bn<256>(g, st);
   else dispatch_bn<128>(g, st);
 }
