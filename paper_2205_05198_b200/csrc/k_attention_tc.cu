@@ -127,14 +127,19 @@ __device__ __forceinline__ uint32_t keep_word(const Rng& rng, uint64_t base, int
     if ((blo >> 30) == ((blo + 31u) >> 30)) {
       const uint32_t c30 = __funnelshift_r(blo, bhi, 30);
       if constexpr (TIE) {
+        // keep = hf > t_hi unless hf == t_hi (then the low word decides). hf = raw ^ (raw >> 31)
+        // differs from raw in bit 0 only, so raw > t_hi decides too unless raw and t_hi agree
+        // above bit 0 (raw - (t_hi & ~1) < 2, one IMAD + one compare instead of a shift, an xor
+        // and a compare); such a key (2^-31) sends the word to the exact path below.
         bool tie = false;
+        const uint32_t t_even = t_hi & ~1u;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const uint32_t hf = hash_hi<true>(blo + j, bhi, hc, mixed_lo, mixed_hi, sm, c30);
-          if (hf > t_hi) word |= 1u << j;
-          tie |= hf == t_hi;
+          const uint32_t raw = hash_hi<true, true>(blo + j, bhi, hc, mixed_lo, mixed_hi, sm, c30);
+          if (raw > t_hi) word |= 1u << j;
+          tie |= raw - t_even < 2u;
         }
-        if (tie) {  // a key's high word equals the threshold's: decide on the low word
+        if (tie) {  // a key near the threshold: decide every key of the word exactly
           word = 0;
 #pragma unroll 1
           for (int j = 0; j < 32; ++j)

@@ -495,9 +495,25 @@ __global__ void __launch_bounds__(512) bdr_v(const T* __restrict__ a, SlotSrc sl
         if (blo <= 0xffffffffu - (uint32_t)(VW - 1)) {
           const uint32_t hx = bhi ^ (bhi >> 30);
           const uint32_t hc = hx * 0x1ce4e5b9u;
+          // fast form (as keep_bits_k): lo >> 30 constant over the VW keys, keep decided on the
+          // raw high word; a key near the threshold (or a 2^30 crossing) takes the exact form
+          bool rare = (blo >> 30) != ((blo + (uint32_t)(VW - 1)) >> 30);
+          if (!rare) {
+            const uint32_t c30 = __funnelshift_r(blo, bhi, 30);
+            const uint32_t t_even = t_hi & ~1u;
 #pragma unroll
-          for (int j = 0; j < VW; ++j)
-            if (keep_fast(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm)) kb |= 1u << j;
+            for (int j = 0; j < VW; ++j) {
+              const uint32_t raw = hash_hi<true, true>(blo + j, bhi, hc, mixed_lo, mixed_hi, sm, c30);
+              if (raw > t_hi) kb |= 1u << j;
+              rare |= raw - t_even < 2u;
+            }
+          }
+          if (rare) {
+            kb = 0;
+#pragma unroll 1
+            for (int j = 0; j < VW; ++j)
+              if (keep_fast(blo + j, bhi, hc, hx, mixed_lo, mixed_hi, t_lo, t_hi, sm)) kb |= 1u << j;
+          }
         } else {
           for (int j = 0; j < VW; ++j)
             if (mix_post((mix_post(B + j) ^ key.mixed) + kG) >= tsh) kb |= 1u << j;

@@ -92,7 +92,10 @@ __device__ __forceinline__ bool keep_fast(uint32_t lo, uint32_t hi0, uint32_t hc
 // compare): keep = hf > t_hi, or hf == t_hi and the low word >= t_lo. A tie has probability
 // 2^-32 per key; the caller flags it (one predicate-OR compare) and redoes that word with
 // keep_fast. Saves two of the ~44 integer instructions per key.
-template <bool C30 = false>
+// RAW: the high word before the final xor-shift (hf = raw ^ (raw >> 31) differs from raw in
+// bit 0 only), for callers that compare against the threshold on raw and fall back on the
+// rare keys whose raw agrees with the threshold above bit 0.
+template <bool C30 = false, bool RAW = false>
 __device__ __forceinline__ uint32_t hash_hi(uint32_t lo, uint32_t hi0, uint32_t hc,
                                             uint32_t mixed_lo, uint32_t mixed_hi,
                                             const ShiftMuls& sm, uint32_t c30 = 0) {
@@ -118,7 +121,7 @@ __device__ __forceinline__ uint32_t hash_hi(uint32_t lo, uint32_t hi0, uint32_t 
   mul_c<0x1ce4e5b9u, 0xbf58476du>(lo, hi);
   xs_alu(lo, hi, 27);
   hi = __umulhi(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;
-  return hi ^ (hi >> 31);
+  return RAW ? hi : hi ^ (hi >> 31);
 }
 
 }  // namespace spl::rngk
