@@ -32,6 +32,7 @@ CASES = [
     dict(shape=WIDE, recompute="selective", dtype="bf16"),
     dict(shape=WIDE, recompute="none", dtype="bf16", graphs=True, steps=3),
     dict(shape=WIDE, recompute="selective", dtype="bf16", env={"SPL_FUSED_AG": "0"}),
+    dict(shape=WIDE, recompute="full", dtype="bf16", causal=True),  # pulled AG, forward re-run
     dict(shape=SMALL, recompute="full", dtype="f32", causal=True),
     dict(shape=SMALL, recompute="selective", dtype="bf16", sp=False),      # f̄ all-reduce
     dict(shape=UMMA, recompute="selective", dtype="bf16", graphs=True, steps=3),  # graph replays
