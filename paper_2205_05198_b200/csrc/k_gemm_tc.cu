@@ -74,6 +74,16 @@ __device__ __forceinline__ float gelu_grad_fast(float x) {
 }
 
 // ------------------------------------------------------------------ epilogue store
+// 32-byte global store (st.global.v8.b32, sm_100): one full sector per lane. p 32-byte aligned.
+__device__ __forceinline__ void st_v8(void* p, const uint32_t (&w)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(w[0]),
+               "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+}
+__device__ __forceinline__ uint32_t pk_bf16(float lo, float hi) {
+  __nv_bfloat162 t = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&t);
+}
 template <int EPI>
 __device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t m, int64_t n0,
                                             const float (&v)[32]) {
@@ -88,6 +98,14 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t m, int64_
           const float4 o = *reinterpret_cast<const float4*>(c + i);
           *reinterpret_cast<float4*>(c + i) =
               make_float4(o.x + v[i], o.y + v[i + 1], o.z + v[i + 2], o.w + v[i + 3]);
+        }
+      } else if (((uintptr_t)c & 31) == 0) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint32_t w[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) w[j] = __float_as_uint(v[i + j]);
+          st_v8(c + i, w);
         }
       } else {
 #pragma unroll
@@ -137,7 +155,21 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t m, int64_
     }
     bf16* c = gemm_row<bf16>(g, m) + n0;
     bf16* c2 = EPI == (int)Epi::BiasGelu ? static_cast<bf16*>(g.C2) + m * g.ldc + n0 : nullptr;
-    if (full) {
+    if (full && (((uintptr_t)c | (uintptr_t)(c2 != nullptr ? c2 : c)) & 31) == 0) {
+      // a row's 32 columns as two 32-byte stores per output (full sectors)
+#pragma unroll
+      for (int i = 0; i < 32; i += 16) {
+        uint32_t w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) w[j] = pk_bf16(o[i + 2 * j], o[i + 2 * j + 1]);
+        st_v8(c + i, w);
+        if constexpr (EPI == (int)Epi::BiasGelu) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) w[j] = pk_bf16(o2[i + 2 * j], o2[i + 2 * j + 1]);
+          st_v8(c2 + i, w);
+        }
+      }
+    } else if (full) {
 #pragma unroll
       for (int i = 0; i < 32; i += 8) {
         uint4 t;
