@@ -39,14 +39,6 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 32-byte global store (st.global.v8.b32, sm_100): a full sector per lane, half the store
-// instructions of 16-byte stores for the stored interior's row segments. p: 32-byte aligned.
-__device__ __forceinline__ void st_v8(void* p, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                      uint32_t a4, uint32_t a5, uint32_t a6, uint32_t a7) {
-  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a0),
-               "r"(a1), "r"(a2), "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7)
-               : "memory");
-}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -529,13 +521,23 @@ __global__ void __launch_bounds__(320, 1)
       float v[32];
       tmem_ld32(tl + Cfg::O_COL + c * 32, v);
       if (qr < S) {
+        if ((((uintptr_t)(out + c * 32)) & 31) == 0) {  // full 32-byte sectors per lane
 #pragma unroll
-        for (int i = 0; i < 32; i += 8)
-          *reinterpret_cast<uint4*>(out + c * 32 + i) =
-              make_uint4(pack_bf16(v[i] * oscale, v[i + 1] * oscale),
-                         pack_bf16(v[i + 2] * oscale, v[i + 3] * oscale),
-                         pack_bf16(v[i + 4] * oscale, v[i + 5] * oscale),
-                         pack_bf16(v[i + 6] * oscale, v[i + 7] * oscale));
+          for (int i = 0; i < 32; i += 16)
+            st_v8(out + c * 32 + i, pack_bf16(v[i] * oscale, v[i + 1] * oscale),
+                  pack_bf16(v[i + 2] * oscale, v[i + 3] * oscale), pack_bf16(v[i + 4] * oscale, v[i + 5] * oscale),
+                  pack_bf16(v[i + 6] * oscale, v[i + 7] * oscale), pack_bf16(v[i + 8] * oscale, v[i + 9] * oscale),
+                  pack_bf16(v[i + 10] * oscale, v[i + 11] * oscale), pack_bf16(v[i + 12] * oscale, v[i + 13] * oscale),
+                  pack_bf16(v[i + 14] * oscale, v[i + 15] * oscale));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8)
+            *reinterpret_cast<uint4*>(out + c * 32 + i) =
+                make_uint4(pack_bf16(v[i] * oscale, v[i + 1] * oscale),
+                           pack_bf16(v[i + 2] * oscale, v[i + 3] * oscale),
+                           pack_bf16(v[i + 4] * oscale, v[i + 5] * oscale),
+                           pack_bf16(v[i + 6] * oscale, v[i + 7] * oscale));
+        }
       }
     }
     if (half == 0 && qr < S && a.lse) a.lse[brow + qr] = (m + log2f(l)) * kLn2;

@@ -750,11 +750,21 @@ __global__ void __launch_bounds__(320, 1)
       float v[32];
       tmem_ld32(tl + DQ_COL + c * 32, v);
       if (qr < S) {
+        const float sc = a.scale;
+        if ((((uintptr_t)(out + c * 32)) & 31) == 0) {  // full 32-byte sectors per lane
 #pragma unroll
-        for (int i = 0; i < 32; i += 8)
-          *reinterpret_cast<uint4*>(out + c * 32 + i) = make_uint4(
-              pack_bf16(v[i] * a.scale, v[i + 1] * a.scale), pack_bf16(v[i + 2] * a.scale, v[i + 3] * a.scale),
-              pack_bf16(v[i + 4] * a.scale, v[i + 5] * a.scale), pack_bf16(v[i + 6] * a.scale, v[i + 7] * a.scale));
+          for (int i = 0; i < 32; i += 16)
+            st_v8(out + c * 32 + i, pack_bf16(v[i] * sc, v[i + 1] * sc), pack_bf16(v[i + 2] * sc, v[i + 3] * sc),
+                  pack_bf16(v[i + 4] * sc, v[i + 5] * sc), pack_bf16(v[i + 6] * sc, v[i + 7] * sc),
+                  pack_bf16(v[i + 8] * sc, v[i + 9] * sc), pack_bf16(v[i + 10] * sc, v[i + 11] * sc),
+                  pack_bf16(v[i + 12] * sc, v[i + 13] * sc), pack_bf16(v[i + 14] * sc, v[i + 15] * sc));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8)
+            *reinterpret_cast<uint4*>(out + c * 32 + i) = make_uint4(
+                pack_bf16(v[i] * sc, v[i + 1] * sc), pack_bf16(v[i + 2] * sc, v[i + 3] * sc),
+                pack_bf16(v[i + 4] * sc, v[i + 5] * sc), pack_bf16(v[i + 6] * sc, v[i + 7] * sc));
+        }
       }
     }
   }

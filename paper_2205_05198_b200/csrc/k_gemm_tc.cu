@@ -75,7 +75,7 @@ __device__ __forceinline__ float gelu_grad_fast(float x) {
 
 // ------------------------------------------------------------------ epilogue store
 // 32-byte global store (st.global.v8.b32, sm_100): one full sector per lane. p 32-byte aligned.
-__device__ __forceinline__ void st_v8(void* p, const uint32_t (&w)[8]) {
+__device__ __forceinline__ void st_v8a(void* p, const uint32_t (&w)[8]) {
   asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(w[0]),
                "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
                : "memory");
@@ -105,7 +105,7 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t m, int64_
           uint32_t w[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) w[j] = __float_as_uint(v[i + j]);
-          st_v8(c + i, w);
+          st_v8a(c + i, w);
         }
       } else {
 #pragma unroll
@@ -162,11 +162,11 @@ __device__ __forceinline__ void store_chunk(const GemmArgs& g, int64_t m, int64_
         uint32_t w[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) w[j] = pk_bf16(o[i + 2 * j], o[i + 2 * j + 1]);
-        st_v8(c + i, w);
+        st_v8a(c + i, w);
         if constexpr (EPI == (int)Epi::BiasGelu) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) w[j] = pk_bf16(o2[i + 2 * j], o2[i + 2 * j + 1]);
-          st_v8(c2 + i, w);
+          st_v8a(c2 + i, w);
         }
       }
     } else if (full) {
