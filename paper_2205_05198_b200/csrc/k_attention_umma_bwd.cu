@@ -776,8 +776,10 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
+}  // namespace
+
 // 3-D map over a stored interior {nblk = lh*b, s, s} (row = query, contiguous keys):
-// dims {s (key), s (query), nblk}; box {box_k, box_q, 1}.
+// dims {s (key), s (query), nblk}; box {box_k, box_q, 1}. Also used by the fused backward.
 CUtensorMap interior_map(const void* ptr, bool u8, int64_t s, int64_t nblk, int box_k, int box_q,
                          bool sw128) {
   CUtensorMap m;
@@ -795,6 +797,8 @@ CUtensorMap interior_map(const void* ptr, bool u8, int64_t s, int64_t nblk, int 
   if (r != CUDA_SUCCESS) raise(3, "cuTensorMapEncodeTiled (interior) failed: " + std::to_string((int)r));
   return m;
 }
+
+namespace {
 
 template <int HD, bool CAUSAL, bool STORED>
 void launch_bwd_umma(const AttnArgs& a, const bf16* dout, bf16* dqkv, const float* delta,

@@ -36,6 +36,8 @@
 namespace spl::k {
 
 CUtensorMap attn_seq_map(const void* ptr, int64_t width, int64_t b, int64_t s, int64_t ld, int rows);
+CUtensorMap interior_map(const void* ptr, bool u8, int64_t s, int64_t nblk, int box_k, int box_q,
+                         bool sw128);
 
 namespace {
 
@@ -78,7 +80,10 @@ constexpr int kTraceX = 3, kTraceY = 100;
     if (tr != nullptr && (it) < 64) tr[(e) * 64 + (it)] = (unsigned long long)clock64();     \
   } while (0)
 
-template <int HD>
+// STORED (no-recompute regime): Sᵀ is not recomputed — P = softmax_out and the dropout mask
+// of each [64 queries x 128 keys] block are loaded by TMA from the stored interior into the
+// Q / dO ring stage (3 of the 5 stored bytes per element read once), P̃ = P·keep/(1-p).
+template <int HD, bool STORED = false>
 struct FusedCfg {
   static_assert(HD == 64 || HD == 96, "fused attention backward: head_dim 64 or 96");
   static constexpr int ATOMS = (HD + 63) / 64;
@@ -87,13 +92,15 @@ struct FusedCfg {
   static constexpr int T128 = ATOMS * A128;
   static constexpr int T64 = ATOMS * A64;
   // (Q, dO, stats) ring depth (a stage is released when the dV/dK MMAs of its tile complete)
-  static constexpr int NS = HD > 64 ? 3 : 5;
+  static constexpr int NS = STORED ? 2 : (HD > 64 ? 3 : 5);
   static constexpr int K_OFF = 0, V_OFF = T128, QD_OFF = 2 * T128;
   static constexpr int ST_OFF = QD_OFF + NS * 2 * T64;          // [NS][-lse·log2e x64][-rowdot x64]
   // dSᵀ [2 tile parities][128 x 64 bf16]
   static constexpr int DS_OFF = (ST_OFF + NS * 512 + 1023) / 1024 * 1024;
   static constexpr int DS_BYTES = 128 * 128;
-  static constexpr int BAR_OFF = DS_OFF + 2 * DS_BYTES;
+  static constexpr int PM_OFF = DS_OFF + 2 * DS_BYTES;            // STORED: [NS][P | mask]
+  static constexpr int P_TILE = 64 * 128 * 2, M_TILE = 64 * 128, PM_STAGE = P_TILE + M_TILE;
+  static constexpr int BAR_OFF = PM_OFF + (STORED ? NS * PM_STAGE : 0);
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   // TMEM: Sᵀ [0,128) (2 x 64), dPᵀ [128,256), dV, dK (HD each), dQᵀ (64)
   static constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + HD;
@@ -102,13 +109,15 @@ struct FusedCfg {
   static constexpr int NQW = (HD + 31) / 32;  // dQ reader warps
 };
 
-template <int HD, bool CAUSAL, bool KT>
+template <int HD, bool CAUSAL, bool KT, bool STORED>
 __global__ void __launch_bounds__(512, 1)
     fa_bwd_fused_umma(const __grid_constant__ CUtensorMap map_kv,  // qkv, 128-row boxes
                       const __grid_constant__ CUtensorMap map_q,   // qkv, 64-row boxes
                       const __grid_constant__ CUtensorMap map_do,  // dO, 64-row boxes
+                      const __grid_constant__ CUtensorMap map_sm,  // STORED: P, box {128 k, 64 q}
+                      const __grid_constant__ CUtensorMap map_mk,  // STORED: mask, same box
                       AttnArgs a, bf16* __restrict__ dqkv) {
-  using C = FusedCfg<HD>;
+  using C = FusedCfg<HD, STORED>;
   constexpr int NS = C::NS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -181,11 +190,16 @@ __global__ void __launch_bounds__(512, 1)
         uint8_t* Dt = Qt + C::T64;
         float* stt = reinterpret_cast<float*>(smem + C::ST_OFF + st * 512);
         const int qb = q_start + it * 64;
-        mbar_expect_tx(&qd_full[st], 2 * C::T64 + 512);
+        mbar_expect_tx(&qd_full[st], 2 * C::T64 + 512 + (STORED ? C::PM_STAGE : 0));
 #pragma unroll
         for (int at = 0; at < C::ATOMS; ++at) {
           tma_load_3d(Qt + at * C::A64, &map_q, &qd_full[st], qcol + 64 * at, bj, qb);
           tma_load_3d(Dt + at * C::A64, &map_do, &qd_full[st], dcol + 64 * at, bj, qb);
+        }
+        if constexpr (STORED) {  // P and mask of (these 64 queries, the CTA's 128 keys)
+          uint8_t* pm = smem + C::PM_OFF + st * C::PM_STAGE;
+          tma_load_3d(pm, &map_sm, &qd_full[st], k0, qb, hb);
+          tma_load_3d(pm + C::P_TILE, &map_mk, &qd_full[st], k0, qb, hb);
         }
         bulk_load(stt, nlse + brow + qb, 256, &qd_full[st]);
         bulk_load(stt + 64, ndel + brow + qb, 256, &qd_full[st]);
@@ -209,8 +223,9 @@ __global__ void __launch_bounds__(512, 1)
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t oa = (kk >> 2) * C::A128 + (kk & 3) * 32;
           const uint32_t ob = (kk >> 2) * C::A64 + (kk & 3) * 32;
-          umma_bf16_w(tmem + C::S_COL + sb * 64, smem_desc(ka + oa, 16, 1024),
-                    smem_desc(qb + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
+          if constexpr (!STORED)
+            umma_bf16_w(tmem + C::S_COL + sb * 64, smem_desc(ka + oa, 16, 1024),
+                        smem_desc(qb + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
           umma_bf16_w(tmem + C::DP_COL + sb * 64, smem_desc(va + oa, 16, 1024),
                     smem_desc(db + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
         }
@@ -302,7 +317,7 @@ __global__ void __launch_bounds__(512, 1)
     // layout directly; otherwise each lane loads (its query, the warp's 32 keys) and the warp
     // transposes the 32 x 32 block. Loaded one own tile ahead.
     auto kword = [&](int it, int h) -> uint32_t {
-      if (!drop_on) return 0xffffffffu;
+      if (STORED || !drop_on) return 0xffffffffu;
       if (it >= nq) return 0u;
       const int qw = (q_start + it * 64 + 32 * h) >> 5;
       if constexpr (KT) return kbits[((int64_t)hb * (S >> 5) + qw) * S + key];
@@ -330,7 +345,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
         uint32_t rs[32], rp[32];
-        tmem_ld32_nw(tl + C::S_COL + sb * 64 + h * 32, rs);
+        if constexpr (!STORED) tmem_ld32_nw(tl + C::S_COL + sb * 64 + h * 32, rs);
         tmem_ld32_nw(tl + C::DP_COL + sb * 64 + h * 32, rp);
         tmem_wait();
         if (trw) TRACE(h ? 8 : 6, it);
@@ -357,11 +372,27 @@ __global__ void __launch_bounds__(512, 1)
             }
             const uint64_t nl2 = ((uint64_t)l4[(i & 3) + 1] << 32) | l4[i & 3];
             const uint64_t nd2 = ((uint64_t)d4[(i & 3) + 1] << 32) | d4[i & 3];
-            float s0, s1;
-            f32x2_split(ffma2(f32x2(__uint_as_float(rs[i]), __uint_as_float(rs[i + 1])), sl2x2, nl2),
-                        s0, s1);
-            float p0 = ex2(s0), p1 = ex2(s1);
-            bool k0b = (kt >> i) & 1u, k1b = (kt >> (i + 1)) & 1u;
+            float p0, p1;
+            bool k0b, k1b;
+            if constexpr (STORED) {  // [64 q][128 k] tiles: query 32h + i, this thread's key
+              const bf16* Pt = reinterpret_cast<const bf16*>(smem + C::PM_OFF + qs * C::PM_STAGE);
+              const uint8_t* Mt = smem + C::PM_OFF + qs * C::PM_STAGE + C::P_TILE;
+              const int qi = 32 * h + i;
+              p0 = __bfloat162float(Pt[qi * 128 + row]);
+              p1 = __bfloat162float(Pt[(qi + 1) * 128 + row]);
+              k0b = Mt[qi * 128 + row] != 0;
+              k1b = Mt[(qi + 1) * 128 + row] != 0;
+              (void)nl2;
+              (void)sl2x2;
+            } else {
+              float s0, s1;
+              f32x2_split(ffma2(f32x2(__uint_as_float(rs[i]), __uint_as_float(rs[i + 1])), sl2x2, nl2),
+                          s0, s1);
+              p0 = ex2(s0);
+              p1 = ex2(s1);
+              k0b = (kt >> i) & 1u;
+              k1b = (kt >> (i + 1)) & 1u;
+            }
             if constexpr (kMasked) {
               const bool v0 = !(CAUSAL && key > q0h + i);
               const bool v1 = !(CAUSAL && key > q0h + i + 1);
@@ -485,7 +516,7 @@ __global__ void fa_bwd_prep(AttnArgs a, const bf16* __restrict__ dout) {
   acc += __shfl_xor_sync(0xffffffffu, acc, 1);
   acc += __shfl_xor_sync(0xffffffffu, acc, 2);
   if (sub == 0 && r < nrows) {
-    a.bstat[row] = -a.lse[row] * kLog2e;
+    a.bstat[row] = a.lse != nullptr ? -a.lse[row] * kLog2e : 0.f;  // (unused when STORED)
     a.bstat[nrows + row] = -acc;
   }
 }
@@ -510,12 +541,12 @@ __global__ void fa_bwd_dq_store(AttnArgs a, bf16* __restrict__ dqkv) {
                  pack_bf16(y.x * sc, y.y * sc), pack_bf16(y.z * sc, y.w * sc));
 }
 
-template <int HD, bool CAUSAL, bool KT>
+template <int HD, bool CAUSAL, bool KT, bool STORED>
 void launch_fused(const AttnArgs& a, const bf16* dout, bf16* dqkv, cudaStream_t st) {
-  using C = FusedCfg<HD>;
+  using C = FusedCfg<HD, STORED>;
   static_assert(C::SMEM <= 232448, "fused attention backward: smem over the limit");
   static bool once = [] {
-    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_fused_umma<HD, CAUSAL, KT>,
+    SPL_CUDA(cudaFuncSetAttribute(fa_bwd_fused_umma<HD, CAUSAL, KT, STORED>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     return true;
   }();
@@ -526,6 +557,11 @@ void launch_fused(const AttnArgs& a, const bf16* dout, bf16* dqkv, cudaStream_t 
   const CUtensorMap m128 = attn_seq_map(a.qkv, a.ld, a.b, a.s, a.ld, 128);
   const CUtensorMap m64 = attn_seq_map(a.qkv, a.ld, a.b, a.s, a.ld, 64);
   const CUtensorMap d64 = attn_seq_map(dout, a.ldo, a.b, a.s, a.ldo, 64);
+  CUtensorMap msm = m128, mmk = m128;  // unused unless STORED
+  if (STORED) {
+    msm = interior_map(a.sm, false, a.s, a.lh * a.b, 128, 64, false);
+    mmk = interior_map(a.mask, true, a.s, a.lh * a.b, 128, 64, false);
+  }
   dim3 grid((unsigned)(a.s / 128), (unsigned)(a.lh * a.b));
   static unsigned long long* trace = [] {
     const char* e = std::getenv("SPL_ATTN_TRACE");
@@ -537,7 +573,7 @@ void launch_fused(const AttnArgs& a, const bf16* dout, bf16* dqkv, cudaStream_t 
     }
     return p;
   }();
-  fa_bwd_fused_umma<HD, CAUSAL, KT><<<grid, 512, C::SMEM, st>>>(m128, m64, d64, a, dqkv);
+  fa_bwd_fused_umma<HD, CAUSAL, KT, STORED><<<grid, 512, C::SMEM, st>>>(m128, m64, d64, msm, mmk, a, dqkv);
   SPL_CHECK_LAUNCH();
   static int traced = 0;
   if (trace != nullptr && traced++ == 2 && grid.x > kTraceX && grid.y > kTraceY) {
@@ -566,9 +602,12 @@ bool attn_bwd_fused_supported(const AttnArgs& a) {
     const char* e = std::getenv("SPL_ATTN_DETERMINISTIC");
     return e != nullptr && e[0] == '1';
   }();
-  return !off && a.sm == nullptr && a.dq_acc != nullptr && a.bstat != nullptr &&
-         (a.hd == 64 || a.hd == 96) && a.s % 128 == 0 && a.s >= 128 && a.lse != nullptr &&
-         (a.keepbits != nullptr || a.drop.thresh == 0) && a.ld % 8 == 0 && a.ldo % 8 == 0 &&
+  const bool regime_ok = a.sm == nullptr
+                             ? (a.lse != nullptr && (a.keepbits != nullptr || a.drop.thresh == 0))
+                             : (a.mask != nullptr && ((uintptr_t)a.sm & 15) == 0 &&
+                                ((uintptr_t)a.mask & 15) == 0);
+  return !off && regime_ok && a.dq_acc != nullptr && a.bstat != nullptr &&
+         (a.hd == 64 || a.hd == 96) && a.s % 128 == 0 && a.s >= 128 && a.ld % 8 == 0 && a.ldo % 8 == 0 &&
          a.qoff % 8 == 0 && ((uintptr_t)a.qkv & 15) == 0 && ((uintptr_t)a.o & 15) == 0 &&
          ((uintptr_t)a.dq_acc & 15) == 0 && ((uintptr_t)a.bstat & 15) == 0 && a.s < (1 << 30);
 }
@@ -577,12 +616,15 @@ void attn_bwd_fused(const AttnArgs& a, const void* dout, void* dqkv, cudaStream_
   const bf16* d = static_cast<const bf16*>(dout);
   bf16* g = static_cast<bf16*>(dqkv);
 #define SPL_FUSED_CASE(HDX)                                                              \
-  if (a.keep_t) {                                                                        \
-    if (a.causal) launch_fused<HDX, true, true>(a, d, g, st);                            \
-    else launch_fused<HDX, false, true>(a, d, g, st);                                    \
+  if (a.sm != nullptr) {                                                                 \
+    if (a.causal) launch_fused<HDX, true, false, true>(a, d, g, st);                     \
+    else launch_fused<HDX, false, false, true>(a, d, g, st);                             \
+  } else if (a.keep_t) {                                                                 \
+    if (a.causal) launch_fused<HDX, true, true, false>(a, d, g, st);                     \
+    else launch_fused<HDX, false, true, false>(a, d, g, st);                             \
   } else {                                                                               \
-    if (a.causal) launch_fused<HDX, true, false>(a, d, g, st);                           \
-    else launch_fused<HDX, false, false>(a, d, g, st);                                   \
+    if (a.causal) launch_fused<HDX, true, false, false>(a, d, g, st);                    \
+    else launch_fused<HDX, false, false, false>(a, d, g, st);                            \
   }
   if (a.hd == 64) {
     SPL_FUSED_CASE(64)

@@ -834,10 +834,9 @@ class Layer final : public LayerBase {
       // side stream at the start of every forward and backward call
       if (std::is_same_v<T, bf16> && d_.dropout_p > 0.0)
         R.keepbits = alloc<uint32_t>(k::keepbits_words(lh_, b_, s_), kWork, r);
-      // fused attention backward (recompute regimes, bf16, head_dim 64/96): fp32 dQ
-      // accumulator and per-row statistics
-      if (std::is_same_v<T, bf16> && kind_ != SPL_RECOMPUTE_NONE && (hd_ == 64 || hd_ == 96) &&
-          s_ % 128 == 0) {
+      // fused attention backward (bf16, head_dim 64/96; recompute regimes and the stored
+      // interior): fp32 dQ accumulator and per-row statistics
+      if (std::is_same_v<T, bf16> && (hd_ == 64 || hd_ == 96) && s_ % 128 == 0) {
         if (!dq_acc) {
           dq_acc = alloc<float>(lh_ * b_ * s_ * hd_, kWork, r);
           bstat = alloc<float>(2 * lh_ * b_ * s_, kWork, r);
