@@ -67,7 +67,12 @@ struct PpCfg {
   static constexpr int O_COL = 256;
 };
 
-template <int HD, bool CAUSAL>
+// MAT (no-recompute regime): two passes over the keys — pass 1 the row max and sum (Q·Kᵀ and
+// exponentials only), pass 2 the normalised P = softmax_out, the mask (the raw keep bit at every
+// position, block.cpp:392-394) and P̃ = P·mask/(1-p) = softmax_dropout_out, written to the
+// stored interior with 32-byte stores, and O += P̃·V (O needs no final rescale). Every key
+// tile is visited, causal ones included (the stored mask carries all bits).
+template <int HD, bool CAUSAL, bool MAT>
 __global__ void __launch_bounds__(384, 1)
     fa_fwd_pp(const __grid_constant__ CUtensorMap map_qkv, AttnArgs a) {
   using Cfg = PpCfg<HD>;
@@ -88,9 +93,10 @@ __global__ void __launch_bounds__(384, 1)
   const int hl = blockIdx.y / (int)a.b, bj = blockIdx.y % (int)a.b;
   const int S = (int)a.s;
   const bool two = q0 + 128 < S;
-  const int nkv0 = CAUSAL ? min(S, q0 + 128) / 128 : S / 128;
-  const int nkv1 = two ? (CAUSAL ? min(S, q0 + 256) / 128 : S / 128) : 0;
+  const int nkv0 = (CAUSAL && !MAT) ? min(S, q0 + 128) / 128 : S / 128;
+  const int nkv1 = two ? ((CAUSAL && !MAT) ? min(S, q0 + 256) / 128 : S / 128) : 0;
   const int nkv = max(nkv0, nkv1);
+  constexpr int PASSES = MAT ? 2 : 1;  // MAT: nkv0 == nkv1 (or tile 1 empty)
   const int qcol = (int)(a.qoff + (int64_t)hl * HD), kcol = (int)(a.koff + (int64_t)hl * HD),
             vcol = (int)(a.voff + (int64_t)hl * HD);
   if (threadIdx.x == 0) {
@@ -121,16 +127,18 @@ __global__ void __launch_bounds__(384, 1)
       if (two)
         for (int at = 0; at < Cfg::ATOMS; ++at)
           tma_load_3d(Qs + Cfg::TILE + at * kAtomBytes, &map_qkv, q_full, qcol + 64 * at, bj, q0 + 128);
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j % Cfg::KVS;
-        mbar_wait(&kv_empty[st], ((j / Cfg::KVS) & 1) ^ 1);
+      for (int u = 0; u < PASSES * nkv; ++u) {  // step u: key tile u % nkv of pass u / nkv
+        const int st = u % Cfg::KVS, j = u % nkv;
+        const bool with_v = u >= (PASSES - 1) * nkv;  // V only in the last pass
+        mbar_wait(&kv_empty[st], ((u / Cfg::KVS) & 1) ^ 1);
         uint8_t* Kt = KVs + st * 2 * Cfg::TILE;
         uint8_t* Vt = Kt + Cfg::TILE;
-        mbar_expect_tx(&kv_full[st], 2 * Cfg::TILE);
+        mbar_expect_tx(&kv_full[st], (with_v ? 2 : 1) * Cfg::TILE);
         for (int at = 0; at < Cfg::ATOMS; ++at)
           tma_load_3d(Kt + at * kAtomBytes, &map_qkv, &kv_full[st], kcol + 64 * at, bj, j * 128);
-        for (int at = 0; at < Cfg::ATOMS; ++at)
-          tma_load_3d(Vt + at * kAtomBytes, &map_qkv, &kv_full[st], vcol + 64 * at, bj, j * 128);
+        if (with_v)
+          for (int at = 0; at < Cfg::ATOMS; ++at)
+            tma_load_3d(Vt + at * kAtomBytes, &map_qkv, &kv_full[st], vcol + 64 * at, bj, j * 128);
       }
     } else if (warp == 1) {
       // ---------------------------------------------- MMA issuer (whole warp, elected lane)
@@ -153,28 +161,47 @@ __global__ void __launch_bounds__(384, 1)
       };
       auto issue_pv = [&](int t, int j) {  // O_t += P̃_t (TMEM, over S_t's first 64 columns) · V(j)
         const int st = j % Cfg::KVS;
+        const int jp = MAT ? j - nkv : j;  // key tile within the PV pass
         mbar_wait(&p_full[t], j & 1);
         tc_fence_after();
         const uint32_t vb = smem_u32(KVs + st * 2 * Cfg::TILE + Cfg::TILE);
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk)
           umma_bf16_ts_w(tmem + Cfg::O_COL + t * HD, tmem + t * 128 + kk * 8,
-                         smem_desc(vb + kk * 2048, kAtomBytes, 1024), idesc_o, (j | kk) != 0 ? 1u : 0u);
+                         smem_desc(vb + kk * 2048, kAtomBytes, 1024), idesc_o, (jp | kk) != 0 ? 1u : 0u);
       };
+      // step u of tile t (u < PASSES·n_t): S_t(u) from stage u; in the last pass P̃_t(u)·V,
+      // in MAT's first pass only the wait for the softmax to have read S_t(u)
       if (nkv0 > 0) issue_s(0, 0);
       if (nkv1 > 0) issue_s(1, 0);
-      for (int j = 0; j < nkv; ++j) {
-        if (j < nkv0) {
-          issue_pv(0, j);
-          if (j + 1 < nkv0) issue_s(0, j + 1);
-          else umma_commit_w(&o_full[0]);
+      if constexpr (MAT) {
+        for (int u = 0; u < 2 * nkv; ++u) {
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const int n = 2 * (t == 0 ? nkv0 : nkv1);
+            if (u < n) {
+              if (u >= n / 2) issue_pv(t, u);
+              else mbar_wait(&p_full[t], u & 1);
+              if (u + 1 < n) issue_s(t, u + 1);
+              else umma_commit_w(&o_full[t]);
+            }
+          }
+          umma_commit_w(&kv_empty[u % Cfg::KVS]);  // both tiles' products of stage u issued
         }
-        if (j < nkv1) {
-          issue_pv(1, j);
-          if (j + 1 < nkv1) issue_s(1, j + 1);
-          else umma_commit_w(&o_full[1]);
+      } else {
+        for (int j = 0; j < nkv; ++j) {
+          if (j < nkv0) {
+            issue_pv(0, j);
+            if (j + 1 < nkv0) issue_s(0, j + 1);
+            else umma_commit_w(&o_full[0]);
+          }
+          if (j < nkv1) {
+            issue_pv(1, j);
+            if (j + 1 < nkv1) issue_s(1, j + 1);
+            else umma_commit_w(&o_full[1]);
+          }
+          umma_commit_w(&kv_empty[j % Cfg::KVS]);  // both tiles' products of stage j issued
         }
-        umma_commit_w(&kv_empty[j % Cfg::KVS]);  // both tiles' products of stage j issued
       }
     }
   } else {
@@ -197,7 +224,121 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t l2 = f32x2(0.f, 0.f);
     uint4 wnext = make_uint4(~0u, ~0u, ~0u, ~0u);
     if (drop_on && nk > 0) wnext = kw[0];
-    for (int j = 0; j < nk; ++j) {
+    auto load_s = [&](uint32_t (&r)[128]) {
+      tmem_ld32_nw(tl + scol, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+      tmem_ld32_nw(tl + scol + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+      tmem_ld32_nw(tl + scol + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
+      tmem_ld32_nw(tl + scol + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
+      tmem_wait();
+    };
+    auto row_max = [&](const uint32_t (&r)[128]) {
+      float c0 = max3f(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]));
+      float c1 = max3f(__uint_as_float(r[3]), __uint_as_float(r[4]), __uint_as_float(r[5]));
+#pragma unroll
+      for (int i = 6; i < 126; i += 4) {
+        c0 = max3f(c0, __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+        c1 = max3f(c1, __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+      }
+      return max3f(c0, c1, fmaxf(__uint_as_float(r[126]), __uint_as_float(r[127])));
+    };
+    if constexpr (MAT) {
+      // ---- pass 1: exact row max and sum (no O to rescale: the reference point always moves)
+      for (int j = 0; j < nk; ++j) {
+        mbar_wait(&s_full[t], j & 1);
+        tc_fence_after();
+        uint32_t r[128];
+        load_s(r);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);  // S_t read: the next Q·Kᵀ may overwrite it
+        if (CAUSAL && j * 128 + 127 > q0t) {
+          const int k0 = j * 128;
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
+            if (k0 + i > qr) r[i] = __float_as_uint(-INFINITY);
+        }
+        const float mt = row_max(r) * sl2;
+        if (mt > m_used) {
+          if (m_used != -INFINITY) {
+            const float f = ex2f(m_used - mt);
+            l2 = fmul2(l2, f32x2(f, f));
+          }
+          m_used = mt;
+        }
+        if (m_used == -INFINITY) continue;  // every key so far masked
+        const uint64_t sl2x2 = f32x2(sl2, sl2), nmm2 = f32x2(-m_used, -m_used);
+#pragma unroll
+        for (int i = 0; i < 128; i += 2) {
+          float x0, x1;
+          f32x2_split(ffma2(f32x2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2, nmm2), x0, x1);
+          l2 = fadd2(l2, f32x2(ex2f(x0), ex2f(x1)));
+        }
+      }
+      // ---- pass 2: normalised P, mask, P̃ -> the stored interior; P̃ -> TMEM for O += P̃·V
+      float le, lo;
+      f32x2_split(l2, le, lo);
+      const float inv_l = 1.f / (le + lo), ik = a.drop.inv_keep;
+      const float mm = m_used == -INFINITY ? 0.f : m_used;
+      const uint64_t sl2x2 = f32x2(sl2, sl2), nmm2 = f32x2(-mm, -mm);
+      const int64_t irow = (brow + qr) * (int64_t)S;
+      for (int j = 0; j < nk; ++j) {
+        const uint4 wcur = wnext;
+        if (drop_on && j + 1 < nk) wnext = kw[j + 1];
+        const int u = nk + j;
+        mbar_wait(&s_full[t], u & 1);
+        tc_fence_after();
+        uint32_t r[128];
+        load_s(r);
+        const uint32_t words[4] = {wcur.x, wcur.y, wcur.z, wcur.w};
+        const int k0 = j * 128;
+        const bool diag = CAUSAL && k0 + 127 > q0t;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t pk[32], pm[32];
+#pragma unroll
+          for (int i = 64 * hh; i < 64 * hh + 64; i += 2) {
+            float x0, x1;
+            f32x2_split(ffma2(f32x2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2, nmm2), x0, x1);
+            float p0 = ex2f(x0) * inv_l, p1 = ex2f(x1) * inv_l;
+            if (CAUSAL) {
+              if (diag && k0 + i > qr) p0 = 0.f;
+              if (diag && k0 + i + 1 > qr) p1 = 0.f;
+            }
+            const uint32_t w = words[i >> 5];
+            const float d0 = (w >> (i & 31)) & 1u ? p0 * ik : 0.f;
+            const float d1 = (w >> ((i + 1) & 31)) & 1u ? p1 * ik : 0.f;
+            pm[(i - 64 * hh) >> 1] = pack_bf16x2(p0, p1);
+            pk[(i - 64 * hh) >> 1] = pack_bf16x2(d0, d1);
+          }
+          uint8_t* smo = reinterpret_cast<uint8_t*>(static_cast<bf16*>(a.sm) + irow + k0 + 64 * hh);
+          uint8_t* sdo = reinterpret_cast<uint8_t*>(static_cast<bf16*>(a.sd) + irow + k0 + 64 * hh);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            st_v8(smo + 32 * v, pm[8 * v], pm[8 * v + 1], pm[8 * v + 2], pm[8 * v + 3], pm[8 * v + 4],
+                  pm[8 * v + 5], pm[8 * v + 6], pm[8 * v + 7]);
+            st_v8(sdo + 32 * v, pk[8 * v], pk[8 * v + 1], pk[8 * v + 2], pk[8 * v + 3], pk[8 * v + 4],
+                  pk[8 * v + 5], pk[8 * v + 6], pk[8 * v + 7]);
+          }
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {  // 32 keys -> 32 mask bytes (the raw keep bit)
+            const uint32_t wb = words[2 * hh + v];
+            uint32_t q8[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const uint32_t bits = (wb >> (4 * e)) & 0xFu;
+              q8[e] = (bits & 1u) | ((bits & 2u) << 7) | ((bits & 4u) << 14) | ((bits & 8u) << 21);
+            }
+            st_v8(a.mask + irow + k0 + 64 * hh + 32 * v, q8[0], q8[1], q8[2], q8[3], q8[4], q8[5],
+                  q8[6], q8[7]);
+          }
+          tmem_st32u(tl + scol + 32 * hh, pk);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+      }
+    }
+    for (int j = 0; j < (MAT ? 0 : nk); ++j) {
       const uint4 wcur = wnext;
       if (drop_on && j + 1 < nk) wnext = kw[j + 1];  // next tile's keep words, one tile ahead
       mbar_wait(&s_full[t], j & 1);
@@ -271,7 +412,7 @@ __global__ void __launch_bounds__(384, 1)
       float le, lo;
       f32x2_split(l2, le, lo);
       const float l = le + lo;
-      const float oscale = a.drop.inv_keep / l;
+      const float oscale = MAT ? 1.f : a.drop.inv_keep / l;  // MAT: P̃ was normalised
       mbar_wait(&o_full[t], 0);
       tc_fence_after();
       // O rows are HD·2 bytes apart from the next query's by b·ldo elements: one thread per row
@@ -314,17 +455,17 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
-template <int HD, bool CAUSAL>
+template <int HD, bool CAUSAL, bool MAT>
 void launch_pp(const AttnArgs& a, cudaStream_t st) {
   using Cfg = PpCfg<HD>;
   static bool once = [] {
-    SPL_CUDA(cudaFuncSetAttribute(fa_fwd_pp<HD, CAUSAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    SPL_CUDA(cudaFuncSetAttribute(fa_fwd_pp<HD, CAUSAL, MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     return true;
   }();
   (void)once;
   const CUtensorMap mq = attn_seq_map(a.qkv, a.ld, a.b, a.s, a.ld, 128);
   dim3 grid((unsigned)((a.s + 255) / 256), (unsigned)(a.lh * a.b));
-  fa_fwd_pp<HD, CAUSAL><<<grid, 384, Cfg::SMEM, st>>>(mq, a);
+  fa_fwd_pp<HD, CAUSAL, MAT><<<grid, 384, Cfg::SMEM, st>>>(mq, a);
   SPL_CHECK_LAUNCH();
 }
 
@@ -335,7 +476,11 @@ bool attn_fwd_pp_supported(const AttnArgs& a) {
     const char* e = std::getenv("SPL_ATTN_FWD_PP");
     return e != nullptr && e[0] == '0';
   }();
-  return !off && a.sm == nullptr && a.lse != nullptr && a.keep_t == 0 &&
+  const bool regime_ok = a.sm == nullptr
+                             ? a.lse != nullptr
+                             : (a.mask != nullptr && a.sd != nullptr && ((uintptr_t)a.sm & 31) == 0 &&
+                                ((uintptr_t)a.sd & 31) == 0 && ((uintptr_t)a.mask & 31) == 0);
+  return !off && regime_ok && a.keep_t == 0 &&
          (a.hd == 64 || a.hd == 96 || a.hd == 128) && a.s % 128 == 0 && a.s < (1 << 30) &&
          a.ld % 8 == 0 && a.ldo % 8 == 0 && ((uintptr_t)a.qkv & 15) == 0 &&
          ((uintptr_t)a.o & 15) == 0 && (a.keepbits != nullptr || a.drop.thresh == 0) &&
@@ -344,9 +489,15 @@ bool attn_fwd_pp_supported(const AttnArgs& a) {
 
 void attn_fwd_pp(const AttnArgs& a, cudaStream_t st) {
   switch (a.hd) {
-    case 64: return a.causal ? launch_pp<64, true>(a, st) : launch_pp<64, false>(a, st);
-    case 96: return a.causal ? launch_pp<96, true>(a, st) : launch_pp<96, false>(a, st);
-    case 128: return a.causal ? launch_pp<128, true>(a, st) : launch_pp<128, false>(a, st);
+#define SPL_PP_CASE(HDX)                                                                    \
+  case HDX:                                                                                 \
+    if (a.sm != nullptr)                                                                    \
+      return a.causal ? launch_pp<HDX, true, true>(a, st) : launch_pp<HDX, false, true>(a, st); \
+    return a.causal ? launch_pp<HDX, true, false>(a, st) : launch_pp<HDX, false, false>(a, st);
+    SPL_PP_CASE(64)
+    SPL_PP_CASE(96)
+    SPL_PP_CASE(128)
+#undef SPL_PP_CASE
     default: raise(3, "attn_fwd_pp: unsupported head_dim");
   }
 }
