@@ -495,3 +495,24 @@ def test_bf16_no_dropout_tcgen05_attention(spl, orc, causal):
     assert rel_l2(dx, ref.dx) <= 1e-2
     grads_close(orc, cfg.hidden, g, ref.grads, 2e-2)
     L.close()
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_bf16_stored_interior_vs_oracle(spl, orc, causal):
+    """No-recompute regime, bf16, head_dim 64, s % 128 == 0: the stored interior written by the
+    two-pass ping-pong forward (32-byte row stores) — softmax_out, the raw mask byte at every
+    position (bit-exact) and softmax_dropout_out — against the oracle's interior."""
+    shape = dict(heads=4, hidden=256, seq=256, batch=2)
+    cfg, x, dy, p = make_case(orc, shape, causal=causal, key=12)
+    ref = orc.seqpar_layer(cfg, 1, p, x, dy, want_interior=True)
+    L, y, dx, g = run(spl, cfg, 1, p, x, dy, "none", dtype="bf16")
+    n = ref.interior[0].size
+    sm = L.saved(0, "softmax_out", (n,)).reshape(ref.interior[0].shape)
+    mk = L.saved(0, "softmax_dropout_mask", (n,)).reshape(ref.interior[1].shape)
+    sd = L.saved(0, "softmax_dropout_out", (n,)).reshape(ref.interior[2].shape)
+    assert np.array_equal(mk, ref.interior[1])
+    # bf16 storage: one rounding (2^-9 relative) of values <= 1 (P) and <= 1/(1-p) (P-tilde)
+    assert np.max(np.abs(sm - ref.interior[0])) <= 4e-3
+    assert np.max(np.abs(sd - ref.interior[2])) <= 5e-3
+    assert rel_l2(y, ref.y) <= 1e-2
+    L.close()
