@@ -61,6 +61,13 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// L2 prefetch of a TMA box (no shared memory, no barrier): the stored-interior tiles come from
+// DRAM, and the 2-stage ring alone leaves their latency exposed.
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
   uint32_t m = 0x0000ffffu;
 #pragma unroll
@@ -200,6 +207,15 @@ __global__ void __launch_bounds__(512, 1)
           uint8_t* pm = smem + C::PM_OFF + st * C::PM_STAGE;
           tma_load_3d(pm, &map_sm, &qd_full[st], k0, qb, hb);
           tma_load_3d(pm + C::P_TILE, &map_mk, &qd_full[st], k0, qb, hb);
+          if (it == 0)  // warm L2 with the tiles the ring reaches next
+            for (int f = 1; f < 4 && f < nq; ++f) {
+              tma_prefetch_3d(&map_sm, k0, qb + 64 * f, hb);
+              tma_prefetch_3d(&map_mk, k0, qb + 64 * f, hb);
+            }
+          if (it + 4 < nq) {
+            tma_prefetch_3d(&map_sm, k0, qb + 256, hb);
+            tma_prefetch_3d(&map_mk, k0, qb + 256, hb);
+          }
         }
         bulk_load(stt, nlse + brow + qb, 256, &qd_full[st]);
         bulk_load(stt + 64, ndel + brow + qb, 256, &qd_full[st]);

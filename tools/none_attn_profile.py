@@ -9,7 +9,7 @@ L = spl.SeqparLayer(cfg, 1, "none", True, "bf16", check_finite=False)
 L.init_params(1234)
 x = [(torch.rand(L.shard_shape(), device="cuda") * 2 - 1).to(torch.bfloat16)]
 dy = [(torch.rand(L.shard_shape(), device="cuda") * 2 - 1).to(torch.bfloat16)]
-for _ in range(2):
+for _ in range(int(os.environ.get("STEPS", "2"))):
     L.forward(x)
     L.backward(dy)
 torch.cuda.synchronize()
