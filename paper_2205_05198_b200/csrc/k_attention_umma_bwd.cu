@@ -36,6 +36,14 @@ static EncodeFnB encode_fn_bwd() {
   return fn;
 }
 
+// L2 prefetch of a TMA box (no shared memory): the stored-interior tiles stream from DRAM
+// through shallow rings (1-2 stages), so they are warmed in L2 a few tiles ahead.
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
 namespace {
 
 using namespace tc;
@@ -199,6 +207,10 @@ __global__ void __launch_bounds__(320, 1)
           uint8_t* St = smem + SMM_OFF + st * (SMT + MKT);
           tma_load_3d(St, &map_sm, &qd_full[st], k0, qb, (int)blockIdx.y);
           tma_load_3d(St + SMT, &map_mk, &qd_full[st], k0, qb, (int)blockIdx.y);
+          for (int f = it == 0 ? 1 : 4; f <= 4 && it + f < nq; ++f) {  // warm L2 4 tiles ahead
+            tma_prefetch_3d(&map_sm, k0, qb + 64 * f, (int)blockIdx.y);
+            tma_prefetch_3d(&map_mk, k0, qb + 64 * f, (int)blockIdx.y);
+          }
         }
       }
     }
@@ -575,6 +587,10 @@ __global__ void __launch_bounds__(320, 1)
           uint8_t* St = smem + SMM_OFF + st * (SMT + MKT);  // st = it % NS here
           tma_load_3d(St, &map_sm, &kv_full[st], it * 64, q0, (int)blockIdx.y);
           tma_load_3d(St + SMT, &map_mk, &kv_full[st], it * 64, q0, (int)blockIdx.y);
+          for (int f = it == 0 ? 1 : 4; f <= 4 && it + f < nkv; ++f) {  // warm L2 4 tiles ahead
+            tma_prefetch_3d(&map_sm, (it + f) * 64, q0, (int)blockIdx.y);
+            tma_prefetch_3d(&map_mk, (it + f) * 64, q0, (int)blockIdx.y);
+          }
         }
       }
     }
