@@ -437,13 +437,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs), bytes counted on the leader's full[s]
-      int it = 0;
-      const uint64_t pol_a = l2_hint ? l2_policy_evict_last() : l2_policy_evict_normal();
-      for (int tile = pair; tile < ntiles; tile += npairs) {
+      int it = 0, local = 0;
+      const uint64_t pol_a = (l2_hint & 1) ? l2_policy_evict_last() : l2_policy_evict_normal();
+      const bool ksnake = (l2_hint & 2) != 0;
+      for (int tile = pair; tile < ntiles; tile += npairs, ++local) {
         int mb, nb;
         tile_coords(tile, tiles_m, tiles_n, group, mb, nb);
         const int m0 = mb * 256 + 128 * (int)rank, n0 = nb * TN + (TN / 2) * (int)rank;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        // K snake: odd waves walk K backwards, so they start on the k-blocks the previous wave
+        // loaded last (still in L2) for the panels the two waves share
+        const bool rev = ksnake && (local & 1);
+        for (int kbi = 0; kbi < nk; ++kbi, ++it) {
+          const int kb = rev ? nk - 1 - kbi : kbi;
           const int s = it % P_STAGES;
           const uint32_t ph = (uint32_t)(it / P_STAGES) & 1u;
           mbar_wait(&empty_bar[s], ph ^ 1u);
@@ -687,10 +692,15 @@ void launch_pair(const GemmArgs& g, cudaStream_t st) {
   const int tiles_m = (int)((g.M + 255) / 256), tiles_n = (int)((g.N + TN - 1) / TN);
   const int ntiles = tiles_m * tiles_n;
   const int pairs = ntiles < kNumSMs / 2 ? ntiles : kNumSMs / 2;
-  const int group = pick_group(g.K, 256, TN, tiles_m, tiles_n, pairs);
+  int group = pick_group(g.K, 256, TN, tiles_m, tiles_n, pairs);
+  if (const char* e = std::getenv("SPL_GEMM_GROUP")) {  // dev sweeps (tools/gemm_group_sweep.py)
+    const int v = std::atoi(e);
+    if (v > 0) group = std::min(v, tiles_m);
+  }
   static const int l2_hint = [] {
     const char* e = std::getenv("SPL_GEMM_L2HINT");
-    return (e != nullptr && e[0] == '0') ? 0 : 1;
+    const char* k = std::getenv("SPL_GEMM_KSNAKE");
+    return ((e != nullptr && e[0] == '0') ? 0 : 1) | ((k != nullptr && k[0] == '0') ? 0 : 2);
   }();
   kern<<<2 * pairs, kThreads, P_SMEM, st>>>(maps, g, tiles_m, tiles_n, group, l2_hint);
   SPL_CHECK_LAUNCH();
