@@ -39,11 +39,36 @@ using namespace tc;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kAtomBytes = 128 * 128;
+constexpr int kPolyDefault = 4;  // SPL_ATTN_POLY default (see poly_period)
 
 __device__ __forceinline__ float ex2f(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// 2^x for a pair of x <= 0 (or -inf) on the FMA pipe instead of the MUFU (XU) pipe, which the
+// ncu capture of this kernel shows as its busiest (XU 52 % active vs FMA 17 %): x clamped to
+// -126 (p < 1 has exponent field 126, so j >= -126 keeps the sum's exponent field >= 0),
+// j = floor(x) by a round-down add of 1.5·2^23 (j sits in the sum's low mantissa bits),
+// 2^(x-j) by a degree-3 polynomial on [0, 1) (relative error <= 8.6e-5, far below the bf16
+// rounding of P̃), and j added into the exponent field: (t_bits << 23) == j << 23 (mod 2^32).
+// Clamped values give a value <= 2^-125 instead of 0: below any bf16 / fp32 sum's ulp.
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t x) {
+  float x0, x1;
+  f32x2_split(x, x0, x1);
+  const uint64_t xc = f32x2(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  uint64_t t;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(t) : "l"(xc), "l"(f32x2(12582912.f, 12582912.f)));
+  const uint64_t jf = fadd2(t, f32x2(-12582912.f, -12582912.f));  // exact
+  const uint64_t fr = ffma2(jf, f32x2(-1.f, -1.f), xc);             // x - j in [0, 1), exact
+  uint64_t p = ffma2(f32x2(0.07706602f, 0.07706602f), fr, f32x2(0.22764611f, 0.22764611f));
+  p = ffma2(p, fr, f32x2(0.69511652f, 0.69511652f));
+  p = ffma2(p, fr, f32x2(1.f, 1.f));  // p(0) = 1: the row maximum's exponential is exact
+  float p0, p1, t0, t1;
+  f32x2_split(p, p0, p1);
+  f32x2_split(t, t0, t1);
+  return f32x2(__uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23)),
+               __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23)));
 }
 __device__ __forceinline__ float max3f(float a, float b, float c) {
   float d;
@@ -72,7 +97,9 @@ struct PpCfg {
 // position, block.cpp:392-394) and P̃ = P·mask/(1-p) = softmax_dropout_out, written to the
 // stored interior with 32-byte stores, and O += P̃·V (O needs no final rescale). Every key
 // tile is visited, causal ones included (the stored mask carries all bits).
-template <int HD, bool CAUSAL, bool MAT>
+// PE: every PE-th element pair of the recompute loop takes its exponentials from ex2_poly2
+// (0: all on MUFU)
+template <int HD, bool CAUSAL, bool MAT, int PE = 0>
 __global__ void __launch_bounds__(384, 1)
     fa_fwd_pp(const __grid_constant__ CUtensorMap map_qkv, AttnArgs a) {
   using Cfg = PpCfg<HD>;
@@ -396,9 +423,23 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
       for (int i = 0; i < 128; i += 2) {
         float x0, x1;
-        f32x2_split(ffma2(f32x2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2, nmm2), x0, x1);
-        const float p0 = ex2f(x0), p1 = ex2f(x1);
-        l2 = fadd2(l2, f32x2(p0, p1));
+        const uint64_t x2 = ffma2(f32x2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sl2x2, nmm2);
+        float p0, p1;
+        if constexpr (PE > 0) {
+          if ((i >> 1) % PE == PE - 1) {
+            const uint64_t e2 = ex2_poly2(x2);
+            l2 = fadd2(l2, e2);
+            f32x2_split(e2, p0, p1);
+          } else {
+            f32x2_split(x2, x0, x1);
+            p0 = ex2f(x0), p1 = ex2f(x1);
+            l2 = fadd2(l2, f32x2(p0, p1));
+          }
+        } else {
+          f32x2_split(x2, x0, x1);
+          p0 = ex2f(x0), p1 = ex2f(x1);
+          l2 = fadd2(l2, f32x2(p0, p1));
+        }
         const uint32_t w = words[i >> 5];
         pk[i >> 1] = pack_bf16x2((w >> (i & 31)) & 1u ? p0 : 0.f, (w >> ((i + 1) & 31)) & 1u ? p1 : 0.f);
       }
@@ -455,18 +496,42 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
-template <int HD, bool CAUSAL, bool MAT>
-void launch_pp(const AttnArgs& a, cudaStream_t st) {
+template <int HD, bool CAUSAL, bool MAT, int PE>
+void launch_pp_pe(const AttnArgs& a, cudaStream_t st) {
   using Cfg = PpCfg<HD>;
   static bool once = [] {
-    SPL_CUDA(cudaFuncSetAttribute(fa_fwd_pp<HD, CAUSAL, MAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    SPL_CUDA(cudaFuncSetAttribute(fa_fwd_pp<HD, CAUSAL, MAT, PE>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     return true;
   }();
   (void)once;
   const CUtensorMap mq = attn_seq_map(a.qkv, a.ld, a.b, a.s, a.ld, 128);
   dim3 grid((unsigned)((a.s + 255) / 256), (unsigned)(a.lh * a.b));
-  fa_fwd_pp<HD, CAUSAL, MAT><<<grid, 384, Cfg::SMEM, st>>>(mq, a);
+  fa_fwd_pp<HD, CAUSAL, MAT, PE><<<grid, 384, Cfg::SMEM, st>>>(mq, a);
   SPL_CHECK_LAUNCH();
+}
+
+// SPL_ATTN_POLY=n (0, 2, 4, 8): every n-th exponential pair of the recompute regimes' forward
+// on the FMA pipe (A/B switch; the default is the measured one)
+int poly_period() {
+  static const int pe = [] {
+    const char* e = std::getenv("SPL_ATTN_POLY");
+    const int v = e ? std::atoi(e) : kPolyDefault;
+    return (v == 2 || v == 4 || v == 8) ? v : 0;
+  }();
+  return pe;
+}
+
+template <int HD, bool CAUSAL, bool MAT>
+void launch_pp(const AttnArgs& a, cudaStream_t st) {
+  if constexpr (!MAT) {
+    switch (poly_period()) {
+      case 2: return launch_pp_pe<HD, CAUSAL, MAT, 2>(a, st);
+      case 4: return launch_pp_pe<HD, CAUSAL, MAT, 4>(a, st);
+      case 8: return launch_pp_pe<HD, CAUSAL, MAT, 8>(a, st);
+      default: break;
+    }
+  }
+  launch_pp_pe<HD, CAUSAL, MAT, 0>(a, st);
 }
 
 }  // namespace
