@@ -178,11 +178,14 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         const uint32_t qa = smem_u32(Qs + t * Cfg::TILE);
         const uint32_t kb = smem_u32(KVs + st * 2 * Cfg::TILE);
+        // descriptors built once per tile; each K step only advances the 14-bit start-address
+        // field (addresses < 256 KB: no carry out of it), one add instead of the shift / mask
+        // chain per descriptor
+        const uint64_t qd = smem_desc(qa, 16, 1024), kd = smem_desc(kb, 16, 1024);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
-          umma_bf16_w(tmem + t * 128, smem_desc(qa + off, 16, 1024), smem_desc(kb + off, 16, 1024),
-                      idesc_s, kk > 0 ? 1u : 0u);
+          const uint32_t off = ((kk >> 2) * kAtomBytes + (kk & 3) * 32) >> 4;
+          umma_bf16_w(tmem + t * 128, desc_add(qd, off), desc_add(kd, off), idesc_s, kk > 0 ? 1u : 0u);
         }
         umma_commit_w(&s_full[t]);
       };
@@ -192,10 +195,11 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(&p_full[t], j & 1);
         tc_fence_after();
         const uint32_t vb = smem_u32(KVs + st * 2 * Cfg::TILE + Cfg::TILE);
+        const uint64_t vd = smem_desc(vb, kAtomBytes, 1024);
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk)
           umma_bf16_ts_w(tmem + Cfg::O_COL + t * HD, tmem + t * 128 + kk * 8,
-                         smem_desc(vb + kk * 2048, kAtomBytes, 1024), idesc_o, (jp | kk) != 0 ? 1u : 0u);
+                         desc_add(vd, kk * (2048 >> 4)), idesc_o, (jp | kk) != 0 ? 1u : 0u);
       };
       // step u of tile t (u < PASSES·n_t): S_t(u) from stage u; in the last pass P̃_t(u)·V,
       // in MAT's first pass only the wait for the softmax to have read S_t(u)

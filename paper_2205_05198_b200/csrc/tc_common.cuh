@@ -224,6 +224,12 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
+// Advance a descriptor's start address by `units` 16-byte units (low word only: the caller
+// keeps the address inside the 14-bit field, so no carry reaches the LBO bits).
+__device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t units) {
+  return (d & 0xFFFFFFFF00000000ull) | (uint32_t)((uint32_t)d + units);
+}
+
 // kind::f16 instruction descriptor: fp32 accumulate, bf16 A/B, majorness, N>>3, M>>4.
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) |
