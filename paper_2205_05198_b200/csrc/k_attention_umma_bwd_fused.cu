@@ -226,6 +226,8 @@ __global__ void __launch_bounds__(512, 1)
       constexpr uint32_t idesc_acc = make_idesc(128, HD, false, true);
       constexpr uint32_t idesc_dq = make_idesc(128, 64, true, true);
       const uint32_t ka = smem_u32(smem + C::K_OFF), va = smem_u32(smem + C::V_OFF);
+      const uint64_t kd0 = smem_desc(ka, 16, 1024), vd0 = smem_desc(va, 16, 1024);
+      const uint64_t kdq = smem_desc(ka, C::A128, 1024);
       mbar_wait(kv_full, 0);
       auto issue_sd = [&](int it) {
         const int sb = it & 1, qs = it % NS;
@@ -235,15 +237,17 @@ __global__ void __launch_bounds__(512, 1)
         if (lane == 0) TRACE(1, it);
         tc_fence_after();
         const uint32_t qb = smem_u32(smem + C::QD_OFF + qs * 2 * C::T64), db = qb + C::T64;
+        // descriptors built once; each K step advances the start-address field (desc_add)
+        const uint64_t qd = smem_desc(qb, 16, 1024), dd = smem_desc(db, 16, 1024);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t oa = (kk >> 2) * C::A128 + (kk & 3) * 32;
-          const uint32_t ob = (kk >> 2) * C::A64 + (kk & 3) * 32;
+          const uint32_t oa = ((kk >> 2) * C::A128 + (kk & 3) * 32) >> 4;
+          const uint32_t ob = ((kk >> 2) * C::A64 + (kk & 3) * 32) >> 4;
           if constexpr (!STORED)
-            umma_bf16_w(tmem + C::S_COL + sb * 64, smem_desc(ka + oa, 16, 1024),
-                        smem_desc(qb + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
-          umma_bf16_w(tmem + C::DP_COL + sb * 64, smem_desc(va + oa, 16, 1024),
-                    smem_desc(db + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
+            umma_bf16_w(tmem + C::S_COL + sb * 64, desc_add(kd0, oa), desc_add(qd, ob), idesc_sd,
+                        kk > 0 ? 1u : 0u);
+          umma_bf16_w(tmem + C::DP_COL + sb * 64, desc_add(vd0, oa), desc_add(dd, ob), idesc_sd,
+                      kk > 0 ? 1u : 0u);
         }
         umma_commit_w(&sd_full[sb]);
       };
@@ -255,13 +259,15 @@ __global__ void __launch_bounds__(512, 1)
         if (lane == 0) TRACE(2, it);
         tc_fence_after();
         const uint32_t dsw = smem_u32(smem + C::DS_OFF + st * C::DS_BYTES);
+        const uint64_t dsd = smem_desc(dsw, 8192, 1024);
         const uint32_t qb = smem_u32(smem + C::QD_OFF + qs * 2 * C::T64), db = qb + C::T64;
+        const uint64_t dd = smem_desc(db, C::A64, 1024), qd = smem_desc(qb, C::A64, 1024);
 #pragma unroll
         for (int kk = 0; kk < 64 / 16; ++kk) {
           // dV += P̃ᵀ·dO, dK += dSᵀ·Q (A: P̃ᵀ / dSᵀ in TMEM, queries 32h.. of half h at
           // columns 32h..+16)
-          const uint64_t bdo = smem_desc(db + kk * 2048, C::A64, 1024);
-          const uint64_t bq = smem_desc(qb + kk * 2048, C::A64, 1024);
+          const uint64_t bdo = desc_add(dd, kk * (2048 >> 4));
+          const uint64_t bq = desc_add(qd, kk * (2048 >> 4));
           const uint32_t col = (uint32_t)(st * 64 + (kk >> 1) * 32 + (kk & 1) * 8);
           umma_bf16_ts_w(tmem + C::DV_COL, tmem + C::S_COL + col, bdo, idesc_acc, (it | kk) != 0 ? 1u : 0u);
           umma_bf16_ts_w(tmem + C::DK_COL, tmem + C::DP_COL + col, bq, idesc_acc, (it | kk) != 0 ? 1u : 0u);
@@ -274,8 +280,8 @@ __global__ void __launch_bounds__(512, 1)
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk)
-          umma_bf16_w(tmem + C::DQ_COL, smem_desc(ka + kk * 2048, C::A128, 1024),
-                    smem_desc(dsw + kk * 2048, 8192, 1024), idesc_dq, kk > 0 ? 1u : 0u);
+          umma_bf16_w(tmem + C::DQ_COL, desc_add(kdq, kk * (2048 >> 4)),
+                      desc_add(dsd, kk * (2048 >> 4)), idesc_dq, kk > 0 ? 1u : 0u);
         umma_commit_w(&w_free[st]);
         umma_commit_w(dq_full);
         if (lane == 0) TRACE(4, it);
