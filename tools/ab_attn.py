@@ -10,12 +10,15 @@ import torch  # noqa: E402
 
 import paper_2205_05198_b200 as spl  # noqa: E402
 
-cfg = spl.BlockConfig(64, 6144, 2048, 4, dropout_p=0.1, causal=False, seed=42)
-L = spl.SeqparLayer(cfg, 1, "selective", True, "bf16", check_finite=False)
+# AB_SHAPE: 22B (default, head_dim 96), 175B (head_dim 128), 530B (head_dim 160, t = 8 heads)
+shape = os.environ.get("AB_SHAPE", "22B")
+a_, h_, b_, t_ = {"22B": (64, 6144, 4, 1), "175B": (96, 12288, 1, 1), "530B": (128, 20480, 1, 8)}[shape]
+cfg = spl.BlockConfig(a_, h_, 2048, b_, dropout_p=0.1, causal=False, seed=42)
+L = spl.SeqparLayer(cfg, t_, "selective", True, "bf16", check_finite=False)  # t_ simulated ranks
 L.init_params(1234)
 g = torch.Generator(device="cuda:0").manual_seed(100)
-x = [(torch.rand(L.shard_shape(), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)]
-dy = [(torch.rand(L.shard_shape(), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)]
+x = [(torch.rand(L.shard_shape(), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(t_)]
+dy = [(torch.rand(L.shard_shape(), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16) for _ in range(t_)]
 L.forward(x)
 dx = L.backward(dy)
 torch.cuda.synchronize()
