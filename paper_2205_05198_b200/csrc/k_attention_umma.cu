@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
-          umma_bf16(tmem + sb * 128, smem_desc(qa + off, 16, 1024), smem_desc(kb + off, 16, 1024),
+          umma_bf16(tmem + sb * 128, desc_add(smem_desc(qa, 16, 1024), off >> 4), desc_add(smem_desc(kb, 16, 1024), off >> 4),
                     idesc_s, kk > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[sb]);
@@ -198,12 +198,12 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t vb = smem_u32(KVs + st * 2 * Cfg::TILE + Cfg::TILE);
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk) {
-          const uint64_t bd = smem_desc(vb + kk * 2048, kAtomBytes, 1024);
+          const uint64_t bd = desc_add(smem_desc(vb, kAtomBytes, 1024), kk * (2048 >> 4));
           if constexpr (PT) {  // P̃ of tile j over the first 64 columns of its S buffer
             const uint32_t ta = tmem + (uint32_t)(((base + j) & 1) * 128 + kk * 8);
             umma_bf16_ts(tmem + Cfg::O_COL, ta, bd, idesc_o, (j | kk) != 0 ? 1u : 0u);
           } else {
-            const uint64_t ad = smem_desc(pa + (kk >> 2) * kAtomBytes + (kk & 3) * 32, 16, 1024);
+            const uint64_t ad = desc_add(smem_desc(pa, 16, 1024), ((kk >> 2) * kAtomBytes + (kk & 3) * 32) >> 4);
             umma_bf16(tmem + Cfg::O_COL, ad, bd, idesc_o, (j | kk) != 0 ? 1u : 0u);
           }
         }

@@ -231,10 +231,10 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t oa = (kk >> 2) * C::A128 + (kk & 3) * 32;
           const uint32_t ob = (kk >> 2) * C::A64 + (kk & 3) * 32;
           if (!STORED)
-            umma_bf16(tmem + S_COL + sb * 64, smem_desc(ka + oa, 16, 1024), smem_desc(qb + ob, 16, 1024),
+            umma_bf16(tmem + S_COL + sb * 64, desc_add(smem_desc(ka, 16, 1024), oa >> 4), desc_add(smem_desc(qb, 16, 1024), ob >> 4),
                       idesc_sd, kk > 0 ? 1u : 0u);
-          umma_bf16(tmem + DP_COL + sb * 64, smem_desc(va + oa, 16, 1024),
-                    smem_desc(db + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
+          umma_bf16(tmem + DP_COL + sb * 64, desc_add(smem_desc(va, 16, 1024), oa >> 4),
+                    desc_add(smem_desc(db, 16, 1024), ob >> 4), idesc_sd, kk > 0 ? 1u : 0u);
         }
         umma_commit(&sd_full[sb]);
       };
@@ -253,16 +253,16 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int kk = 0; kk < 64 / 16; ++kk) {
           // dV += P̃ᵀ·dO ; dK += dSᵀ·Q  (B = dO / Q tiles read MN-major)
-          const uint64_t bdo = smem_desc(db + kk * 2048, C::A64, 1024);
-          const uint64_t bq = smem_desc(qb + kk * 2048, C::A64, 1024);
+          const uint64_t bdo = desc_add(smem_desc(db, C::A64, 1024), kk * (2048 >> 4));
+          const uint64_t bq = desc_add(smem_desc(qb, C::A64, 1024), kk * (2048 >> 4));
           if constexpr (!STORED) {  // A from TMEM: queries 32h.. of half h at columns 32h..+16
             const uint32_t col = (uint32_t)(sb * 64 + (kk >> 1) * 32 + (kk & 1) * 8);
             umma_bf16_ts(tmem + DV_COL, tmem + S_COL + col, bdo, idesc_acc, (it | kk) != 0 ? 1u : 0u);
             umma_bf16_ts(tmem + DK_COL, tmem + DP_COL + col, bq, idesc_acc, (it | kk) != 0 ? 1u : 0u);
           } else {
-            umma_bf16(tmem + DV_COL, smem_desc(pw + kk * 32, 16, 1024), bdo, idesc_acc,
+            umma_bf16(tmem + DV_COL, desc_add(smem_desc(pw, 16, 1024), kk * 2), bdo, idesc_acc,
                       (it | kk) != 0 ? 1u : 0u);
-            umma_bf16(tmem + DK_COL, smem_desc(dw + kk * 32, 16, 1024), bq, idesc_acc,
+            umma_bf16(tmem + DK_COL, desc_add(smem_desc(dw, 16, 1024), kk * 2), bq, idesc_acc,
                       (it | kk) != 0 ? 1u : 0u);
           }
         }
@@ -611,10 +611,10 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t oa = (kk >> 2) * C::A128 + (kk & 3) * 32;
           const uint32_t ob = (kk >> 2) * C::A64 + (kk & 3) * 32;
           if (!STORED)
-            umma_bf16(tmem + st * 64, smem_desc(qa + oa, 16, 1024), smem_desc(kb + ob, 16, 1024),
+            umma_bf16(tmem + st * 64, desc_add(smem_desc(qa, 16, 1024), oa >> 4), desc_add(smem_desc(kb, 16, 1024), ob >> 4),
                       idesc_sd, kk > 0 ? 1u : 0u);
-          umma_bf16(tmem + 128 + st * 64, smem_desc(da + oa, 16, 1024),
-                    smem_desc(vb + ob, 16, 1024), idesc_sd, kk > 0 ? 1u : 0u);
+          umma_bf16(tmem + 128 + st * 64, desc_add(smem_desc(da, 16, 1024), oa >> 4),
+                    desc_add(smem_desc(vb, 16, 1024), ob >> 4), idesc_sd, kk > 0 ? 1u : 0u);
         }
         umma_commit(&sd_full[st]);
       };
@@ -629,12 +629,12 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t kb = smem_u32(smem + KV_OFF + ks * 2 * C::T64);
 #pragma unroll
         for (int kk = 0; kk < 64 / 16; ++kk) {
-          const uint64_t bk = smem_desc(kb + kk * 2048, C::A64, 1024);
+          const uint64_t bk = desc_add(smem_desc(kb, C::A64, 1024), kk * (2048 >> 4));
           if constexpr (!STORED) {  // dS from TMEM: keys 32h.. of half h at columns 32h..+16
             const uint32_t col = (uint32_t)(st * 64 + (kk >> 1) * 32 + (kk & 1) * 8);
             umma_bf16_ts(tmem + DQ_COL, tmem + col, bk, idesc_acc, (it | kk) != 0 ? 1u : 0u);
           } else {
-            umma_bf16(tmem + DQ_COL, smem_desc(dsw + kk * 32, 16, 1024), bk, idesc_acc,
+            umma_bf16(tmem + DQ_COL, desc_add(smem_desc(dsw, 16, 1024), kk * 2), bk, idesc_acc,
                       (it | kk) != 0 ? 1u : 0u);
           }
         }
